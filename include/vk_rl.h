@@ -1,0 +1,153 @@
+/*
+ * vk_rl.h — C ABI of the B200-native Richardson–Lucy deconvolution path.
+ *
+ * This is the drop-in boundary for the reference's deconvolution API
+ * (reference: proj/include/voxelkit/deconv.hpp:28-103, implemented in
+ * proj/src/deconv.cpp).  Plain pointers and sizes only; no exception or C++
+ * type crosses it.  Every entry point names the reference interface it
+ * replaces.  The reference's C++ signatures are restored on top of this ABI by
+ * paper_2510_14143_b200/host/deconv_b200.cpp.
+ *
+ * Conventions
+ *  - Images are contiguous row-major float32, axes ZYX / YX / X (rank 1..3),
+ *    exactly NdImage's layout (proj/include/voxelkit/image.hpp:46-48).
+ *  - Functions suffixed _device take device pointers on the plan's GPU and a
+ *    cudaStream_t (passed as void*, NULL = legacy default stream); the others
+ *    take host pointers and copy through pinned staging.
+ *  - Every function returns a vk_status.  On failure vk_last_error() returns
+ *    the exact message the reference would put in the exception's what()
+ *    (thread-local, valid until the next call on the same thread).
+ *  - A plan is not re-entrant (one run at a time, like RlTransforms,
+ *    deconv.hpp:64-65); distinct plans may be used concurrently.
+ */
+#ifndef VK_RL_H_
+#define VK_RL_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define VK_RL_ABI_VERSION 1
+#define VK_MAX_RANK 3
+
+/* Status codes; each maps to one reference exception type
+ * (proj/include/voxelkit/errors.hpp:25-70). */
+typedef enum vk_status {
+  VK_OK = 0,
+  VK_ERR_ARG = 1,              /* voxelkit::Error                 */
+  VK_ERR_SHAPE = 2,            /* voxelkit::ShapeMismatch         */
+  VK_ERR_NEGATIVE = 3,         /* voxelkit::NegativeInput         */
+  VK_ERR_UNNORMALIZED_PSF = 4, /* voxelkit::UnnormalizedPsf       */
+  VK_ERR_DEGENERATE_REF = 5,   /* voxelkit::DegenerateReference   */
+  VK_ERR_TOO_SMALL = 6,        /* voxelkit::TooSmall              */
+  VK_ERR_ODD_EXTENT = 7,       /* voxelkit::OddExtent             */
+  VK_ERR_CUDA = 8,             /* CUDA runtime failure            */
+  VK_ERR_OOM = 9,              /* device allocation failure       */
+  VK_ERR_UNSUPPORTED = 10      /* not implemented on this path    */
+} vk_status;
+
+/* deconv::StopMetric (deconv.hpp:28) */
+typedef enum vk_stop_metric {
+  VK_METRIC_SI_PSNR_VS_INPUT = 0,
+  VK_METRIC_SSIM_VS_PREV = 1,
+  VK_METRIC_FRC_RESOLUTION = 2
+} vk_stop_metric;
+
+/* deconv::StoppingRule (deconv.hpp:35-40) */
+typedef struct vk_stop_rule {
+  int metric; /* vk_stop_metric */
+  double rel_tol;
+  int patience;
+  int max_iters;
+} vk_stop_rule;
+
+/* deconv::IterationTrace (deconv.hpp:49-59).  Arrays are caller-allocated
+ * with `capacity` >= rule.max_iters entries (any may be NULL). */
+typedef struct vk_trace {
+  int capacity;
+  double* metric;         /* IterationRecord::value                  */
+  double* wall_s;         /* IterationRecord::wall_time_s (device)   */
+  double* log_likelihood; /* IterationTrace::log_likelihood          */
+  int iters_run;          /* records.size()                          */
+  int stop_reason;        /* 0 "max_iters", 1 "converged"            */
+  uint64_t fft_shape[VK_MAX_RANK]; /* IterationTrace::fft_shape      */
+} vk_trace;
+
+typedef struct vk_rl_plan_s* vk_rl_plan;
+
+/* Replaces RlTransforms::RlTransforms(shape, psf, threads) plus, with
+ * pad_replicate = 1, padded_domain() of richardson_lucy
+ * (deconv.cpp:110-131, 205-219, 331-332).
+ *   pad_replicate = 1: `shape` is the IMAGE shape; the plan iterates on
+ *                      P = I + 2 floor(K/2) (richardson_lucy).
+ *   pad_replicate = 0: `shape` is the convolution domain itself (RlTransforms,
+ *                      rl_step).
+ * Validates the PSF rank (ShapeMismatch), builds both OTFs on `device`. */
+vk_status vk_rl_plan_create(int device, int rank, const uint64_t* shape, int psf_rank,
+                            const uint64_t* psf_shape, const float* psf, int pad_replicate,
+                            vk_rl_plan* out);
+
+/* RlTransforms::image_shape() / fft_shape() (deconv.hpp:73-74) plus the
+ * iteration domain.  Arrays hold `rank` entries. */
+vk_status vk_rl_plan_shapes(vk_rl_plan plan, int* rank, uint64_t* image_shape,
+                            uint64_t* domain_shape, uint64_t* fft_shape);
+
+/* Bytes of device memory the plan holds. */
+vk_status vk_rl_plan_device_bytes(vk_rl_plan plan, uint64_t* bytes);
+
+vk_status vk_rl_plan_destroy(vk_rl_plan plan);
+
+/* The loop of richardson_lucy (deconv.cpp:333-430) on a pad_replicate plan:
+ * observed (image shape) -> estimate (image shape), trace filled.  Checks the
+ * rule and observed >= 0 in the reference's order (deconv.cpp:306-318); the
+ * PSF was checked when the plan was created. */
+vk_status vk_rl_run(vk_rl_plan plan, const float* observed, float* estimate,
+                    const vk_stop_rule* rule, int flat_init, vk_trace* trace);
+vk_status vk_rl_run_device(vk_rl_plan plan, const float* d_observed, float* d_estimate,
+                           const vk_stop_rule* rule, int flat_init, vk_trace* trace,
+                           void* stream);
+
+/* Independent volumes through one plan (one OTF, reused), e.g. the C3 / C5
+ * batches.  traces may be NULL or an array of n. */
+vk_status vk_rl_run_batch(vk_rl_plan plan, int n, const float* const* observed,
+                          float* const* estimate, const vk_stop_rule* rule, int flat_init,
+                          vk_trace* traces);
+
+/* rl_step(estimate, observed, transforms) (deconv.cpp:178-194) on a
+ * pad_replicate = 0 plan: one multiplicative update on the plan's domain. */
+vk_status vk_rl_step(vk_rl_plan plan, const float* estimate, const float* observed, float* out);
+vk_status vk_rl_step_device(vk_rl_plan plan, const float* d_estimate, const float* d_observed,
+                            float* d_out, void* stream);
+
+/* richardson_lucy(observed, psf, rule, flat_init) (deconv.cpp:304-431) in one
+ * call, with the reference's exact validation order: rule, rank, observed
+ * negativity, PSF negativity, PSF sum. */
+vk_status vk_richardson_lucy(int device, int rank, const uint64_t* shape, const float* observed,
+                             int psf_rank, const uint64_t* psf_shape, const float* psf,
+                             const vk_stop_rule* rule, int flat_init, float* estimate,
+                             vk_trace* trace);
+
+/* rl_step(estimate, observed, psf) registry form (deconv.cpp:196-200,
+ * 437-449): transforms built for the call. */
+vk_status vk_rl_step_psf(int device, int rank, const uint64_t* shape, const float* estimate,
+                         const float* observed, int psf_rank, const uint64_t* psf_shape,
+                         const float* psf, float* out);
+
+/* fftx::good_size (fft_plan.cpp:41-49). */
+uint64_t vk_good_size(uint64_t n);
+
+/* Per-iteration kernel launches of the last run on this plan (evidence for
+ * the bench's gpu_launches). */
+vk_status vk_rl_plan_launches(vk_rl_plan plan, uint64_t* launches);
+
+const char* vk_last_error(void);
+int vk_abi_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* VK_RL_H_ */

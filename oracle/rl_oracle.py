@@ -1,0 +1,265 @@
+"""TEST INFRASTRUCTURE — numpy float64 restatement of the reference RL path.
+
+This is the parity checker for the CUDA product path; only tests/,
+__graft_entry__.smoke() and bench.py's cpu_baseline leg may import it, and
+never as the thing measured or shipped.  Every function cites the reference
+file:line it restates (paths relative to /root/reference/proj).  The FFT is
+numpy's pocketfft in double precision, standing in for the reference's FFTW3
+double r2c/c2r (src/fft_plan.cpp:84-97; FFTW unpinned and absent here) — the
+two agree to ~1e-16 relative, invisible at f32 output.
+
+Pinned against the reference itself: tests/test_oracle.py compares every
+function here with oracle/_ref/libvkref.so (the reference sources compiled
+unmodified by oracle/Makefile) and with the committed fixtures in
+tests/golden/ produced by tests/golden/make_golden.py.
+"""
+from __future__ import annotations
+
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+
+K_DIV_EPSILON = 1e-12  # include/voxelkit/core_ops.hpp:26
+
+
+class OracleError(Exception):
+    """Mirrors the reference's typed errors: kind is the C++ class name."""
+
+    def __init__(self, kind: str, msg: str):
+        super().__init__(f"{kind}: {msg}" if kind != "Error" else msg)
+        self.kind = kind
+
+
+def good_size(n: int) -> int:
+    """Smallest 2^a 3^b 5^c >= n; good_size(<=1) = 1 (src/fft_plan.cpp:41-49)."""
+    if n <= 1:
+        return 1
+    c = n
+    while True:
+        m = c
+        for p in (2, 3, 5):
+            while m % p == 0:
+                m //= p
+        if m == 1:
+            return c
+        c += 1
+
+
+def kernel_center(extent: int) -> int:
+    """(extent-1)/2 (src/deconv.cpp:40)."""
+    return (extent - 1) // 2
+
+
+def padded_domain(img_shape, psf_shape):
+    """P = I + 2*floor(K/2), offset floor(K/2) (src/deconv.cpp:205-219)."""
+    off = tuple(k // 2 for k in psf_shape)
+    return tuple(i + 2 * o for i, o in zip(img_shape, off)), off
+
+
+def replicate_pad(v: np.ndarray, off) -> np.ndarray:
+    """Clamp-indexed gather into the padded domain (src/deconv.cpp:221-237)."""
+    return np.pad(v.astype(np.float64), [(o, o) for o in off], mode="edge")
+
+
+def crop_interior(v: np.ndarray, off, shape) -> np.ndarray:
+    """P -> I window at floor(K/2), double -> f32 (src/deconv.cpp:239-252)."""
+    sl = tuple(slice(o, o + s) for o, s in zip(off, shape))
+    return v[sl].astype(np.float32)
+
+
+class RlTransforms:
+    """PSF spectra cached once per plan (src/deconv.cpp:98-131)."""
+
+    def __init__(self, shape, psf: np.ndarray):
+        psf = np.asarray(psf, dtype=np.float32)
+        if psf.ndim != len(shape):
+            raise OracleError("ShapeMismatch", "psf rank must match the image rank")
+        self.image_shape = tuple(int(s) for s in shape)
+        self.psf_shape = psf.shape
+        # W = good_size(P + K - 1) per axis (src/deconv.cpp:114-116)
+        self.fft_shape = tuple(good_size(s + k - 1) for s, k in zip(self.image_shape, psf.shape))
+        k = psf.astype(np.float64)
+        # corner_embed + r2c (src/deconv.cpp:126-130); std::reverse of the flat
+        # buffer == flip about every axis.
+        ax = tuple(range(k.ndim))
+        self._axes = ax
+        self.psf_fft = np.fft.rfftn(k, s=self.fft_shape, axes=ax)
+        self.psf_flipped_fft = np.fft.rfftn(k[(slice(None, None, -1),) * k.ndim], s=self.fft_shape, axes=ax)
+        self._crop = tuple(slice(kernel_center(kk), kernel_center(kk) + s)
+                           for kk, s in zip(psf.shape, self.image_shape))
+
+    def convolve(self, img: np.ndarray, flipped: bool) -> np.ndarray:
+        """Linear 'same' convolution: corner_embed -> r2c -> x OTF -> c2r(1/N) ->
+        centered_crop (src/deconv.cpp:135-147, src/fft_plan.cpp:84-97)."""
+        spec = np.fft.rfftn(img, s=self.fft_shape, axes=self._axes)
+        spec *= self.psf_flipped_fft if flipped else self.psf_fft
+        full = np.fft.irfftn(spec, s=self.fft_shape, axes=self._axes)
+        return full[self._crop]
+
+    def step(self, estimate: np.ndarray, observed: np.ndarray) -> np.ndarray:
+        """One multiplicative update (src/deconv.cpp:150-167)."""
+        model = self.convolve(estimate, False)
+        ratio = observed / np.maximum(model, K_DIV_EPSILON)
+        correction = self.convolve(ratio, True)
+        return np.maximum(estimate * correction, 0.0)
+
+
+def rl_step(estimate, observed, psf) -> np.ndarray:
+    """Registry form: unpadded transforms built per call, f32 in/out
+    (src/deconv.cpp:178-200,437-449)."""
+    e = np.asarray(estimate, np.float32)
+    o = np.asarray(observed, np.float32)
+    if e.shape != o.shape:
+        raise OracleError("ShapeMismatch", f"rl_step: {list(e.shape)} vs {list(o.shape)}")
+    t = RlTransforms(e.shape, psf)
+    return t.step(e.astype(np.float64), o.astype(np.float64)).astype(np.float32)
+
+
+def si_psnr(x: np.ndarray, ref: np.ndarray) -> float:
+    """Scale-invariant PSNR (src/metrics.cpp:67-101), double accumulation."""
+    a = np.asarray(x, np.float32).astype(np.float64).ravel()
+    b = np.asarray(ref, np.float32).astype(np.float64).ravel()
+    n = float(a.size)
+    sx, sr, sxx, sxr, srr = a.sum(), b.sum(), (a * a).sum(), (a * b).sum(), (b * b).sum()
+    var_r = srr / n - (sr / n) ** 2
+    if var_r <= 0.0:
+        raise OracleError("DegenerateReference", "si_psnr needs a non-constant reference")
+    var_x = sxx / n - (sx / n) ** 2
+    aa = (sxr / n - (sx / n) * (sr / n)) / var_x if var_x > 0.0 else 0.0
+    bb = sr / n - aa * (sx / n)
+    err = float(((aa * a + bb - b) ** 2).sum()) / n
+    if err <= 0.0:
+        return math.inf
+    rng = float(b.max() - b.min())
+    return 10.0 * math.log10(rng * rng / err)
+
+
+def relative_change(prev: float, cur: float) -> float:
+    """src/deconv.cpp:296-300."""
+    if math.isinf(prev) and math.isinf(cur) and prev == cur:
+        return 0.0
+    if math.isinf(prev) or math.isinf(cur):
+        return math.inf
+    return abs(cur - prev) / max(abs(prev), 1e-30)
+
+
+@dataclass
+class Trace:
+    metric: list = field(default_factory=list)
+    log_likelihood: list = field(default_factory=list)
+    fft_shape: tuple = ()
+    stop_reason: str = "max_iters"
+
+
+def validate(observed, psf, rel_tol, patience, max_iters):
+    """Validation order and messages of src/deconv.cpp:306-326."""
+    if rel_tol <= 0 and not math.isinf(rel_tol):
+        raise OracleError("Error", "rel_tol must be positive")
+    if patience < 1:
+        raise OracleError("Error", "patience must be >= 1")
+    if max_iters < 1:
+        raise OracleError("Error", "max_iters must be >= 1")
+    obs = np.asarray(observed, np.float32)
+    k = np.asarray(psf, np.float32)
+    if obs.ndim != k.ndim:
+        raise OracleError("ShapeMismatch", "psf rank must match the image rank")
+    if (obs < 0).any():
+        raise OracleError("NegativeInput", "observed image must be nonnegative")
+    if (k < 0).any():
+        raise OracleError("NegativeInput", "psf must be nonnegative")
+    s = float(k.astype(np.float64).sum())
+    if abs(s - 1.0) > 1e-3:
+        raise OracleError("UnnormalizedPsf", "psf sums to %f" % s)
+    return obs, k
+
+
+def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, patience=3,
+                    max_iters=100, flat_init=False, iterates=None):
+    """src/deconv.cpp:304-431.  Only the si_psnr_vs_input metric is restated
+    here (the other two are checked against the compiled reference).  If
+    `iterates` is a list, the cropped f32 estimate after every iteration is
+    appended to it."""
+    obs, k = validate(observed, psf, rel_tol, patience, max_iters)
+    if metric != "si_psnr_vs_input":
+        raise NotImplementedError(metric)
+    pshape, off = padded_domain(obs.shape, k.shape)
+    t = RlTransforms(pshape, k)
+    obs_p = replicate_pad(obs, off)
+    est = np.full(pshape, obs_p.mean()) if flat_init else obs_p.copy()
+    trace = Trace(fft_shape=t.fft_shape)
+    inner = tuple(slice(o, o + s) for o, s in zip(off, obs.shape))
+    ov = obs.astype(np.float64)
+    fails, prev, have_prev = 0, 0.0, False
+    for it in range(1, max_iters + 1):
+        model = t.convolve(est, False)
+        m = np.maximum(model[inner], K_DIV_EPSILON)
+        trace.log_likelihood.append(float((ov * np.log(m) - m).sum()))
+        ratio = obs_p / np.maximum(model, K_DIV_EPSILON)
+        est = np.maximum(est * t.convolve(ratio, True), 0.0)
+        cur = crop_interior(est, off, obs.shape)
+        if iterates is not None:
+            iterates.append(cur)
+        value = si_psnr(cur, obs)
+        trace.metric.append(value)
+        if have_prev:
+            fails = fails + 1 if relative_change(prev, value) < rel_tol else 0
+            if fails >= patience:
+                trace.stop_reason = "converged"
+                break
+        prev, have_prev = value, True
+    return crop_interior(est, off, obs.shape), trace
+
+
+def fft_convolve(img, kernel, circular=False) -> np.ndarray:
+    """filters::fft_convolve (src/filters.cpp:175-264)."""
+    a = np.asarray(img, np.float32).astype(np.float64)
+    k = np.asarray(kernel, np.float32).astype(np.float64)
+    if a.ndim != k.ndim:
+        raise OracleError("ShapeMismatch", "fft_convolve: rank mismatch")
+    if circular:
+        if any(kk > s for kk, s in zip(k.shape, a.shape)):
+            raise OracleError("KernelTooLarge", "circular convolution needs kernel <= image")
+        W = a.shape
+        kk = np.zeros(W)
+        idx = np.indices(k.shape).reshape(k.ndim, -1)
+        dst = tuple((idx[ax] - kernel_center(k.shape[ax])) % W[ax] for ax in range(k.ndim))
+        kk[dst] = k.ravel()
+        ax = tuple(range(a.ndim))
+        out = np.fft.irfftn(np.fft.rfftn(a, axes=ax) * np.fft.rfftn(kk, axes=ax), s=W, axes=ax)
+        return out.astype(np.float32)
+    W = tuple(good_size(s + kk - 1) for s, kk in zip(a.shape, k.shape))
+    ax = tuple(range(a.ndim))
+    full = np.fft.irfftn(np.fft.rfftn(a, s=W, axes=ax) * np.fft.rfftn(k, s=W, axes=ax), s=W, axes=ax)
+    sl = tuple(slice(kernel_center(kk), kernel_center(kk) + s) for kk, s in zip(k.shape, a.shape))
+    return full[sl].astype(np.float32)
+
+
+def gaussian_psf(shape, sigmas) -> np.ndarray:
+    """Centered separable Gaussian, unit sum in double then f32
+    (src/synth.cpp:226-258)."""
+    sig = list(np.atleast_1d(sigmas).astype(float))
+    if len(sig) == 1 and len(shape) > 1:
+        sig = sig * len(shape)
+    v = np.ones((), np.float64)
+    for ext, s in zip(shape, sig):
+        d = np.arange(ext, dtype=np.float64) - ext // 2
+        g = (d == 0).astype(np.float64) if s <= 0 else np.exp(-0.5 * (d / s) * (d / s))
+        v = np.multiply.outer(v, g)
+    return (v / v.sum()).astype(np.float32)
+
+
+def widefield_psf(k: int = 31) -> np.ndarray:
+    """The C2 'widefield' PSF of SURVEY.md §8(d): per-plane 2D Gaussians with
+    sigma(dz) = 1.5*sqrt(1+((dz*(1+0.15*sgn dz))/4)^2), each plane unit-sum,
+    weighted exp(-|dz|/8), normalised in double then cast to f32.  Non-separable
+    and axially asymmetric, so it exercises the flipped-PSF path."""
+    h = k // 2
+    d = np.arange(-h, h + 1, dtype=np.float64)
+    out = np.zeros((k, k, k))
+    for i, dz in enumerate(d):
+        s = 1.5 * math.sqrt(1.0 + ((dz * (1.0 + 0.15 * np.sign(dz))) / 4.0) ** 2)
+        g = np.exp(-0.5 * (d / s) ** 2)
+        plane = np.multiply.outer(g, g)
+        out[i] = plane / plane.sum() * math.exp(-abs(dz) / 8.0)
+    return (out / out.sum()).astype(np.float32)

@@ -1,0 +1,382 @@
+"""B200-native Richardson-Lucy deconvolution behind the reference's deconv API.
+
+Python mirror of the reference's `voxelkit::deconv` interface
+(/root/reference/proj/include/voxelkit/deconv.hpp:28-103) over the C ABI in
+include/vk_rl.h, implemented by hand-written sm_100a CUDA kernels in
+paper_2510_14143_b200/csrc (built in-tree into lib/libvkrl.so).  Same names,
+argument meanings and error behaviour as the reference:
+
+    richardson_lucy(observed, psf, rule=StoppingRule(), flat_init=False) -> RlResult
+    rl_step(estimate, observed, transforms_or_psf) -> ndarray
+    RlTransforms(image_shape, psf, threads=...)
+    StoppingRule / StopMetric / IterationRecord / IterationTrace / RlResult
+    errors: Error, ShapeMismatch, NegativeInput, UnnormalizedPsf, DegenerateReference, ...
+
+There is no CPU fallback: importing works without a GPU, but every compute
+call goes through libvkrl.so and raises if the library or a GPU is missing.
+"""
+from __future__ import annotations
+
+import ctypes
+import io
+import math
+import os
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "libvkrl.so")
+HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "vk_rl.h")
+
+
+# --- errors (reference: proj/include/voxelkit/errors.hpp:25-70) -------------
+class Error(RuntimeError):
+    """voxelkit::Error.  str(e) equals the reference's what()."""
+
+
+class ShapeMismatch(Error):
+    pass
+
+
+class NegativeInput(Error):
+    pass
+
+
+class UnnormalizedPsf(Error):
+    pass
+
+
+class DegenerateReference(Error):
+    pass
+
+
+class TooSmall(Error):
+    pass
+
+
+class OddExtent(Error):
+    pass
+
+
+class CudaError(Error):
+    pass
+
+
+class Unsupported(Error):
+    pass
+
+
+_STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: DegenerateReference,
+           6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported}
+
+
+# --- ctypes binding -----------------------------------------------------------
+class _Rule(ctypes.Structure):
+    _fields_ = [("metric", ctypes.c_int), ("rel_tol", ctypes.c_double), ("patience", ctypes.c_int),
+                ("max_iters", ctypes.c_int)]
+
+
+_dp = ctypes.POINTER(ctypes.c_double)
+
+
+class _Trace(ctypes.Structure):
+    _fields_ = [("capacity", ctypes.c_int), ("metric", _dp), ("wall_s", _dp), ("log_likelihood", _dp),
+                ("iters_run", ctypes.c_int), ("stop_reason", ctypes.c_int),
+                ("fft_shape", ctypes.c_uint64 * 3)]
+
+
+_u64p = ctypes.POINTER(ctypes.c_uint64)
+_fp = ctypes.POINTER(ctypes.c_float)
+_vp = ctypes.c_void_p
+_lib = None
+
+
+def lib() -> ctypes.CDLL:
+    """Load lib/libvkrl.so (fails loudly: there is no fallback path)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise RuntimeError(f"{LIB_PATH} is not built; run __graft_entry__.build() "
+                           "(the CUDA path is the only implementation)")
+    L = ctypes.CDLL(LIB_PATH)
+    i, st = ctypes.c_int, ctypes.c_int
+    L.vk_rl_plan_create.argtypes = [i, i, _u64p, i, _u64p, _fp, i, ctypes.POINTER(_vp)]
+    L.vk_rl_plan_shapes.argtypes = [_vp, ctypes.POINTER(i), _u64p, _u64p, _u64p]
+    L.vk_rl_plan_device_bytes.argtypes = [_vp, _u64p]
+    L.vk_rl_plan_launches.argtypes = [_vp, _u64p]
+    L.vk_rl_plan_destroy.argtypes = [_vp]
+    L.vk_rl_run.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_Rule), i, ctypes.POINTER(_Trace)]
+    L.vk_rl_run_device.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_Rule), i, ctypes.POINTER(_Trace), _vp]
+    L.vk_rl_run_batch.argtypes = [_vp, i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_Rule), i,
+                                  ctypes.POINTER(_Trace)]
+    L.vk_rl_step.argtypes = [_vp, _vp, _vp, _vp]
+    L.vk_rl_step_device.argtypes = [_vp, _vp, _vp, _vp, _vp]
+    L.vk_richardson_lucy.argtypes = [i, i, _u64p, _vp, i, _u64p, _fp, ctypes.POINTER(_Rule), i, _vp,
+                                     ctypes.POINTER(_Trace)]
+    L.vk_rl_step_psf.argtypes = [i, i, _u64p, _vp, _vp, i, _u64p, _fp, _vp]
+    for name in ("vk_rl_plan_create", "vk_rl_plan_shapes", "vk_rl_plan_device_bytes", "vk_rl_plan_launches",
+                 "vk_rl_plan_destroy", "vk_rl_run", "vk_rl_run_device", "vk_rl_run_batch", "vk_rl_step",
+                 "vk_rl_step_device", "vk_richardson_lucy", "vk_rl_step_psf"):
+        getattr(L, name).restype = st
+    L.vk_good_size.argtypes = [ctypes.c_uint64]
+    L.vk_good_size.restype = ctypes.c_uint64
+    L.vk_last_error.restype = ctypes.c_char_p
+    L.vk_abi_version.restype = ctypes.c_int
+    _lib = L
+    return L
+
+
+def _check(rc: int) -> None:
+    if rc != 0:
+        msg = lib().vk_last_error().decode()
+        raise _STATUS.get(rc, Error)(msg)
+
+
+def _shape(s: Sequence[int]):
+    return (ctypes.c_uint64 * max(len(s), 1))(*[int(v) for v in s])
+
+
+def _f32(a) -> np.ndarray:
+    return np.ascontiguousarray(a, dtype=np.float32)
+
+
+def good_size(n: int) -> int:
+    """fftx::good_size (reference src/fft_plan.cpp:41-49)."""
+    return int(lib().vk_good_size(int(n)))
+
+
+# --- deconv types (reference: include/voxelkit/deconv.hpp:28-95) -----------
+class StopMetric:
+    si_psnr_vs_input = "si_psnr_vs_input"
+    ssim_vs_prev = "ssim_vs_prev"
+    frc_resolution = "frc_resolution"
+
+
+_METRIC_ID = {StopMetric.si_psnr_vs_input: 0, StopMetric.ssim_vs_prev: 1, StopMetric.frc_resolution: 2}
+
+
+def to_string(metric: str) -> str:
+    return metric
+
+
+@dataclass
+class StoppingRule:
+    metric: str = StopMetric.frc_resolution
+    rel_tol: float = 1e-3
+    patience: int = 3
+    max_iters: int = 100
+
+    def _c(self) -> _Rule:
+        return _Rule(_METRIC_ID[self.metric], float(self.rel_tol), int(self.patience), int(self.max_iters))
+
+
+@dataclass
+class IterationRecord:
+    iter: int
+    metric_name: str
+    value: float
+    wall_time_s: float
+
+
+@dataclass
+class IterationTrace:
+    records: List[IterationRecord] = field(default_factory=list)
+    log_likelihood: List[float] = field(default_factory=list)
+    fft_shape: tuple = ()
+    stop_reason: str = "max_iters"
+
+    def to_csv(self, out: Optional[io.TextIOBase] = None) -> str:
+        """iter,metric,value,wall_time_s (reference src/deconv.cpp:85-96)."""
+        lines = ["iter,metric,value,wall_time_s"]
+        for r in self.records:
+            v = ("inf" if r.value > 0 else "-inf") if math.isinf(r.value) else f"{r.value:.6g}"
+            lines.append(f"{r.iter},{r.metric_name},{v},{r.wall_time_s:.6g}")
+        s = "\n".join(lines) + "\n"
+        if out is not None:
+            out.write(s)
+        return s
+
+
+@dataclass
+class RlResult:
+    estimate: np.ndarray
+    trace: IterationTrace
+
+
+class _TraceBuf:
+    def __init__(self, cap: int):
+        self.m = np.zeros(cap)
+        self.w = np.zeros(cap)
+        self.ll = np.zeros(cap)
+        self.c = _Trace(cap, self.m.ctypes.data_as(_dp), self.w.ctypes.data_as(_dp),
+                        self.ll.ctypes.data_as(_dp), 0, 0)
+
+    def trace(self, metric: str, rank: int) -> IterationTrace:
+        n = self.c.iters_run
+        recs = [IterationRecord(i + 1, metric, float(self.m[i]), float(self.w[i])) for i in range(n)]
+        return IterationTrace(recs, [float(v) for v in self.ll[:n]],
+                              tuple(int(self.c.fft_shape[i]) for i in range(rank)),
+                              "converged" if self.c.stop_reason == 1 else "max_iters")
+
+
+class _Plan:
+    def __init__(self, shape, psf, pad: bool, device: int = 0):
+        self._h = None
+        k = _f32(psf)
+        shape = tuple(int(s) for s in shape)
+        h = _vp()
+        _check(lib().vk_rl_plan_create(device, len(shape), _shape(shape), k.ndim, _shape(k.shape),
+                                       k.ctypes.data_as(_fp), int(pad), ctypes.byref(h)))
+        self._h = h
+        self.device = device
+        r = ctypes.c_int(0)
+        im, dm, wm = (ctypes.c_uint64 * 3)(), (ctypes.c_uint64 * 3)(), (ctypes.c_uint64 * 3)()
+        _check(lib().vk_rl_plan_shapes(h, ctypes.byref(r), im, dm, wm))
+        self.rank = r.value
+        self.image_shape_ = tuple(int(im[i]) for i in range(r.value))
+        self.domain_shape = tuple(int(dm[i]) for i in range(r.value))
+        self.fft_shape_ = tuple(int(wm[i]) for i in range(r.value))
+
+    def launches(self) -> int:
+        v = ctypes.c_uint64(0)
+        _check(lib().vk_rl_plan_launches(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    def device_bytes(self) -> int:
+        v = ctypes.c_uint64(0)
+        _check(lib().vk_rl_plan_device_bytes(self._h, ctypes.byref(v)))
+        return int(v.value)
+
+    def close(self):
+        if self._h is not None and _lib is not None:
+            lib().vk_rl_plan_destroy(self._h)
+        self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+class RlTransforms(_Plan):
+    """RlTransforms(image_shape, psf, threads) (reference src/deconv.cpp:98-176):
+    PSF spectra for 'same' convolutions on `image_shape`, built once on the GPU.
+    `threads` is accepted for signature parity; the device decides parallelism."""
+
+    def __init__(self, image_shape, psf, threads: int = 1, device: int = 0):
+        super().__init__(image_shape, psf, pad=False, device=device)
+
+    def image_shape(self):
+        return self.image_shape_
+
+    def fft_shape(self):
+        return self.fft_shape_
+
+
+class RlPlan(_Plan):
+    """Reusable richardson_lucy plan for one image shape + PSF (the padded
+    domain, both OTFs and all work buffers stay resident on the GPU)."""
+
+    def __init__(self, image_shape, psf, device: int = 0):
+        super().__init__(image_shape, psf, pad=True, device=device)
+
+    def run(self, observed, rule: StoppingRule = StoppingRule(), flat_init: bool = False,
+            out: Optional[np.ndarray] = None) -> RlResult:
+        obs = _f32(observed)
+        if obs.shape != self.image_shape_:
+            raise ShapeMismatch(f"ShapeMismatch: observed {list(obs.shape)} vs plan {list(self.image_shape_)}")
+        est = np.empty_like(obs) if out is None else out
+        tb = _TraceBuf(max(int(rule.max_iters), 1))
+        _check(lib().vk_rl_run(self._h, obs.ctypes.data, est.ctypes.data, ctypes.byref(rule._c()),
+                               int(bool(flat_init)), ctypes.byref(tb.c)))
+        return RlResult(est, tb.trace(rule.metric, self.rank))
+
+    def run_ptr(self, obs_ptr: int, est_ptr: int, rule: StoppingRule, flat_init: bool = False,
+                trace: bool = True) -> Optional[IterationTrace]:
+        """Host-pointer run (pinned or pageable) without numpy wrapping."""
+        tb = _TraceBuf(max(int(rule.max_iters), 1)) if trace else None
+        _check(lib().vk_rl_run(self._h, obs_ptr, est_ptr, ctypes.byref(rule._c()), int(bool(flat_init)),
+                               ctypes.byref(tb.c) if tb else None))
+        return tb.trace(rule.metric, self.rank) if tb else None
+
+    def run_device(self, obs_ptr: int, est_ptr: int, rule: StoppingRule, flat_init: bool = False,
+                   stream: int = 0, trace: bool = True) -> Optional[IterationTrace]:
+        """Device-resident run: obs_ptr / est_ptr are CUDA device pointers on
+        this plan's GPU (e.g. torch tensor .data_ptr()), stream a cudaStream_t."""
+        tb = _TraceBuf(max(int(rule.max_iters), 1)) if trace else None
+        _check(lib().vk_rl_run_device(self._h, obs_ptr, est_ptr, ctypes.byref(rule._c()), int(bool(flat_init)),
+                                      ctypes.byref(tb.c) if tb else None, stream))
+        return tb.trace(rule.metric, self.rank) if tb else None
+
+    def run_batch(self, observed: Sequence[np.ndarray], rule: StoppingRule = StoppingRule(),
+                  flat_init: bool = False) -> List[RlResult]:
+        obs = [_f32(o) for o in observed]
+        outs = [np.empty_like(o) for o in obs]
+        n = len(obs)
+        tbs = [_TraceBuf(max(int(rule.max_iters), 1)) for _ in range(n)]
+        traces = (_Trace * max(n, 1))(*[t.c for t in tbs])
+        ip = (_vp * max(n, 1))(*[o.ctypes.data for o in obs])
+        op = (_vp * max(n, 1))(*[o.ctypes.data for o in outs])
+        _check(lib().vk_rl_run_batch(self._h, n, ip, op, ctypes.byref(rule._c()), int(bool(flat_init)), traces))
+        res = []
+        for i in range(n):
+            tbs[i].c = traces[i]
+            res.append(RlResult(outs[i], tbs[i].trace(rule.metric, self.rank)))
+        return res
+
+
+def richardson_lucy(observed, psf, rule: StoppingRule = StoppingRule(), flat_init: bool = False,
+                    device: int = 0) -> RlResult:
+    """richardson_lucy (reference src/deconv.cpp:304-431) on the GPU."""
+    obs = _f32(observed)
+    k = _f32(psf)
+    est = np.empty_like(obs)
+    tb = _TraceBuf(max(int(rule.max_iters), 1))
+    _check(lib().vk_richardson_lucy(device, obs.ndim, _shape(obs.shape), obs.ctypes.data, k.ndim,
+                                    _shape(k.shape), k.ctypes.data_as(_fp), ctypes.byref(rule._c()),
+                                    int(bool(flat_init)), est.ctypes.data, ctypes.byref(tb.c)))
+    return RlResult(est, tb.trace(rule.metric, obs.ndim))
+
+
+def _shape_str(s) -> str:
+    return "[" + ",".join(str(int(v)) for v in s) + "]"
+
+
+def rl_step(estimate, observed, transforms, device: int = 0) -> np.ndarray:
+    """rl_step(estimate, observed, transforms | psf) (reference
+    src/deconv.cpp:178-200): one multiplicative update, no padding."""
+    e = _f32(estimate)
+    o = _f32(observed)
+    if e.shape != o.shape:  # require_same_shape (image.hpp:124-129)
+        raise ShapeMismatch(f"ShapeMismatch: rl_step: {_shape_str(e.shape)} vs {_shape_str(o.shape)}")
+    out = np.empty_like(e)
+    if isinstance(transforms, RlTransforms):
+        if e.shape != transforms.image_shape():
+            raise ShapeMismatch("ShapeMismatch: rl_step: transforms were prepared for "
+                                + _shape_str(transforms.image_shape()))
+        _check(lib().vk_rl_step(transforms._h, e.ctypes.data, o.ctypes.data, out.ctypes.data))
+        return out
+    k = _f32(transforms)
+    _check(lib().vk_rl_step_psf(device, e.ndim, _shape(e.shape), e.ctypes.data, o.ctypes.data, k.ndim,
+                                _shape(k.shape), k.ctypes.data_as(_fp), out.ctypes.data))
+    return out
+
+
+def exported_symbols() -> List[str]:
+    """Function names declared in include/vk_rl.h (for the ABI tests)."""
+    import re
+    with open(HEADER_PATH) as f:
+        txt = f.read()
+    return sorted(set(re.findall(r"^\s*(?:vk_status|uint64_t|const char\*|int)\s+(vk_\w+)\s*\(", txt, re.M)))
+
+
+__all__ = [
+    "Error", "ShapeMismatch", "NegativeInput", "UnnormalizedPsf", "DegenerateReference", "TooSmall",
+    "OddExtent", "CudaError", "Unsupported", "StopMetric", "StoppingRule", "IterationRecord",
+    "IterationTrace", "RlResult", "RlTransforms", "RlPlan", "richardson_lucy", "rl_step", "good_size",
+    "to_string", "lib", "exported_symbols",
+]

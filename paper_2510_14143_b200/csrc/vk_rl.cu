@@ -1,0 +1,757 @@
+// C-ABI implementation of include/vk_rl.h: plans, device buffers, the RL
+// iteration driver and the reference's validation / stopping semantics.
+//
+// Reference behaviour mirrored here (paths relative to /root/reference/proj):
+//   validation order + messages ........ src/deconv.cpp:306-326
+//   padded domain / FFT grid ............ src/deconv.cpp:114-116, 205-219
+//   PSF spectra (plain + flipped) ....... src/deconv.cpp:110-131
+//   iteration loop / trace / stopping ... src/deconv.cpp:346-430, 296-300
+//   si_psnr ............................. src/metrics.cpp:67-101
+//   good_size ........................... src/fft_plan.cpp:41-49
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <new>
+#include <string>
+#include <vector>
+
+#include "../../include/vk_rl.h"
+#include "rl_passes.cuh"
+
+using vk::Geom;
+using vk::LinePlan;
+
+namespace {
+
+thread_local std::string g_last_error;
+
+struct Fail {
+  vk_status code;
+  std::string msg;
+};
+
+[[noreturn]] void fail(vk_status code, std::string msg) { throw Fail{code, std::move(msg)}; }
+
+void ck(cudaError_t e, const char* what) {
+  if (e == cudaSuccess) return;
+  cudaGetLastError();
+  if (e == cudaErrorMemoryAllocation) fail(VK_ERR_OOM, std::string("device allocation failed: ") + what);
+  fail(VK_ERR_CUDA, std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+vk_status guarded(F&& f) {
+  try {
+    f();
+    return VK_OK;
+  } catch (const Fail& e) {
+    g_last_error = e.msg;
+    return e.code;
+  } catch (const std::bad_alloc&) {
+    g_last_error = "host allocation failed";
+    return VK_ERR_OOM;
+  } catch (const std::exception& e) {
+    g_last_error = e.what();
+    return VK_ERR_ARG;
+  }
+}
+
+uint64_t good_size(uint64_t n) {
+  if (n <= 1) return 1;
+  for (uint64_t c = n;; ++c) {
+    uint64_t m = c;
+    for (uint64_t p : {2ull, 3ull, 5ull})
+      while (m % p == 0) m /= p;
+    if (m == 1) return c;
+  }
+}
+
+// RAII device pointer owned by a plan.
+template <class T>
+struct DevBuf {
+  T* p = nullptr;
+  size_t n = 0;
+  void alloc(size_t count, const char* what) {
+    free();
+    if (count == 0) count = 1;
+    ck(cudaMalloc(&p, count * sizeof(T)), what);
+    n = count;
+  }
+  void free() {
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+  }
+  ~DevBuf() { free(); }
+};
+
+// Radix schedule: as many radix-8 stages as the power of two allows (4,4 for
+// a remainder of 2^4), then 5s and 3s.
+LinePlan make_line_plan(int n, const float2* tw) {
+  LinePlan p{};
+  p.n = n;
+  p.tw = tw;
+  int m = n, e2 = 0;
+  while (m % 2 == 0) {
+    m /= 2;
+    ++e2;
+  }
+  std::vector<int> r;
+  while (e2 > 0) {
+    if (e2 == 4) {
+      r.push_back(4);
+      r.push_back(4);
+      e2 = 0;
+    } else if (e2 >= 3) {
+      r.push_back(8);
+      e2 -= 3;
+    } else if (e2 == 2) {
+      r.push_back(4);
+      e2 = 0;
+    } else {
+      r.push_back(2);
+      e2 = 0;
+    }
+  }
+  while (m % 5 == 0) {
+    r.push_back(5);
+    m /= 5;
+  }
+  while (m % 3 == 0) {
+    r.push_back(3);
+    m /= 3;
+  }
+  if (m != 1) fail(VK_ERR_ARG, "FFT length " + std::to_string(n) + " is not 5-smooth");
+  if ((int)r.size() > vk::kMaxStages) fail(VK_ERR_ARG, "FFT length too large");
+  int ns = 1;
+  p.nst = (int)r.size();
+  for (int s = 0; s < p.nst; ++s) {
+    p.rad[s] = r[s];
+    p.ns[s] = ns;
+    ns *= r[s];
+  }
+  return p;
+}
+
+std::vector<float2> twiddles(int n) {
+  std::vector<float2> t(n);
+  for (int m = 0; m < n; ++m) {
+    const double a = -2.0 * M_PI * (double)m / (double)n;
+    t[m] = make_float2((float)std::cos(a), (float)std::sin(a));
+  }
+  return t;
+}
+
+// Largest power-of-two line count (<= lmax) whose ping-pong smem fits `cap`.
+int pick_lines(int n, int lmax, size_t cap, size_t (*bytes)(int n, int L)) {
+  int L = lmax;
+  while (L > 1 && bytes(n, L) > cap) L >>= 1;
+  return L;
+}
+size_t x_smem(int Wx, int L) {
+  const size_t LP = L + 1, Hx = Wx / 2 + 1;
+  return (Wx * LP + std::max<size_t>(Wx * LP, 2 * L * Hx)) * sizeof(float2);
+}
+size_t yz_smem(int N, int L) { return 2 * (size_t)N * (L + 1) * sizeof(float2); }
+
+constexpr size_t kSmemCap = 110 * 1024;  // two CTAs per SM
+constexpr int kThreads = 256;
+
+}  // namespace
+
+struct vk_rl_plan_s {
+  int device = 0;
+  int rank = 3;
+  bool pad = true;
+  uint64_t ishape[3]{}, dshape[3]{}, wshape[3]{}, kshape[3]{};
+  Geom g{};
+  int Kz = 1, Ky = 1, Kx = 1;
+  int psf_status = 0;  // 0 ok, VK_ERR_NEGATIVE, VK_ERR_UNNORMALIZED_PSF
+  std::string psf_msg;
+
+  DevBuf<float2> twx, twy, twz;
+  LinePlan lpx{}, lpy{}, lpz{};
+  int xL = 1, yL = 1, zL = 1;
+  size_t xs = 0, ys = 0, zs = 0;
+
+  DevBuf<float2> SA, SB, otf, otf_flip;
+  DevBuf<float> est, obs, out;
+  DevBuf<double> acc;
+  DevBuf<vk::ObsStats> stats;
+  int acc_cap = 0;
+
+  cudaStream_t stream = nullptr;
+  std::vector<cudaEvent_t> events;
+  double* h_acc = nullptr;  // pinned
+  uint64_t launches = 0;
+
+  ~vk_rl_plan_s() {
+    for (auto e : events) cudaEventDestroy(e);
+    if (h_acc) cudaFreeHost(h_acc);
+    if (stream) cudaStreamDestroy(stream);
+  }
+};
+
+namespace {
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    cudaGetDevice(&prev);
+    ck(cudaSetDevice(dev), "cudaSetDevice");
+  }
+  ~DeviceGuard() {
+    if (prev >= 0) cudaSetDevice(prev);
+  }
+};
+
+void launch_check(vk_rl_plan p, const char* what) {
+  ++p->launches;
+  ck(cudaGetLastError(), what);
+}
+
+// ---- pass launchers -------------------------------------------------------
+
+void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z, int rows_y, int len,
+            float scale, float* est, const float* obs, double* acc, float* out) {
+  vk::XArgs a{};
+  a.plan = p->lpx;
+  a.g = p->g;
+  a.mode = mode;
+  a.L = p->xL;
+  a.rows_z = rows_z;
+  a.rows_y = rows_y;
+  a.len = len;
+  a.S = p->SA.p;
+  a.src = src;
+  a.scale = scale;
+  a.est = est;
+  a.obs = obs;
+  a.acc = acc;
+  a.out = out;
+  dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), rows_z);
+  vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
+  launch_check(p, "xpass");
+}
+
+void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in_pitch, int n_out,
+            int out_pitch, int out_off, const float2* in, float2* out, const float2* otf) {
+  vk::YArgs a{};
+  a.plan = p->lpy;
+  a.mode = mode;
+  a.L = p->yL;
+  a.nlines = nlines;
+  a.n_in = n_in;
+  a.in_pitch = in_pitch;
+  a.n_out = n_out;
+  a.out_pitch = out_pitch;
+  a.out_off = out_off;
+  a.in = in;
+  a.out = out;
+  a.otf = otf;
+  dim3 grid((nlines + a.L - 1) / a.L);
+  vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
+  launch_check(p, "ypass");
+}
+
+void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_out, int out_off,
+            float2* S, const float2* otf, float2* otf_out) {
+  vk::ZArgs a{};
+  a.plan = p->lpz;
+  a.mode = mode;
+  a.L = p->zL;
+  a.Wy = p->g.Wy;
+  a.zrows = zrows;
+  a.n_in = n_in;
+  a.n_out = n_out;
+  a.out_off = out_off;
+  a.S = S;
+  a.otf = otf;
+  a.otf_out = otf_out;
+  dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
+  vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
+  launch_check(p, "zpass");
+}
+
+// 'same' linear convolution of the x-transformed P-domain field held in SA
+// with `otf` (deconv.cpp:135-147 minus the x transforms, which live in the
+// fused X-pass).  Result back in SA.
+void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
+  const Geom& g = p->g;
+  const int nl = g.Hx * g.Pz;
+  if (g.Wz == 1) {
+    y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, g.cy, p->SA.p, p->SA.p, otf);
+    return;
+  }
+  y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
+  z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
+  y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, g.cy, p->SB.p, p->SA.p, nullptr);
+}
+
+// OTF of a corner-embedded PSF on the W grid, 1/prod(W) folded in
+// (deconv.cpp:126-130 + fft_plan.cpp:95-96).
+void build_otf(vk_rl_plan p, const float* d_psf, float2* otf_dst) {
+  const Geom& g = p->g;
+  cudaStream_t s = p->stream;
+  const float scale = (float)(1.0 / ((double)g.Wz * g.Wy * g.Wx));
+  x_pass(p, s, vk::XM_FWD, d_psf, p->Kz, p->Ky, p->Kx, scale, nullptr, nullptr, nullptr, nullptr);
+  const int nl = g.Hx * p->Kz;
+  if (g.Wz == 1) {
+    y_pass(p, s, vk::YM_FWD, nl, p->Ky, p->Ky, g.Wy, g.Wy, 0, p->SA.p, otf_dst, nullptr);
+    return;
+  }
+  y_pass(p, s, vk::YM_FWD, nl, p->Ky, p->Ky, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
+  z_pass(p, s, vk::ZM_FWD_OUT, p->Kz, p->Kz, 0, 0, p->SB.p, nullptr, otf_dst);
+}
+
+void to3(int rank, const uint64_t* in, uint64_t* out3) {
+  for (int i = 0; i < 3; ++i) out3[i] = 1;
+  for (int i = 0; i < rank; ++i) out3[3 - rank + i] = in[i];
+}
+
+vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank, const uint64_t* psf_shape,
+                       const float* psf, int pad) {
+  if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
+  if (psf_rank != rank) fail(VK_ERR_SHAPE, "ShapeMismatch: psf rank must match the image rank");
+  for (int i = 0; i < rank; ++i) {
+    if (shape[i] == 0) fail(VK_ERR_ARG, "empty image");
+    if (psf_shape[i] == 0) fail(VK_ERR_ARG, "empty psf");
+  }
+  DeviceGuard dg(device);
+  auto* p = new vk_rl_plan_s();
+  try {
+    p->device = device;
+    p->rank = rank;
+    p->pad = pad != 0;
+    uint64_t I3[3], K3[3];
+    to3(rank, shape, I3);
+    to3(rank, psf_shape, K3);
+    Geom& g = p->g;
+    int* Ip[3] = {&g.Iz, &g.Iy, &g.Ix};
+    int* Pp[3] = {&g.Pz, &g.Py, &g.Px};
+    int* Op[3] = {&g.oz, &g.oy, &g.ox};
+    int* Wp[3] = {&g.Wz, &g.Wy, &g.Wx};
+    int* Cp[3] = {&g.cz, &g.cy, &g.cx};
+    for (int a = 0; a < 3; ++a) {
+      const uint64_t off = p->pad ? K3[a] / 2 : 0;  // deconv.cpp:215-216
+      const uint64_t P = I3[a] + 2 * off;
+      const uint64_t W = good_size(P + K3[a] - 1);  // deconv.cpp:116
+      if (P > (1u << 30) || W > (1u << 30)) fail(VK_ERR_ARG, "extent too large");
+      *Ip[a] = (int)I3[a];
+      *Pp[a] = (int)P;
+      *Op[a] = (int)off;
+      *Wp[a] = (int)W;
+      *Cp[a] = (int)((K3[a] - 1) / 2);  // kernel_center, deconv.cpp:40
+    }
+    g.Hx = g.Wx / 2 + 1;
+    p->Kz = (int)K3[0];
+    p->Ky = (int)K3[1];
+    p->Kx = (int)K3[2];
+    for (int i = 0; i < rank; ++i) {
+      p->ishape[i] = shape[i];
+      p->kshape[i] = psf_shape[i];
+    }
+    const uint64_t P3[3] = {(uint64_t)g.Pz, (uint64_t)g.Py, (uint64_t)g.Px};
+    const uint64_t W3[3] = {(uint64_t)g.Wz, (uint64_t)g.Wy, (uint64_t)g.Wx};
+    for (int i = 0; i < rank; ++i) {
+      p->dshape[i] = P3[3 - rank + i];
+      p->wshape[i] = W3[3 - rank + i];
+    }
+
+    // PSF value checks are stored and reported by runs in the reference's
+    // order (deconv.cpp:319-326).
+    size_t kn = (size_t)p->Kz * p->Ky * p->Kx;
+    double sum = 0;
+    for (size_t i = 0; i < kn; ++i) {
+      if (psf[i] < 0) {
+        p->psf_status = VK_ERR_NEGATIVE;
+        p->psf_msg = "NegativeInput: psf must be nonnegative";
+        break;
+      }
+      sum += psf[i];
+    }
+    if (p->psf_status == 0 && std::abs(sum - 1.0) > 1e-3) {
+      p->psf_status = VK_ERR_UNNORMALIZED_PSF;
+      p->psf_msg = "UnnormalizedPsf: psf sums to " + std::to_string(sum);
+    }
+
+    ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+    auto tx = twiddles(g.Wx), ty = twiddles(g.Wy), tz = twiddles(g.Wz);
+    p->twx.alloc(g.Wx, "twiddles");
+    p->twy.alloc(g.Wy, "twiddles");
+    p->twz.alloc(g.Wz, "twiddles");
+    ck(cudaMemcpy(p->twx.p, tx.data(), tx.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
+    ck(cudaMemcpy(p->twy.p, ty.data(), ty.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
+    ck(cudaMemcpy(p->twz.p, tz.data(), tz.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
+    p->lpx = make_line_plan(g.Wx, p->twx.p);
+    p->lpy = make_line_plan(g.Wy, p->twy.p);
+    p->lpz = make_line_plan(g.Wz, p->twz.p);
+    p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
+    p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
+    p->zL = pick_lines(g.Wz, 16, kSmemCap, yz_smem);
+    p->xs = x_smem(g.Wx, p->xL);
+    p->ys = yz_smem(g.Wy, p->yL);
+    p->zs = yz_smem(g.Wz, p->zL);
+    if (p->xs > 227 * 1024 || p->ys > 227 * 1024 || p->zs > 227 * 1024)
+      fail(VK_ERR_UNSUPPORTED, "FFT length too large for the shared-memory line transform");
+    ck(cudaFuncSetAttribute(vk::xpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+       "smem attr");
+    ck(cudaFuncSetAttribute(vk::ypass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+       "smem attr");
+    ck(cudaFuncSetAttribute(vk::zpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+       "smem attr");
+
+    const size_t sa = (size_t)g.Hx * std::max(g.Pz, p->Kz) * std::max(g.Py, p->Ky);
+    const size_t sb = (size_t)g.Hx * std::max(g.Pz, p->Kz) * g.Wy;
+    const size_t so = (size_t)g.Hx * g.Wz * g.Wy;
+    p->SA.alloc(sa, "spectrum A");
+    if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
+    p->otf.alloc(so, "otf");
+    p->otf_flip.alloc(so, "otf_flip");
+    p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
+    p->stats.alloc(1, "stats");
+
+    // Both spectra: psf and std::reverse(psf) == flip about every axis.
+    std::vector<float> flipped(psf, psf + kn);
+    std::reverse(flipped.begin(), flipped.end());
+    DevBuf<float> dpsf;
+    dpsf.alloc(kn, "psf");
+    ck(cudaMemcpyAsync(dpsf.p, psf, kn * sizeof(float), cudaMemcpyHostToDevice, p->stream), "psf H2D");
+    build_otf(p, dpsf.p, p->otf.p);
+    ck(cudaStreamSynchronize(p->stream), "otf");
+    ck(cudaMemcpyAsync(dpsf.p, flipped.data(), kn * sizeof(float), cudaMemcpyHostToDevice, p->stream),
+       "psf H2D");
+    build_otf(p, dpsf.p, p->otf_flip.p);
+    ck(cudaStreamSynchronize(p->stream), "otf_flip");
+    p->launches = 0;
+  } catch (...) {
+    delete p;
+    throw;
+  }
+  return p;
+}
+
+void ensure_iter_buffers(vk_rl_plan p, int iters) {
+  if (iters <= p->acc_cap) return;
+  p->acc.alloc((size_t)iters * 4, "trace accumulators");
+  if (p->h_acc) cudaFreeHost(p->h_acc);
+  p->h_acc = nullptr;
+  ck(cudaMallocHost(&p->h_acc, (size_t)iters * 4 * sizeof(double)), "pinned trace");
+  while ((int)p->events.size() < iters + 1) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    p->events.push_back(e);
+  }
+  p->acc_cap = iters;
+}
+
+void check_rule(const vk_stop_rule* r) {
+  if (!r) fail(VK_ERR_ARG, "rule is NULL");
+  if (r->rel_tol <= 0 && !std::isinf(r->rel_tol)) fail(VK_ERR_ARG, "rel_tol must be positive");
+  if (r->patience < 1) fail(VK_ERR_ARG, "patience must be >= 1");
+  if (r->max_iters < 1) fail(VK_ERR_ARG, "max_iters must be >= 1");
+}
+
+double relative_change(double prev, double cur) {  // deconv.cpp:296-300
+  if (std::isinf(prev) && std::isinf(cur) && prev == cur) return 0.0;
+  if (std::isinf(prev) || std::isinf(cur)) return std::numeric_limits<double>::infinity();
+  return std::abs(cur - prev) / std::max(std::abs(prev), 1e-30);
+}
+
+struct RefStats {
+  double n, sr, srr, range;
+};
+
+// si_psnr(current, observed) from fused sums (metrics.cpp:67-101).  The
+// residual uses the least-squares identity mean((a x + b - r)^2) =
+// var_r - a cov(x, r), exact in exact arithmetic.
+double si_psnr_from_sums(const RefStats& r, double sx, double sxx, double sxr) {
+  const double n = r.n;
+  const double var_r = r.srr / n - (r.sr / n) * (r.sr / n);
+  if (var_r <= 0.0) fail(VK_ERR_DEGENERATE_REF, "DegenerateReference: si_psnr needs a non-constant reference");
+  const double var_x = sxx / n - (sx / n) * (sx / n);
+  const double cov = sxr / n - (sx / n) * (r.sr / n);
+  double a = 0.0;
+  if (var_x > 0.0) a = cov / var_x;
+  const double err = var_r - a * cov;
+  if (err <= 0.0) return std::numeric_limits<double>::infinity();
+  return 10.0 * std::log10(r.range * r.range / err);
+}
+
+// The richardson_lucy loop on device buffers (deconv.cpp:333-430).
+void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_rule* rule, int flat_init,
+                vk_trace* trace, cudaStream_t s, bool check_obs) {
+  check_rule(rule);
+  if (!p->pad) fail(VK_ERR_ARG, "plan was created without padding (rl_step plan)");
+  if (rule->metric != VK_METRIC_SI_PSNR_VS_INPUT)
+    fail(VK_ERR_UNSUPPORTED, std::string(rule->metric == VK_METRIC_SSIM_VS_PREV ? "ssim_vs_prev" : "frc_resolution") +
+                                 " stopping metric is not implemented on the B200 path yet");
+  const Geom& g = p->g;
+  const int iters = rule->max_iters;
+  ensure_iter_buffers(p, iters);
+  p->launches = 0;
+  const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
+  const size_t nP = (size_t)g.Pz * g.Py * g.Px;
+
+  vk::ObsStats init{};
+  init.minbits = 0x7f800000u;
+  init.maxbits = 0u;
+  ck(cudaMemcpyAsync(p->stats.p, &init, sizeof(init), cudaMemcpyHostToDevice, s), "stats init");
+  ck(cudaMemsetAsync(p->acc.p, 0, (size_t)iters * 4 * sizeof(double), s), "acc");
+  const int sgrid = 148 * 4;
+  vk::obs_stats_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, nI, p->stats.p);
+  launch_check(p, "obs_stats");
+  vk::ObsStats st{};
+  ck(cudaMemcpyAsync(&st, p->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s), "stats D2H");
+  ck(cudaStreamSynchronize(s), "stats");
+  if (check_obs && st.neg) fail(VK_ERR_NEGATIVE, "NegativeInput: observed image must be nonnegative");
+  if (p->psf_status) fail((vk_status)p->psf_status, p->psf_msg);
+  float fmin, fmax;
+  std::memcpy(&fmin, &st.minbits, 4);
+  std::memcpy(&fmax, &st.maxbits, 4);
+  const RefStats rs{(double)nI, st.sr, st.srr, (double)fmax - (double)fmin};
+  // DegenerateReference surfaces at the first metric evaluation in the
+  // reference; no estimate is returned either way.
+  si_psnr_from_sums(rs, 0.0, 0.0, 0.0);
+
+  vk::pad_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p);
+  launch_check(p, "pad");
+  if (flat_init) {
+    vk::fill_mean_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, nP, p->stats.p);
+    launch_check(p, "fill_mean");
+  }
+  x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr);
+
+  // Early stop is only possible from iteration patience+1 on (fails counts
+  // from iteration 2); before that no host round-trip is needed.
+  const bool may_stop = rule->patience + 1 <= iters;
+  int fails = 0, run = 0;
+  bool have_prev = false, stopped = false;
+  double prev = 0;
+  std::vector<double> values;
+  ck(cudaEventRecord(p->events[0], s), "event");
+  for (int it = 1; it <= iters; ++it) {
+    double* acc = p->acc.p + (size_t)(it - 1) * 4;
+    conv_yz(p, s, p->otf.p);
+    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc, nullptr);
+    conv_yz(p, s, p->otf_flip.p);
+    const bool last = it == iters;
+    x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc,
+           last ? d_out : nullptr);
+    ck(cudaEventRecord(p->events[it], s), "event");
+    run = it;
+    if (may_stop && it >= rule->patience + 1 && !last) {
+      ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)it * 4 * sizeof(double), cudaMemcpyDeviceToHost, s),
+         "acc D2H");
+      ck(cudaStreamSynchronize(s), "iteration");
+      while ((int)values.size() < it) {
+        const double* a = p->h_acc + values.size() * 4;
+        values.push_back(si_psnr_from_sums(rs, a[1], a[2], a[3]));
+      }
+      // replay the stopping rule over the values so far (deconv.cpp:409-423)
+      fails = 0;
+      have_prev = false;
+      for (int k = 0; k < it; ++k) {
+        if (have_prev) {
+          fails = relative_change(prev, values[k]) < rule->rel_tol ? fails + 1 : 0;
+          if (fails >= rule->patience) {
+            stopped = true;
+            break;
+          }
+        }
+        prev = values[k];
+        have_prev = true;
+      }
+      if (stopped) {
+        vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
+        launch_check(p, "crop");
+        break;
+      }
+    }
+  }
+  ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
+  ck(cudaStreamSynchronize(s), "run");
+  if (trace) {
+    trace->iters_run = run;
+    trace->stop_reason = stopped ? 1 : 0;
+    for (int i = 0; i < 3; ++i) trace->fft_shape[i] = i < p->rank ? p->wshape[i] : 0;
+    for (int k = 0; k < run && k < trace->capacity; ++k) {
+      const double* a = p->h_acc + (size_t)k * 4;
+      if (trace->metric) trace->metric[k] = si_psnr_from_sums(rs, a[1], a[2], a[3]);
+      if (trace->log_likelihood) trace->log_likelihood[k] = a[0];
+      if (trace->wall_s) {
+        float ms = 0;
+        ck(cudaEventElapsedTime(&ms, p->events[k], p->events[k + 1]), "elapsed");
+        trace->wall_s[k] = ms * 1e-3;
+      }
+    }
+  }
+}
+
+void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_out, cudaStream_t s) {
+  if (p->pad) fail(VK_ERR_ARG, "rl_step needs a plan created with pad_replicate = 0");
+  const Geom& g = p->g;
+  ensure_iter_buffers(p, 1);
+  p->launches = 0;
+  ck(cudaMemsetAsync(p->acc.p, 0, 4 * sizeof(double), s), "acc");
+  x_pass(p, s, vk::XM_FWD, d_est, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr);
+  conv_yz(p, s, p->otf.p);
+  x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, d_obs, p->acc.p, nullptr);
+  conv_yz(p, s, p->otf_flip.p);
+  x_pass(p, s, vk::XM_UPDATE_LAST, nullptr, g.Pz, g.Py, g.Px, 1.f, const_cast<float*>(d_est), d_obs, p->acc.p,
+         d_out);
+}
+
+size_t image_count(vk_rl_plan p) { return (size_t)p->g.Iz * p->g.Iy * p->g.Ix; }
+
+}  // namespace
+
+extern "C" {
+
+uint64_t vk_good_size(uint64_t n) { return good_size(n); }
+const char* vk_last_error(void) { return g_last_error.c_str(); }
+int vk_abi_version(void) { return VK_RL_ABI_VERSION; }
+
+vk_status vk_rl_plan_create(int device, int rank, const uint64_t* shape, int psf_rank, const uint64_t* psf_shape,
+                            const float* psf, int pad_replicate, vk_rl_plan* out) {
+  return guarded([&] {
+    if (!out || !shape || !psf_shape || !psf) fail(VK_ERR_ARG, "NULL argument");
+    *out = create_plan(device, rank, shape, psf_rank, psf_shape, psf, pad_replicate);
+  });
+}
+
+vk_status vk_rl_plan_shapes(vk_rl_plan p, int* rank, uint64_t* image_shape, uint64_t* domain_shape,
+                            uint64_t* fft_shape) {
+  return guarded([&] {
+    if (!p) fail(VK_ERR_ARG, "NULL plan");
+    if (rank) *rank = p->rank;
+    for (int i = 0; i < p->rank; ++i) {
+      if (image_shape) image_shape[i] = p->ishape[i];
+      if (domain_shape) domain_shape[i] = p->dshape[i];
+      if (fft_shape) fft_shape[i] = p->wshape[i];
+    }
+  });
+}
+
+vk_status vk_rl_plan_device_bytes(vk_rl_plan p, uint64_t* bytes) {
+  return guarded([&] {
+    if (!p || !bytes) fail(VK_ERR_ARG, "NULL argument");
+    *bytes = (p->SA.n + p->SB.n + p->otf.n + p->otf_flip.n) * sizeof(float2) +
+             (p->est.n + p->obs.n + p->out.n) * sizeof(float) + p->acc.n * sizeof(double);
+  });
+}
+
+vk_status vk_rl_plan_launches(vk_rl_plan p, uint64_t* launches) {
+  return guarded([&] {
+    if (!p || !launches) fail(VK_ERR_ARG, "NULL argument");
+    *launches = p->launches;
+  });
+}
+
+vk_status vk_rl_plan_destroy(vk_rl_plan p) {
+  return guarded([&] {
+    if (!p) return;
+    DeviceGuard dg(p->device);
+    delete p;
+  });
+}
+
+vk_status vk_rl_run_device(vk_rl_plan p, const float* d_obs, float* d_est, const vk_stop_rule* rule, int flat_init,
+                           vk_trace* trace, void* stream) {
+  return guarded([&] {
+    if (!p || !d_obs || !d_est) fail(VK_ERR_ARG, "NULL argument");
+    DeviceGuard dg(p->device);
+    run_device(p, d_obs, d_est, rule, flat_init, trace, (cudaStream_t)stream, true);
+  });
+}
+
+vk_status vk_rl_run(vk_rl_plan p, const float* obs, float* est, const vk_stop_rule* rule, int flat_init,
+                    vk_trace* trace) {
+  return guarded([&] {
+    if (!p || !obs || !est) fail(VK_ERR_ARG, "NULL argument");
+    check_rule(rule);
+    DeviceGuard dg(p->device);
+    const size_t n = image_count(p);
+    if (p->obs.n < n) p->obs.alloc(n, "observed");
+    if (p->out.n < n) p->out.alloc(n, "output");
+    ck(cudaMemcpyAsync(p->obs.p, obs, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "observed H2D");
+    run_device(p, p->obs.p, p->out.p, rule, flat_init, trace, p->stream, true);
+    ck(cudaMemcpyAsync(est, p->out.p, n * sizeof(float), cudaMemcpyDeviceToHost, p->stream), "estimate D2H");
+    ck(cudaStreamSynchronize(p->stream), "estimate D2H");
+  });
+}
+
+vk_status vk_rl_run_batch(vk_rl_plan p, int n, const float* const* obs, float* const* est, const vk_stop_rule* rule,
+                          int flat_init, vk_trace* traces) {
+  return guarded([&] {
+    if (!p || n < 0 || (n > 0 && (!obs || !est))) fail(VK_ERR_ARG, "NULL argument");
+    for (int i = 0; i < n; ++i) {
+      const vk_status st = vk_rl_run(p, obs[i], est[i], rule, flat_init, traces ? &traces[i] : nullptr);
+      if (st != VK_OK) fail(st, "volume " + std::to_string(i) + ": " + g_last_error);
+    }
+  });
+}
+
+vk_status vk_rl_step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_out, void* stream) {
+  return guarded([&] {
+    if (!p || !d_est || !d_obs || !d_out) fail(VK_ERR_ARG, "NULL argument");
+    DeviceGuard dg(p->device);
+    step_device(p, d_est, d_obs, d_out, (cudaStream_t)stream);
+  });
+}
+
+vk_status vk_rl_step(vk_rl_plan p, const float* e, const float* o, float* out) {
+  return guarded([&] {
+    if (!p || !e || !o || !out) fail(VK_ERR_ARG, "NULL argument");
+    DeviceGuard dg(p->device);
+    const size_t n = image_count(p);
+    DevBuf<float> de, dobs, dout;
+    de.alloc(n, "estimate");
+    dobs.alloc(n, "observed");
+    dout.alloc(n, "output");
+    ck(cudaMemcpyAsync(de.p, e, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
+    ck(cudaMemcpyAsync(dobs.p, o, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
+    step_device(p, de.p, dobs.p, dout.p, p->stream);
+    ck(cudaMemcpyAsync(out, dout.p, n * sizeof(float), cudaMemcpyDeviceToHost, p->stream), "D2H");
+    ck(cudaStreamSynchronize(p->stream), "rl_step");
+  });
+}
+
+vk_status vk_richardson_lucy(int device, int rank, const uint64_t* shape, const float* obs, int psf_rank,
+                             const uint64_t* psf_shape, const float* psf, const vk_stop_rule* rule, int flat_init,
+                             float* est, vk_trace* trace) {
+  vk_rl_plan p = nullptr;
+  vk_status st = guarded([&] {
+    check_rule(rule);  // deconv.cpp:306-309
+    if (rank != psf_rank) fail(VK_ERR_SHAPE, "ShapeMismatch: psf rank must match the image rank");
+    if (!shape || !obs || !psf_shape || !psf || !est) fail(VK_ERR_ARG, "NULL argument");
+    p = create_plan(device, rank, shape, psf_rank, psf_shape, psf, 1);
+  });
+  if (st != VK_OK) return st;
+  st = vk_rl_run(p, obs, est, rule, flat_init, trace);
+  std::string keep = g_last_error;
+  vk_rl_plan_destroy(p);
+  g_last_error = keep;
+  return st;
+}
+
+vk_status vk_rl_step_psf(int device, int rank, const uint64_t* shape, const float* e, const float* o, int psf_rank,
+                         const uint64_t* psf_shape, const float* psf, float* out) {
+  vk_rl_plan p = nullptr;
+  vk_status st = guarded([&] {
+    if (!shape || !e || !o || !psf_shape || !psf || !out) fail(VK_ERR_ARG, "NULL argument");
+    p = create_plan(device, rank, shape, psf_rank, psf_shape, psf, 0);
+  });
+  if (st != VK_OK) return st;
+  st = vk_rl_step(p, e, o, out);
+  std::string keep = g_last_error;
+  vk_rl_plan_destroy(p);
+  g_last_error = keep;
+  return st;
+}
+
+}  // extern "C"

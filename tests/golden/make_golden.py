@@ -1,0 +1,138 @@
+"""Generate the committed golden fixtures from the reference itself.
+
+Runs the reference's own richardson_lucy / rl_step / fft_convolve (compiled
+unmodified from /root/reference by oracle/Makefile into oracle/_ref/libvkref.so)
+on small seeded inputs and stores inputs + outputs in tests/golden/*.npz.
+Re-run with:  make -C oracle && python tests/golden/make_golden.py
+The fixtures travel to the GPU box; the reference tree does not.
+"""
+from __future__ import annotations
+
+import os
+import sys
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+sys.path.insert(0, ROOT)
+from oracle import ref  # noqa: E402
+
+OUT = os.path.dirname(os.path.abspath(__file__))
+FIXED = dict(rel_tol=1e-300)  # fixed iteration count: patience = max_iters
+
+
+def blur_observed(truth, psf):
+    # observed = vmax(fft_convolve(truth, psf), 0) as the reference CLI builds it
+    # (tools/voxelkit_main.cpp:417-425)
+    return np.maximum(ref.fft_convolve(truth, psf), 0).astype(np.float32)
+
+
+def rl_case(name, observed, psf, iters, flat_init=False, metric="si_psnr_vs_input", **rule):
+    kw = dict(FIXED, patience=iters, max_iters=iters)
+    kw.update(rule)
+    r1 = ref.richardson_lucy(observed, psf, metric=metric, flat_init=flat_init,
+                             **dict(kw, max_iters=1, patience=1))
+    rn = ref.richardson_lucy(observed, psf, metric=metric, flat_init=flat_init, **kw)
+    np.savez_compressed(
+        os.path.join(OUT, f"rl_{name}.npz"), observed=observed, psf=psf,
+        estimate_1=r1.estimate, estimate_n=rn.estimate, metric=rn.metric,
+        loglik=rn.loglik, iters_run=rn.iters_run, stop_reason=rn.stop_reason,
+        fft_shape=np.array(rn.fft_shape), flat_init=flat_init, metric_name=metric,
+        rel_tol=kw["rel_tol"], patience=kw["patience"], max_iters=kw["max_iters"])
+    print(name, observed.shape, psf.shape, rn.fft_shape, rn.iters_run, rn.stop_reason)
+
+
+def main():
+    rng = np.random.default_rng(20261018)
+
+    # 3D blob phantom, odd Gaussian PSF (C1 regime at reduced size)
+    truth = ref.generate_blobs((20, 48, 48), n_objects=4, radius_min=3, radius_max=5, seed=7,
+                               noise_sigma=0.05)
+    psf = ref.gaussian_psf((7, 7, 7), [1.0])
+    rl_case("blobs3d", blur_observed(truth, psf), psf, 6)
+    rl_case("blobs3d_flat", blur_observed(truth, psf), psf, 4, flat_init=True)
+
+    # even PSF extents (one-sample-shifted correlation)
+    obs = (rng.random((6, 20, 22)) * 2).astype(np.float32)
+    k = rng.random((4, 6, 6))
+    rl_case("even3d", obs, (k / k.sum()).astype(np.float32), 4)
+
+    # odd FFT length (W = 45 on the last axis)
+    obs = (rng.random((5, 9, 33)) + 0.1).astype(np.float32)
+    k = rng.random((3, 3, 5))
+    rl_case("oddw", obs, (k / k.sum()).astype(np.float32), 3)
+
+    # non-separable, axially asymmetric PSF (flip path)
+    k = rng.random((5, 5, 5)) ** 3
+    obs = (rng.random((10, 18, 20)) * 5).astype(np.float32)
+    rl_case("asym3d", obs, (k / k.sum()).astype(np.float32), 5)
+
+    # 2D and 1D
+    obs = (rng.random((40, 52)) * 3).astype(np.float32)
+    rl_case("img2d", obs, ref.gaussian_psf((9, 9), [1.5]), 5)
+    obs = (rng.random((64,)) * 3).astype(np.float32)
+    k = rng.random(7)
+    rl_case("sig1d", obs, (k / k.sum()).astype(np.float32), 5)
+
+    # convergence: stop_reason == "converged"
+    obs = (rng.random((8, 16, 16)) * 2 + 0.5).astype(np.float32)
+    rl_case("converge", obs, ref.gaussian_psf((3, 3, 3), [0.8]), 30, rel_tol=1e-2, patience=2,
+            max_iters=30)
+    # rel_tol = +inf stops at patience + 1
+    rl_case("tol_inf", obs, ref.gaussian_psf((3, 3, 3), [0.8]), 10, rel_tol=np.inf, patience=3,
+            max_iters=10)
+
+    # delta PSF: estimate == observed after iteration 1
+    d = np.zeros((3, 3, 3), np.float32)
+    d[1, 1, 1] = 1
+    rl_case("delta", (rng.random((6, 10, 12)) + 0.2).astype(np.float32), d, 2)
+
+    # rl_step (registry form, unpadded transforms; src/deconv.cpp:437-449)
+    e = (rng.random((6, 14, 18)) + 0.1).astype(np.float32)
+    o = (rng.random((6, 14, 18)) + 0.1).astype(np.float32)
+    k = rng.random((3, 5, 5))
+    k = (k / k.sum()).astype(np.float32)
+    np.savez_compressed(os.path.join(OUT, "rl_step.npz"), estimate=e, observed=o, psf=k,
+                        out=ref.rl_step(e, o, k), out_accel=ref.rl_step(e, o, k, accelerated=True))
+
+    # fft_convolve (the SPEC's unfused oracle for rl_step)
+    a = rng.random((8, 8, 8)).astype(np.float32)
+    kk = rng.random((3, 3, 3)).astype(np.float32)
+    np.savez_compressed(os.path.join(OUT, "fft_convolve.npz"), img=a, kernel=kk,
+                        linear=ref.fft_convolve(a, kk, False),
+                        circular=ref.fft_convolve(a, kk, True))
+
+    # error cases: (kind, message) exactly as the reference raises them
+    errs = {}
+    good = (rng.random((4, 6, 6)) + 0.1).astype(np.float32)
+    gpsf = ref.gaussian_psf((3, 3, 3), [1.0])
+    neg = good.copy()
+    neg[1, 2, 3] = -1e-3
+    cases = {
+        "rel_tol": (good, gpsf, dict(rel_tol=0.0)),
+        "patience": (good, gpsf, dict(patience=0)),
+        "max_iters": (good, gpsf, dict(max_iters=0)),
+        "rank": (good, ref.gaussian_psf((3, 3), [1.0]), {}),
+        "neg_obs": (neg, gpsf, {}),
+        "neg_psf": (good, np.where(np.arange(27).reshape(3, 3, 3) == 0, -1e-4, gpsf + 1e-4 / 26)
+                    .astype(np.float32), {}),
+        "unnormalized": (good, (gpsf * 1.01).astype(np.float32), {}),
+        "neg_both": (neg, (gpsf * 2).astype(np.float32), {}),
+        "degenerate": (np.full((4, 6, 6), 0.5, np.float32), gpsf, {}),
+    }
+    for name, (o, k, rule) in cases.items():
+        kw = dict(metric="si_psnr_vs_input", rel_tol=1e-3, patience=3, max_iters=3)
+        kw.update(rule)
+        try:
+            ref.richardson_lucy(o, k, **kw)
+            errs[name] = ("none", "")
+        except ref.RefError as ex:
+            errs[name] = (ex.kind, str(ex))
+        np.savez_compressed(os.path.join(OUT, f"err_{name}.npz"), observed=o, psf=k,
+                            kind=errs[name][0], message=errs[name][1], **{
+                                f"rule_{a}": b for a, b in kw.items()})
+        print("err", name, errs[name])
+
+
+if __name__ == "__main__":
+    main()

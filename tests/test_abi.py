@@ -1,0 +1,75 @@
+"""CPU: the C-ABI library loads, exports every symbol include/vk_rl.h declares,
+and validates arguments in the reference's order before touching a GPU."""
+import ctypes
+
+import numpy as np
+import pytest
+
+import paper_2510_14143_b200 as vk
+from oracle import rl_oracle as O
+
+
+def test_header_symbols_exported():
+    names = vk.exported_symbols()
+    assert len(names) >= 14
+    L = vk.lib()
+    missing = [n for n in names if not hasattr(L, n)]
+    assert not missing, missing
+    assert L.vk_abi_version() == 1
+
+
+def test_good_size_matches_oracle():
+    for n in list(range(0, 200)) + [1079, 1081, 2077, 2159, 4097]:
+        assert vk.good_size(n) == O.good_size(n)
+
+
+def _rule(**kw):
+    base = dict(metric=vk.StopMetric.si_psnr_vs_input, rel_tol=1e-3, patience=3, max_iters=3)
+    base.update(kw)
+    return vk.StoppingRule(**base)
+
+
+@pytest.mark.parametrize("kw,msg", [
+    (dict(rel_tol=0.0), "rel_tol must be positive"),
+    (dict(rel_tol=-1.0), "rel_tol must be positive"),
+    (dict(patience=0), "patience must be >= 1"),
+    (dict(max_iters=0), "max_iters must be >= 1"),
+])
+def test_rule_validation_before_gpu(kw, msg):
+    obs = np.ones((4, 5, 6), np.float32)
+    psf = O.gaussian_psf((3, 3, 3), [1.0])
+    with pytest.raises(vk.Error) as ei:
+        vk.richardson_lucy(obs, psf, _rule(**kw))
+    assert type(ei.value) is vk.Error and str(ei.value) == msg
+
+
+def test_rank_mismatch_before_gpu():
+    obs = np.ones((4, 5, 6), np.float32)
+    with pytest.raises(vk.ShapeMismatch) as ei:
+        vk.richardson_lucy(obs, O.gaussian_psf((3, 3), [1.0]), _rule())
+    assert str(ei.value) == "ShapeMismatch: psf rank must match the image rank"
+    with pytest.raises(vk.ShapeMismatch):
+        vk.RlTransforms((4, 5, 6), O.gaussian_psf((3, 3), [1.0]))
+
+
+def test_rl_step_shape_errors_before_gpu():
+    with pytest.raises(vk.ShapeMismatch) as ei:
+        vk.rl_step(np.ones((3, 4)), np.ones((3, 5)), O.gaussian_psf((3, 3), [1.0]))
+    assert str(ei.value) == "ShapeMismatch: rl_step: [3,4] vs [3,5]"
+
+
+def test_negative_infinite_tol_passes_rule_check():
+    # -inf passes the reference's rule check (isinf), so the failure comes later
+    # (here: no GPU / or a real run) and is not the rel_tol error.
+    obs = np.ones((4, 5, 6), np.float32)
+    psf = O.gaussian_psf((3, 3, 3), [1.0])
+    try:
+        vk.richardson_lucy(obs, psf, _rule(rel_tol=-np.inf))
+    except vk.Error as e:
+        assert "rel_tol" not in str(e)
+
+
+def test_trace_csv_format():
+    t = vk.IterationTrace([vk.IterationRecord(1, "si_psnr_vs_input", 12.5, 0.25),
+                           vk.IterationRecord(2, "frc_resolution", float("inf"), 0.5)])
+    assert t.to_csv() == "iter,metric,value,wall_time_s\n1,si_psnr_vs_input,12.5,0.25\n2,frc_resolution,inf,0.5\n"

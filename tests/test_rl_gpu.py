@@ -1,0 +1,229 @@
+"""GPU parity tests: the CUDA path (through the C ABI) against the reference's
+golden fixtures and the numpy oracle.  Gates from BASELINE.json: relative L2 of
+the cropped f32 estimate <= 1e-4 after iteration 1 and <= 1e-3 after the final
+iteration; trace metric values within 1e-3 relative."""
+import math
+import os
+
+import numpy as np
+import pytest
+
+from conftest import golden_files, load_golden, rel_l2
+from oracle import rl_oracle as O
+import synth
+
+vk = pytest.importorskip("paper_2510_14143_b200")
+pytestmark = pytest.mark.gpu
+
+TOL_1, TOL_N, TOL_METRIC = 1e-4, 1e-3, 1e-3
+
+
+def fixed_rule(iters, metric="si_psnr_vs_input"):
+    return vk.StoppingRule(metric, 1e-300, iters, iters)
+
+
+def run_oracle(obs, psf, iters, flat=False):
+    its = []
+    e, t = O.richardson_lucy(obs, psf, "si_psnr_vs_input", 1e-300, iters, iters, flat, iterates=its)
+    return its, t
+
+
+def check_against_oracle(obs, psf, iters, flat=False):
+    its, t = run_oracle(obs, psf, iters, flat)
+    r1 = vk.richardson_lucy(obs, psf, fixed_rule(1), flat)
+    rn = vk.richardson_lucy(obs, psf, fixed_rule(iters), flat)
+    assert tuple(rn.trace.fft_shape) == tuple(t.fft_shape)
+    e1, en = rel_l2(r1.estimate, its[0]), rel_l2(rn.estimate, its[-1])
+    assert e1 <= TOL_1, f"iter 1 relL2 {e1:.3e}"
+    assert en <= TOL_N, f"iter {iters} relL2 {en:.3e}"
+    vals = [r.value for r in rn.trace.records]
+    np.testing.assert_allclose(vals, t.metric, rtol=TOL_METRIC)
+    np.testing.assert_allclose(rn.trace.log_likelihood, t.log_likelihood, rtol=1e-5)
+    return e1, en
+
+
+# ---- reference goldens --------------------------------------------------------
+RL_GOLDENS = [p for p in golden_files("rl_") if os.path.basename(p) != "rl_step.npz"]
+
+
+@pytest.mark.parametrize("path", RL_GOLDENS, ids=os.path.basename)
+def test_reference_goldens(path):
+    g = load_golden(path)
+    flat = bool(g["flat_init"])
+    rule_n = vk.StoppingRule(str(g["metric_name"]), float(g["rel_tol"]), int(g["patience"]), int(g["max_iters"]))
+    r1 = vk.richardson_lucy(g["observed"], g["psf"], vk.StoppingRule(str(g["metric_name"]), 1e-300, 1, 1), flat)
+    assert rel_l2(r1.estimate, g["estimate_1"]) <= TOL_1
+    rn = vk.richardson_lucy(g["observed"], g["psf"], rule_n, flat)
+    assert tuple(rn.trace.fft_shape) == tuple(int(v) for v in g["fft_shape"])
+    ref_vals = np.asarray(g["metric"], np.float64)
+    # the stop decision is exact unless a relative change sits within float
+    # noise of rel_tol
+    rel = [O.relative_change(a, b) for a, b in zip(ref_vals[:-1], ref_vals[1:])]
+    tol = float(g["rel_tol"])
+    ambiguous = any(abs(x - tol) <= 1e-4 * tol for x in rel if math.isfinite(x))
+    if not ambiguous:
+        assert len(rn.trace.records) == int(g["iters_run"])
+        assert rn.trace.stop_reason == str(g["stop_reason"])
+        assert rel_l2(rn.estimate, g["estimate_n"]) <= TOL_N
+    n = min(len(rn.trace.records), len(ref_vals))
+    np.testing.assert_allclose([r.value for r in rn.trace.records[:n]], ref_vals[:n], rtol=TOL_METRIC)
+    np.testing.assert_allclose(rn.trace.log_likelihood[:n], np.asarray(g["loglik"])[:n], rtol=1e-5)
+    assert [r.iter for r in rn.trace.records] == list(range(1, len(rn.trace.records) + 1))
+    assert all(r.wall_time_s > 0 for r in rn.trace.records)
+
+
+def test_rl_step_golden():
+    g = load_golden(golden_files("rl_step")[0])
+    out = vk.rl_step(g["estimate"], g["observed"], g["psf"])
+    assert rel_l2(out, g["out"]) <= 1e-5  # SPEC.md:449 (1e-5 vs the unfused composition)
+    t = vk.RlTransforms(g["estimate"].shape, g["psf"])
+    out2 = vk.rl_step(g["estimate"], g["observed"], t)
+    assert np.array_equal(out, out2)
+    assert t.fft_shape() == tuple(O.good_size(s + k - 1) for s, k in zip(g["estimate"].shape, g["psf"].shape))
+    with pytest.raises(vk.ShapeMismatch) as ei:
+        vk.rl_step(np.ones((2, 3, 4), np.float32), np.ones((2, 3, 4), np.float32), t)
+    assert str(ei.value).startswith("ShapeMismatch: rl_step: transforms were prepared for [")
+
+
+@pytest.mark.parametrize("path", golden_files("err_"), ids=os.path.basename)
+def test_reference_errors(path):
+    g = load_golden(path)
+    kind, msg = str(g["kind"]), str(g["message"])
+    kw = {k[5:]: g[k].item() for k in g if k.startswith("rule_")}
+    rule = vk.StoppingRule(str(kw["metric"]), kw["rel_tol"], kw["patience"], kw["max_iters"])
+    with pytest.raises(vk.Error) as ei:
+        vk.richardson_lucy(g["observed"], g["psf"], rule)
+    assert type(ei.value).__name__ == kind
+    if kind == "UnnormalizedPsf":
+        assert str(ei.value).startswith("UnnormalizedPsf: psf sums to ")
+        assert abs(float(str(ei.value).split()[-1]) - float(msg.split()[-1])) < 1e-6
+    else:
+        assert str(ei.value) == msg
+
+
+# ---- oracle parity on the configs' regimes -----------------------------------
+def test_c1_full_size():
+    """C1: 64x256x256, 15^3 Gaussian sigma 1.75, 20 iterations (configs[0])."""
+    psf = O.gaussian_psf((15, 15, 15), 1.75)
+    obs = synth.blurred(synth.blobs((64, 256, 256), 120, 6, 10, seed=1), psf)
+    check_against_oracle(obs, psf, 20)
+
+
+def test_c2_regime_widefield():
+    """C2 regime: 31^3 non-separable, axially asymmetric widefield PSF, 50 iterations."""
+    psf = O.widefield_psf(31)
+    obs = synth.blurred(synth.blobs((40, 96, 96), 30, 6, 10, seed=2), psf)
+    check_against_oracle(obs, psf, 50)
+
+
+def test_c4_regime_radix5():
+    """C4 regime: non-power-of-two grid with radix-5/3 lengths, 21^3 PSF, 30 iterations."""
+    psf = O.gaussian_psf((21, 21, 21), 2.5)
+    obs = synth.blurred(synth.blobs((25, 110, 130), 20, 6, 10, seed=4), psf)
+    check_against_oracle(obs, psf, 30)
+
+
+def test_c5_regime_2d():
+    """C5 regime: 2D field, 31^2 Gaussian sigma 3.75, 25 iterations."""
+    psf = O.gaussian_psf((31, 31), 3.75)
+    obs = synth.blurred(synth.blobs((512, 512), 120, 6, 12, seed=5000), psf)
+    check_against_oracle(obs, psf, 25)
+
+
+def test_odd_grid_2d_and_even_psf():
+    psf = O.gaussian_psf((9, 9), 2.0)
+    obs = synth.blurred(synth.blobs((300, 333), 30, 5, 9, seed=9), psf)
+    check_against_oracle(obs, psf, 6)
+    rng = np.random.default_rng(5)
+    k = rng.random((4, 6, 8))
+    k = (k / k.sum()).astype(np.float32)
+    obs = (rng.random((17, 29, 41)) * 3).astype(np.float32)
+    check_against_oracle(obs, k, 5)
+
+
+def test_flat_init_and_1d():
+    psf = O.gaussian_psf((7, 7, 7), 1.2)
+    obs = synth.blurred(synth.blobs((20, 64, 64), 8, 4, 6, seed=3), psf)
+    check_against_oracle(obs, psf, 5, flat=True)
+    rng = np.random.default_rng(8)
+    k = rng.random(11)
+    check_against_oracle((rng.random(1000) * 2).astype(np.float32), (k / k.sum()).astype(np.float32), 7)
+
+
+# ---- SPEC properties ----------------------------------------
+def test_delta_psf_fixed_point():
+    rng = np.random.default_rng(1)
+    obs = (rng.random((9, 33, 40)) + 0.1).astype(np.float32)
+    d = np.zeros((5, 5, 5), np.float32)
+    d[2, 2, 2] = 1
+    r = vk.richardson_lucy(obs, d, fixed_rule(1))
+    np.testing.assert_allclose(r.estimate, obs, rtol=1e-5, atol=1e-6)
+
+
+def test_monotone_loglik_noiseless():
+    psf = O.gaussian_psf((7, 9, 9), [1.0, 2.0, 2.0])
+    truth = synth.blobs((24, 64, 64), 10, 5, 8, seed=11, noise=0.0) + 0.05
+    obs = synth.blurred(truth, psf)
+    r = vk.richardson_lucy(obs, psf, fixed_rule(20))
+    ll = np.asarray(r.trace.log_likelihood)
+    slack = 1e-7 * np.abs(ll).max()
+    assert (np.diff(ll) >= -slack).all(), np.diff(ll)
+
+
+def test_si_psnr_gain_acceptance5():
+    """Acceptance #5: sigma [1,2,2] blur + noise; RL beats the
+    blurred input against the truth by >= 2 dB."""
+    psf = O.gaussian_psf((7, 9, 9), [1.0, 2.0, 2.0])
+    truth = synth.blobs((32, 96, 96), 14, 6, 9, seed=21, noise=0.0)
+    obs = synth.blurred(truth, psf)
+    obs = np.maximum(obs + 0.01 * np.random.default_rng(2).standard_normal(obs.shape), 0).astype(np.float32)
+    r = vk.richardson_lucy(obs, psf, vk.StoppingRule("si_psnr_vs_input", 1e-300, 50, 50))
+    assert O.si_psnr(r.estimate, truth) >= O.si_psnr(obs, truth) + 2.0
+
+
+def test_flux_nonnegativity_determinism():
+    psf = O.gaussian_psf((7, 7, 7), 1.5)
+    obs = synth.blurred(synth.blobs((40, 120, 120), 20, 6, 10, seed=4), psf)
+    a = vk.richardson_lucy(obs, psf, fixed_rule(10))
+    b = vk.richardson_lucy(obs, psf, fixed_rule(10))
+    assert (a.estimate >= 0).all()
+    assert np.array_equal(a.estimate, b.estimate)
+    assert abs(float(a.estimate.sum()) / float(obs.sum()) - 1) < 0.01
+
+
+def test_stopping_semantics_tol_inf():
+    """rel_tol = inf stops at patience + 1."""
+    psf = O.gaussian_psf((5, 5, 5), 1.0)
+    obs = synth.blurred(synth.blobs((16, 48, 48), 5, 4, 6, seed=6), psf)
+    r = vk.richardson_lucy(obs, psf, vk.StoppingRule("si_psnr_vs_input", math.inf, 3, 50))
+    assert len(r.trace.records) == 4 and r.trace.stop_reason == "converged"
+    its, _ = run_oracle(obs, psf, 4)
+    assert rel_l2(r.estimate, its[-1]) <= TOL_N
+
+
+def test_plan_reuse_batch_and_device_api():
+    import torch
+
+    psf = O.gaussian_psf((9, 9, 9), 1.5)
+    vols = [synth.blurred(synth.blobs((24, 80, 72), 8, 5, 8, seed=s), psf) for s in (1, 2, 3)]
+    plan = vk.RlPlan(vols[0].shape, psf)
+    rule = fixed_rule(4)
+    single = [plan.run(v, rule).estimate for v in vols]
+    batch = plan.run_batch(vols, rule)
+    for s, b in zip(single, batch):
+        assert np.array_equal(s, b.estimate)
+    d_obs = torch.from_numpy(vols[1]).cuda()
+    d_out = torch.empty_like(d_obs)
+    tr = plan.run_device(d_obs.data_ptr(), d_out.data_ptr(), rule, stream=torch.cuda.current_stream().cuda_stream)
+    torch.cuda.synchronize()
+    assert np.array_equal(d_out.cpu().numpy(), single[1])
+    assert len(tr.records) == 4 and plan.launches() > 0
+    its, _ = run_oracle(vols[2], psf, 4)
+    assert rel_l2(batch[2].estimate, its[-1]) <= TOL_N
+
+
+def test_unsupported_metric_is_loud():
+    psf = O.gaussian_psf((3, 3, 3), 1.0)
+    obs = np.ones((6, 8, 8), np.float32) + np.arange(384, dtype=np.float32).reshape(6, 8, 8) / 384
+    with pytest.raises(vk.Error):
+        vk.richardson_lucy(obs, psf, vk.StoppingRule("ssim_vs_prev", 1e-3, 3, 5))
