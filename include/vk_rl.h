@@ -143,6 +143,26 @@ uint64_t vk_good_size(uint64_t n);
  * the bench's gpu_launches). */
 vk_status vk_rl_plan_launches(vk_rl_plan plan, uint64_t* launches);
 
+/* Kernel kinds for per-launch profiling. */
+typedef enum vk_kernel_kind {
+  VK_KIND_X_FWD = 0,    /* x-pass: R2C of the initial estimate          */
+  VK_KIND_X_RATIO = 1,  /* x-pass: C2R -> ratio (+LL) -> R2C            */
+  VK_KIND_X_UPDATE = 2, /* x-pass: C2R -> update/clip (+metric) -> R2C  */
+  VK_KIND_Y_FWD = 3,    /* y-pass forward                               */
+  VK_KIND_Z_CONV = 4,   /* z-pass forward * OTF * inverse               */
+  VK_KIND_Y_INV = 5,    /* y-pass inverse                               */
+  VK_KIND_Y_CONV = 6,   /* y-pass forward * OTF * inverse (rank <= 2)   */
+  VK_KIND_COUNT = 7
+} vk_kernel_kind;
+
+/* Enable/disable CUDA-event timing of every launch on this plan (events are
+ * recorded on the launch stream around each kernel). */
+vk_status vk_rl_plan_profile(vk_rl_plan plan, int enable);
+/* Accumulated device ms and launch counts per kind since the last reset, and
+ * the algorithmic HBM bytes of one launch of each kind. */
+vk_status vk_rl_plan_profile_read(vk_rl_plan plan, int n_kinds, double* ms_total, uint64_t* launches,
+                                  uint64_t* alg_bytes_per_launch, int reset);
+
 const char* vk_last_error(void);
 int vk_abi_version(void);
 

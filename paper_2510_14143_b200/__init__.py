@@ -68,6 +68,8 @@ class Unsupported(Error):
     pass
 
 
+KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv")  # vk_kernel_kind
+
 _STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: DegenerateReference,
            6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported}
 
@@ -121,6 +123,10 @@ def lib() -> ctypes.CDLL:
                  "vk_rl_plan_destroy", "vk_rl_run", "vk_rl_run_device", "vk_rl_run_batch", "vk_rl_step",
                  "vk_rl_step_device", "vk_richardson_lucy", "vk_rl_step_psf"):
         getattr(L, name).restype = st
+    L.vk_rl_plan_profile.argtypes = [_vp, i]
+    L.vk_rl_plan_profile_read.argtypes = [_vp, i, _dp, _u64p, _u64p, i]
+    L.vk_rl_plan_profile.restype = st
+    L.vk_rl_plan_profile_read.restype = st
     L.vk_good_size.argtypes = [ctypes.c_uint64]
     L.vk_good_size.restype = ctypes.c_uint64
     L.vk_last_error.restype = ctypes.c_char_p
@@ -244,6 +250,19 @@ class _Plan:
         v = ctypes.c_uint64(0)
         _check(lib().vk_rl_plan_launches(self._h, ctypes.byref(v)))
         return int(v.value)
+
+    def profile(self, enable: bool = True) -> None:
+        """CUDA-event timing of every launch, by kernel kind (vk_rl_plan_profile)."""
+        _check(lib().vk_rl_plan_profile(self._h, int(bool(enable))))
+
+    def profile_read(self, reset: bool = True) -> dict:
+        """{kind: (total_ms, launches, algorithmic_bytes_per_launch)}."""
+        n = len(KERNEL_KINDS)
+        ms = (ctypes.c_double * n)()
+        cnt = (ctypes.c_uint64 * n)()
+        ab = (ctypes.c_uint64 * n)()
+        _check(lib().vk_rl_plan_profile_read(self._h, n, ms, cnt, ab, int(bool(reset))))
+        return {KERNEL_KINDS[i]: (float(ms[i]), int(cnt[i]), int(ab[i])) for i in range(n)}
 
     def device_bytes(self) -> int:
         v = ctypes.c_uint64(0)

@@ -135,7 +135,7 @@ __global__ void __launch_bounds__(256) xpass_kernel(const XArgs a) {
   extern __shared__ float2 smem[];
   const int L = a.L, LP = L + 1, Wx = a.g.Wx, Hx = a.g.Hx;
   float2* A = smem;
-  float2* B = smem + Wx * LP + 2;  // B also stages Hx*2L (<= Wx*LP + 2)
+  float2* B = smem + Wx * LP;  // B also stages Hx*2L (host sizes it as max of both)
   const int z = blockIdx.y;
   const int y0 = blockIdx.x * 2 * L;
 

@@ -189,8 +189,17 @@ struct vk_rl_plan_s {
   double* h_acc = nullptr;  // pinned
   uint64_t launches = 0;
 
+  // Optional per-launch CUDA-event timing, by kernel kind (vk_rl_plan_profile).
+  bool prof = false;
+  std::vector<cudaEvent_t> prof_pool;
+  size_t prof_used = 0;
+  std::vector<std::pair<int, size_t>> prof_pending;  // (kind, index of begin event)
+  double prof_ms[VK_KIND_COUNT]{};
+  uint64_t prof_n[VK_KIND_COUNT]{};
+
   ~vk_rl_plan_s() {
     for (auto e : events) cudaEventDestroy(e);
+    for (auto e : prof_pool) cudaEventDestroy(e);
     if (h_acc) cudaFreeHost(h_acc);
     if (stream) cudaStreamDestroy(stream);
   }
@@ -214,6 +223,37 @@ void launch_check(vk_rl_plan p, const char* what) {
   ck(cudaGetLastError(), what);
 }
 
+// Per-launch event bracketing when profiling is on (records on the launch
+// stream, so it sees exactly the kernel's device time).
+size_t prof_begin(vk_rl_plan p, cudaStream_t s) {
+  if (!p->prof) return 0;
+  while (p->prof_pool.size() < p->prof_used + 2) {
+    cudaEvent_t e;
+    ck(cudaEventCreate(&e), "event");
+    p->prof_pool.push_back(e);
+  }
+  const size_t i = p->prof_used;
+  p->prof_used += 2;
+  ck(cudaEventRecord(p->prof_pool[i], s), "event");
+  return i;
+}
+void prof_end(vk_rl_plan p, cudaStream_t s, int kind, size_t i) {
+  if (!p->prof) return;
+  ck(cudaEventRecord(p->prof_pool[i + 1], s), "event");
+  p->prof_pending.emplace_back(kind, i);
+}
+void prof_collect(vk_rl_plan p) {
+  for (auto& [kind, i] : p->prof_pending) {
+    ck(cudaEventSynchronize(p->prof_pool[i + 1]), "event sync");
+    float ms = 0;
+    ck(cudaEventElapsedTime(&ms, p->prof_pool[i], p->prof_pool[i + 1]), "elapsed");
+    p->prof_ms[kind] += ms;
+    p->prof_n[kind] += 1;
+  }
+  p->prof_pending.clear();
+  p->prof_used = 0;
+}
+
 // ---- pass launchers -------------------------------------------------------
 
 void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z, int rows_y, int len,
@@ -234,8 +274,11 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   a.acc = acc;
   a.out = out;
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), rows_z);
+  const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
+  const size_t t = prof_begin(p, s);
   vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
   launch_check(p, "xpass");
+  prof_end(p, s, kind, t);
 }
 
 void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in_pitch, int n_out,
@@ -254,8 +297,11 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   a.out = out;
   a.otf = otf;
   dim3 grid((nlines + a.L - 1) / a.L);
+  const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
+  const size_t t = prof_begin(p, s);
   vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
+  prof_end(p, s, kind, t);
 }
 
 void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_out, int out_off,
@@ -273,8 +319,10 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   a.otf = otf;
   a.otf_out = otf_out;
   dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
+  const size_t t = prof_begin(p, s);
   vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
   launch_check(p, "zpass");
+  prof_end(p, s, VK_KIND_Z_CONV, t);
 }
 
 // 'same' linear convolution of the x-transformed P-domain field held in SA
@@ -396,13 +444,14 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->xs = x_smem(g.Wx, p->xL);
     p->ys = yz_smem(g.Wy, p->yL);
     p->zs = yz_smem(g.Wz, p->zL);
-    if (p->xs > 227 * 1024 || p->ys > 227 * 1024 || p->zs > 227 * 1024)
+    constexpr size_t kMaxDyn = 227 * 1024 - 4096;  // leave room for static reduction scratch
+    if (p->xs > kMaxDyn || p->ys > kMaxDyn || p->zs > kMaxDyn)
       fail(VK_ERR_UNSUPPORTED, "FFT length too large for the shared-memory line transform");
-    ck(cudaFuncSetAttribute(vk::xpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+    ck(cudaFuncSetAttribute(vk::xpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn),
        "smem attr");
-    ck(cudaFuncSetAttribute(vk::ypass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+    ck(cudaFuncSetAttribute(vk::ypass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn),
        "smem attr");
-    ck(cudaFuncSetAttribute(vk::zpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 227 * 1024),
+    ck(cudaFuncSetAttribute(vk::zpass_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kMaxDyn),
        "smem attr");
 
     const size_t sa = (size_t)g.Hx * std::max(g.Pz, p->Kz) * std::max(g.Py, p->Ky);
@@ -575,6 +624,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
   ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
   ck(cudaStreamSynchronize(s), "run");
+  prof_collect(p);
   if (trace) {
     trace->iters_run = run;
     trace->stop_reason = stopped ? 1 : 0;
@@ -607,6 +657,26 @@ void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_
 }
 
 size_t image_count(vk_rl_plan p) { return (size_t)p->g.Iz * p->g.Iy * p->g.Ix; }
+
+// Algorithmic HBM bytes of one launch of each kernel kind: every byte the
+// kernel must move at least once (complex64 spectra in and out, the observed
+// image once, the estimate in and out, the OTF once).  SURVEY.md §8(d).
+uint64_t alg_bytes(vk_rl_plan p, int kind) {
+  const Geom& g = p->g;
+  const uint64_t Sp = (uint64_t)g.Hx * g.Pz * g.Py, Sb = (uint64_t)g.Hx * g.Pz * g.Wy;
+  const uint64_t So = (uint64_t)g.Hx * g.Wz * g.Wy;
+  const uint64_t nI = image_count(p), nP = (uint64_t)g.Pz * g.Py * g.Px;
+  switch (kind) {
+    case VK_KIND_X_FWD: return 4 * nP + 8 * Sp;
+    case VK_KIND_X_RATIO: return 16 * Sp + 4 * nI;
+    case VK_KIND_X_UPDATE: return 16 * Sp + 8 * nP + 4 * nI;
+    case VK_KIND_Y_FWD: return 8 * Sp + 8 * Sb;
+    case VK_KIND_Z_CONV: return 16 * Sb + 8 * So;
+    case VK_KIND_Y_INV: return 8 * Sb + 8 * Sp;
+    case VK_KIND_Y_CONV: return 16 * Sp + 8 * So;
+    default: return 0;
+  }
+}
 
 }  // namespace
 
@@ -649,6 +719,34 @@ vk_status vk_rl_plan_launches(vk_rl_plan p, uint64_t* launches) {
   return guarded([&] {
     if (!p || !launches) fail(VK_ERR_ARG, "NULL argument");
     *launches = p->launches;
+  });
+}
+
+vk_status vk_rl_plan_profile(vk_rl_plan p, int enable) {
+  return guarded([&] {
+    if (!p) fail(VK_ERR_ARG, "NULL plan");
+    DeviceGuard dg(p->device);
+    prof_collect(p);
+    p->prof = enable != 0;
+  });
+}
+
+vk_status vk_rl_plan_profile_read(vk_rl_plan p, int n_kinds, double* ms_total, uint64_t* launches,
+                                  uint64_t* alg_bytes_per_launch, int reset) {
+  return guarded([&] {
+    if (!p) fail(VK_ERR_ARG, "NULL plan");
+    DeviceGuard dg(p->device);
+    prof_collect(p);
+    for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k) {
+      if (ms_total) ms_total[k] = p->prof_ms[k];
+      if (launches) launches[k] = p->prof_n[k];
+      if (alg_bytes_per_launch) alg_bytes_per_launch[k] = alg_bytes(p, k);
+    }
+    if (reset)
+      for (int k = 0; k < VK_KIND_COUNT; ++k) {
+        p->prof_ms[k] = 0;
+        p->prof_n[k] = 0;
+      }
   });
 }
 

@@ -66,7 +66,14 @@ def test_reference_goldens(path):
         assert rn.trace.stop_reason == str(g["stop_reason"])
         assert rel_l2(rn.estimate, g["estimate_n"]) <= TOL_N
     n = min(len(rn.trace.records), len(ref_vals))
-    np.testing.assert_allclose([r.value for r in rn.trace.records[:n]], ref_vals[:n], rtol=TOL_METRIC)
+    ours = np.array([r.value for r in rn.trace.records[:n]])
+    # A reference value of +inf means the f64 estimate reproduced the f32
+    # observed image exactly (err == 0, metrics.cpp:97).  In f32 the FFT round
+    # trip leaves ~1e-7 relative residue, so the value is finite but far above
+    # any real-data si_psnr (documented deviation).
+    inf = np.isinf(ref_vals[:n])
+    assert (ours[inf] >= 100.0).all(), ours[inf]
+    np.testing.assert_allclose(ours[~inf], ref_vals[:n][~inf], rtol=TOL_METRIC)
     np.testing.assert_allclose(rn.trace.log_likelihood[:n], np.asarray(g["loglik"])[:n], rtol=1e-5)
     assert [r.iter for r in rn.trace.records] == list(range(1, len(rn.trace.records) + 1))
     assert all(r.wall_time_s > 0 for r in rn.trace.records)
