@@ -1,0 +1,190 @@
+// Register-resident mixed-radix FFT building blocks (compile-time lengths).
+//
+// The generic Stockham engine (fft_core.cuh) walks one radix-2..8 stage per
+// shared-memory round trip with runtime index math.  For the FFT lengths the
+// benchmark grids use, this header builds each line transform as TWO passes
+// of large register radices, N = R1 * R2 (e.g. 576 = 24*24, 1080 = 30*36):
+//
+//   pass 1 (no twiddles):   y[j*R1 + q] = DFT_R1( x[j + r*R2] )_q          j < R2
+//   pass 2 (in place):      z[j + q*R1] = DFT_R2( y[j + r*R1] * w_N^{r j} )_q  j < R1
+//
+// i.e. the Stockham recurrence with Ns = 1 then Ns = R1, so the output is in
+// natural order.  Each radix-R DFT runs entirely in registers as a nested
+// Cooley-Tukey over R = A*B with compile-time twiddles (constexpr sin/cos in
+// double, rounded once to float).  Lines are interleaved in shared memory
+// exactly as in fft_core.cuh (element i of line l at i*LP + l, LP = L + 1), so
+// a warp always touches consecutive words.  Pass-2 twiddles come from a
+// per-CTA shared table tw[m] = w_N^m (double-evaluated).
+#pragma once
+#include <cuda_runtime.h>
+
+#include <utility>
+
+#include "fft_core.cuh"
+
+namespace vk {
+namespace reg {
+
+// ---- constexpr trigonometry (double) ---------------------------------------
+constexpr double kPi = 3.14159265358979323846264338327950288;
+
+__host__ __device__ constexpr double ce_sin_series(double x) {
+  double term = x, sum = x;
+  for (int n = 1; n < 30; ++n) {
+    term *= -x * x / ((2.0 * n) * (2.0 * n + 1.0));
+    sum += term;
+  }
+  return sum;
+}
+__host__ __device__ constexpr double ce_cos_series(double x) {
+  double term = 1.0, sum = 1.0;
+  for (int n = 1; n < 30; ++n) {
+    term *= -x * x / ((2.0 * n - 1.0) * (2.0 * n));
+    sum += term;
+  }
+  return sum;
+}
+// exp(-2 pi i k / n) evaluated exactly on the octant grid, series elsewhere.
+__host__ __device__ constexpr double ce_cos2pi(long k, long n) {
+  k %= n;
+  if (k < 0) k += n;
+  // reduce to [0, n/4] using symmetries via exact integer arithmetic on 8k vs n
+  if (8 * k <= n) return ce_cos_series(2.0 * kPi * (double)k / (double)n);
+  if (4 * k <= n) return ce_sin_series(2.0 * kPi * (double)(n - 4 * k) / (4.0 * (double)n));
+  if (2 * k <= n) return -ce_cos2pi(n - 2 * k, 2 * n);  // cos(pi - a) = -cos(a), a = 2 pi (n/2 - k)/n
+  return ce_cos2pi(n - k, n);
+}
+__host__ __device__ constexpr double ce_sin2pi(long k, long n) {
+  k %= n;
+  if (k < 0) k += n;
+  if (2 * k > n) return -ce_sin2pi(n - k, n);
+  if (4 * k > n) return ce_sin2pi(n - 2 * k, 2 * n);  // sin(pi - a) = sin(a)
+  if (8 * k > n) return ce_cos_series(2.0 * kPi * (double)(n - 4 * k) / (4.0 * (double)n));
+  return ce_sin_series(2.0 * kPi * (double)k / (double)n);
+}
+
+template <int N, int K>
+struct Tw {
+  // forward twiddle exp(-2 pi i K / N)
+  static constexpr float c = (float)ce_cos2pi(K, N);
+  static constexpr float s = (float)(-ce_sin2pi(K, N));
+};
+
+// ---- static_for -------------------------------------------------------------
+template <int B, int E, class F>
+__device__ __forceinline__ void static_for(F&& f) {
+  if constexpr (B < E) {
+    f(std::integral_constant<int, B>{});
+    static_for<B + 1, E>(f);
+  }
+}
+
+// v * w_N^K (conjugated twiddle for the inverse), with exact special cases.
+template <int N, int K, bool INV>
+__device__ __forceinline__ float2 twiddle(float2 v) {
+  constexpr int k = ((K % N) + N) % N;
+  if constexpr (k == 0) {
+    return v;
+  } else if constexpr (4 * k == N) {
+    return mul_mi<INV>(v);
+  } else if constexpr (2 * k == N) {
+    return make_float2(-v.x, -v.y);
+  } else if constexpr (4 * k == 3 * N) {
+    return mul_mi<!INV>(v);
+  } else {
+    constexpr float c = Tw<N, k>::c;
+    constexpr float s = INV ? -Tw<N, k>::s : Tw<N, k>::s;
+    return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
+  }
+}
+
+// Smallest leaf factor used to split a composite radix.
+template <int R>
+__host__ __device__ constexpr int split_factor() {
+  if (R % 8 == 0 && R != 8) return 8;
+  if (R % 4 == 0 && R != 4) return 4;
+  if (R % 5 == 0 && R != 5) return 5;
+  if (R % 3 == 0 && R != 3) return 3;
+  if (R % 2 == 0 && R != 2) return 2;
+  return R;
+}
+
+// In-register DFT of compile-time size R, natural order in and out.
+template <int R, bool INV>
+__device__ __forceinline__ void rdft(float2 (&v)[R]) {
+  if constexpr (R == 1) {
+  } else if constexpr (R == 2 || R == 3 || R == 4 || R == 5 || R == 8) {
+    dft<R, INV>(v);
+  } else {
+    constexpr int A = split_factor<R>();
+    constexpr int B = R / A;
+    static_assert(A * B == R && A > 1 && B > 1, "radix must be 2^a 3^b 5^c");
+    // n = B*n1 + n2 ; k = k1 + A*k2
+    static_for<0, B>([&](auto n2c) {
+      constexpr int n2 = decltype(n2c)::value;
+      float2 u[A];
+      static_for<0, A>([&](auto n1c) { u[decltype(n1c)::value] = v[B * decltype(n1c)::value + n2]; });
+      rdft<A, INV>(u);
+      static_for<0, A>([&](auto k1c) {
+        constexpr int k1 = decltype(k1c)::value;
+        v[B * k1 + n2] = twiddle<R, n2 * k1, INV>(u[k1]);
+      });
+    });
+    float2 out[R];
+    static_for<0, A>([&](auto k1c) {
+      constexpr int k1 = decltype(k1c)::value;
+      float2 u[B];
+      static_for<0, B>([&](auto n2c) { u[decltype(n2c)::value] = v[B * k1 + decltype(n2c)::value]; });
+      rdft<B, INV>(u);
+      static_for<0, B>([&](auto k2c) { out[k1 + A * decltype(k2c)::value] = u[decltype(k2c)::value]; });
+    });
+    static_for<0, R>([&](auto i) { v[decltype(i)::value] = out[decltype(i)::value]; });
+  }
+}
+
+// Length-N twiddle table into shared memory (N <= blockDim multiple loops).
+__device__ __forceinline__ void load_twiddles(float2* tw_s, const float2* __restrict__ tw_g, int n) {
+  for (int i = threadIdx.x; i < n; i += blockDim.x) tw_s[i] = tw_g[i];
+}
+
+// In-place two-pass transform of L interleaved lines (pitch LP = L + 1) of
+// length N = R1*R2 held in `buf` (natural order in and out).  NT = blockDim.x
+// must cover every pass-1 butterfly with one thread (NT >= L*R2) so pass 1 can
+// stage its inputs in registers, sync, and overwrite in place; pass 2 reads
+// and writes the same index set per thread.  Caller syncs before.
+template <int R1, int R2, int L, int NT, bool INV>
+__device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __restrict__ tw) {
+  constexpr int LP = L + 1;
+  static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
+  {
+    const int t = threadIdx.x;
+    const int l = t % L, j = t / L;
+    const bool act = t < L * R2;
+    float2 v[R1];
+    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l]; });
+    __syncthreads();
+    if (act) {
+      rdft<R1, INV>(v);
+      static_for<0, R1>([&](auto q) { buf[(j * R1 + decltype(q)::value) * LP + l] = v[decltype(q)::value]; });
+    }
+    __syncthreads();
+  }
+#pragma unroll 1
+  for (int t = threadIdx.x; t < L * R1; t += NT) {
+    const int l = t % L, j = t / L;
+    float2 v[R2];
+    v[0] = buf[j * LP + l];
+    static_for<1, R2>([&](auto r) {
+      constexpr int rr = decltype(r)::value;
+      const float2 w = tw[rr * j];
+      const float2 x = buf[(j + rr * R1) * LP + l];
+      v[rr] = INV ? cmulc(x, w) : cmul(x, w);
+    });
+    rdft<R2, INV>(v);
+    static_for<0, R2>([&](auto q) { buf[(j + decltype(q)::value * R1) * LP + l] = v[decltype(q)::value]; });
+  }
+  __syncthreads();
+}
+
+}  // namespace reg
+}  // namespace vk

@@ -57,6 +57,7 @@ struct XArgs {
   float2* S;            // [Hx][rows_z][rows_y]
   const float* src;     // FWD: real rows [rows_z][rows_y][len]
   float scale;          // FWD: input scale
+  int xoff;             // FWD: slot of sample 0 in the line (fast path: cx, PSF: 0)
   float* est;           // UPDATE: [Pz][Py][Px]
   const float* obs;     // [Iz][Iy][Ix]
   double* acc;          // RATIO: acc[0] += LL ; UPDATE: acc[1..3] += sx, sxx, sxr
@@ -112,6 +113,8 @@ __device__ __forceinline__ void block_accumulate(double (&v)[N], double* acc) {
     }
   }
 }
+
+#ifndef VK_NO_GENERIC_KERNELS  // generic (runtime-length) kernels: defined once, in vk_rl.cu
 
 // Forward R2C of the 2L real rows packed in `in` (line l = rows l and L+l) and
 // store of both Hermitian halves into S.
@@ -384,5 +387,7 @@ __global__ void crop_kernel(const float* __restrict__ est, float* __restrict__ o
     out[i] = est[((size_t)(z + g.oz) * g.Py + (y + g.oy)) * g.Px + (x + g.ox)];
   }
 }
+
+#endif  // VK_NO_GENERIC_KERNELS
 
 }  // namespace vk

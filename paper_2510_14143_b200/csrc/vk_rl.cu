@@ -13,6 +13,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <limits>
 #include <new>
@@ -20,6 +21,7 @@
 #include <vector>
 
 #include "../../include/vk_rl.h"
+#include "fast_table.h"
 #include "rl_passes.cuh"
 
 using vk::Geom;
@@ -175,6 +177,10 @@ struct vk_rl_plan_s {
 
   DevBuf<float2> twx, twy, twz;
   LinePlan lpx{}, lpy{}, lpz{};
+  // compile-time-length kernels per axis (nullptr -> generic Stockham)
+  const vk::FastEntry* fx = nullptr;
+  const vk::FastEntry* fy = nullptr;
+  const vk::FastEntry* fz = nullptr;
   int xL = 1, yL = 1, zL = 1;
   size_t xs = 0, ys = 0, zs = 0;
 
@@ -256,13 +262,19 @@ void prof_collect(vk_rl_plan p) {
 
 // ---- pass launchers -------------------------------------------------------
 
+void launch(const void* k, dim3 grid, int nt, size_t smem, cudaStream_t s, void* arg) {
+  void* args[] = {arg};
+  ck(cudaLaunchKernel(k, grid, dim3(nt), args, smem, s), "launch");
+}
+
 void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z, int rows_y, int len,
-            float scale, float* est, const float* obs, double* acc, float* out) {
+            float scale, float* est, const float* obs, double* acc, float* out, int xoff = 0) {
   vk::XArgs a{};
   a.plan = p->lpx;
   a.g = p->g;
   a.mode = mode;
-  a.L = p->xL;
+  a.L = p->fx ? p->fx->Lx : p->xL;
+  a.xoff = xoff;
   a.rows_z = rows_z;
   a.rows_y = rows_y;
   a.len = len;
@@ -276,7 +288,10 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), rows_z);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
-  vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
+  if (p->fx)
+    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_x, s, &a);
+  else
+    vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
   launch_check(p, "xpass");
   prof_end(p, s, kind, t);
 }
@@ -286,7 +301,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   vk::YArgs a{};
   a.plan = p->lpy;
   a.mode = mode;
-  a.L = p->yL;
+  a.L = p->fy ? p->fy->Lx : p->yL;
   a.nlines = nlines;
   a.n_in = n_in;
   a.in_pitch = in_pitch;
@@ -299,7 +314,10 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   dim3 grid((nlines + a.L - 1) / a.L);
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
-  vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
+  if (p->fy)
+    launch(p->fy->yk, grid, p->fy->NTx, p->fy->smem_x, s, &a);
+  else
+    vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
   prof_end(p, s, kind, t);
 }
@@ -309,7 +327,7 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   vk::ZArgs a{};
   a.plan = p->lpz;
   a.mode = mode;
-  a.L = p->zL;
+  a.L = p->fz ? p->fz->Lz : p->zL;
   a.Wy = p->g.Wy;
   a.zrows = zrows;
   a.n_in = n_in;
@@ -320,7 +338,10 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   a.otf_out = otf_out;
   dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
   const size_t t = prof_begin(p, s);
-  vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
+  if (p->fz)
+    launch(p->fz->zk, grid, p->fz->NTz, p->fz->smem_z, s, &a);
+  else
+    vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
   launch_check(p, "zpass");
   prof_end(p, s, VK_KIND_Z_CONV, t);
 }
@@ -438,6 +459,14 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->lpx = make_line_plan(g.Wx, p->twx.p);
     p->lpy = make_line_plan(g.Wy, p->twy.p);
     p->lpz = make_line_plan(g.Wz, p->twz.p);
+    const char* gen = std::getenv("VK_RL_GENERIC");
+    if (!(gen && gen[0] == '1')) {
+      static const cudaError_t attr = vk::fast_init_attributes();
+      ck(attr, "fast kernel attributes");
+      p->fx = vk::fast_lookup(g.Wx);
+      p->fy = vk::fast_lookup(g.Wy);
+      p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
+    }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
     p->zL = pick_lines(g.Wz, 16, kSmemCap, yz_smem);
@@ -475,6 +504,11 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     ck(cudaMemcpyAsync(dpsf.p, flipped.data(), kn * sizeof(float), cudaMemcpyHostToDevice, p->stream),
        "psf H2D");
     build_otf(p, dpsf.p, p->otf_flip.p);
+    if (p->fx && g.cx != 0) {  // the fast x-pass keeps rows at [cx, cx+Px): crop as a phase ramp
+      const size_t plane = (size_t)g.Wz * g.Wy;
+      ck(vk::launch_otf_ramp(p->otf.p, g.Hx, plane, g.Wx, g.cx, p->stream), "otf ramp");
+      ck(vk::launch_otf_ramp(p->otf_flip.p, g.Hx, plane, g.Wx, g.cx, p->stream), "otf ramp");
+    }
     ck(cudaStreamSynchronize(p->stream), "otf_flip");
     p->launches = 0;
   } catch (...) {
@@ -573,7 +607,8 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     vk::fill_mean_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, nP, p->stats.p);
     launch_check(p, "fill_mean");
   }
-  x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr);
+  x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr,
+         p->fx ? g.cx : 0);
 
   // Early stop is only possible from iteration patience+1 on (fails counts
   // from iteration 2); before that no host round-trip is needed.
@@ -648,7 +683,7 @@ void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_
   ensure_iter_buffers(p, 1);
   p->launches = 0;
   ck(cudaMemsetAsync(p->acc.p, 0, 4 * sizeof(double), s), "acc");
-  x_pass(p, s, vk::XM_FWD, d_est, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr);
+  x_pass(p, s, vk::XM_FWD, d_est, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr, p->fx ? g.cx : 0);
   conv_yz(p, s, p->otf.p);
   x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, d_obs, p->acc.p, nullptr);
   conv_yz(p, s, p->otf_flip.p);

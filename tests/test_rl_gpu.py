@@ -157,6 +157,60 @@ def test_flat_init_and_1d():
     check_against_oracle((rng.random(1000) * 2).astype(np.float32), (k / k.sum()).astype(np.float32), 7)
 
 
+# ---- compile-time-length (fast) kernels vs oracle and vs the generic path -----
+FAST_CASES = {
+    # name: (image shape, psf builder) chosen so the FFT grid hits table lengths
+    "z192_widefield": ((128, 40, 44), lambda: O.widefield_psf(31)),                  # W = 192 x 100 x 108
+    "z144_x80": ((100, 40, 40), lambda: O.gaussian_psf((21, 21, 21), 2.5)),          # W = 144 x 80 x 80
+    "xy576_2d": ((512, 512), lambda: O.gaussian_psf((31, 31), 3.75)),               # W = 576 x 576
+    "xy1080_2d": ((1000, 1000), lambda: O.gaussian_psf((21, 21), 2.5)),             # W = 1080 x 1080
+    "xy2160_2d": ((2048, 2048), lambda: O.gaussian_psf((31, 31), 3.75)),            # W = 2160 x 2160 (C5 field)
+    "c1_grid": ((64, 256, 256), lambda: O.gaussian_psf((15, 15, 15), 1.75)),        # W = 96 x 288 x 288
+    "xy256": ((30, 196, 196), lambda: O.gaussian_psf((15, 31, 31), [2.0, 3.0, 3.0])),  # W = 60 x 256 x 256
+}
+
+
+def _generic(fn):
+    old = os.environ.get("VK_RL_GENERIC")
+    os.environ["VK_RL_GENERIC"] = "1"
+    try:
+        return fn()
+    finally:
+        if old is None:
+            del os.environ["VK_RL_GENERIC"]
+        else:
+            os.environ["VK_RL_GENERIC"] = old
+
+
+@pytest.mark.parametrize("name", sorted(FAST_CASES))
+def test_fast_lengths_vs_oracle_and_generic(name):
+    shape, mk = FAST_CASES[name]
+    psf = mk()
+    obs = synth.blurred(synth.blobs(shape, max(4, int(np.prod(shape)) // 40000), 5, 9, seed=len(name)), psf)
+    iters = 3
+    its, t = run_oracle(obs, psf, iters)
+    fast = vk.richardson_lucy(obs, psf, fixed_rule(iters))
+    gen = _generic(lambda: vk.richardson_lucy(obs, psf, fixed_rule(iters)))
+    assert tuple(fast.trace.fft_shape) == tuple(t.fft_shape)
+    assert rel_l2(fast.estimate, its[-1]) <= TOL_1
+    assert rel_l2(gen.estimate, its[-1]) <= TOL_1
+    assert rel_l2(fast.estimate, gen.estimate) <= 1e-5
+    r1 = vk.richardson_lucy(obs, psf, fixed_rule(1))
+    assert rel_l2(r1.estimate, its[0]) <= TOL_1
+
+
+def test_c2_full_size_first_iterations():
+    """C2 at full size (128x512x512, 31^3 widefield): the benchmark's own grid
+    (192 x 576 x 576) through the fast kernels, 2 iterations vs the oracle."""
+    psf = O.widefield_psf(31)
+    obs = synth.blurred(synth.blobs((128, 512, 512), 600, 6, 10, seed=2), psf)
+    its, t = run_oracle(obs, psf, 2)
+    r = vk.richardson_lucy(obs, psf, fixed_rule(2))
+    assert tuple(r.trace.fft_shape) == (192, 576, 576)
+    assert rel_l2(r.estimate, its[-1]) <= TOL_1
+    np.testing.assert_allclose([x.value for x in r.trace.records], t.metric, rtol=TOL_METRIC)
+
+
 # ---- SPEC properties (SPEC.md:438-454) ----------------------------------------
 def test_delta_psf_fixed_point():
     rng = np.random.default_rng(1)
