@@ -12,18 +12,17 @@ namespace {
 
 template <int R1, int R2, int LX, int LZ>
 FastEntry make_entry() {
-  using CX = FastCfg<R1, R2, LX>;
-  using CZ = FastCfg<R1, R2, LZ>;
   FastEntry e{};
   e.N = R1 * R2;
   e.Lx = LX;
-  e.NTx = CX::NT;
-  e.smem_x = CX::smem;
+  e.NTx = FastCfg<R1, R2, LX>::NT;
+  e.smem_x = FastCfg<R1, R2, LX>::smem;
+  e.smem_yconv = FastCfg<R1, R2, LX, true>::smem;
   e.xk = (const void*)xpass_fast<R1, R2, LX>;
   e.yk = (const void*)ypass_fast<R1, R2, LX>;
   e.Lz = LZ;
-  e.NTz = CZ::NT;
-  e.smem_z = CZ::smem;
+  e.NTz = FastCfg<R1, R2, LZ, true>::NT;
+  e.smem_z = FastCfg<R1, R2, LZ, true>::smem;
   e.zk = (const void*)zpass_fast<R1, R2, LZ>;
   return e;
 }
@@ -34,7 +33,7 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16>(),  // 192
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 16, 8>(),   // 576
+    make_entry<24, 24, 8, 8>(),    // 576
     make_entry<30, 36, 8, 4>(),    // 1080
     make_entry<45, 48, 4, 2>(),    // 2160
 };
@@ -51,17 +50,15 @@ cudaError_t fast_init_attributes() {
   for (const auto& e : kTable) {
     cudaError_t r;
     if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_x))) return r;
-    if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_x))) return r;
+    if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yconv))) return r;
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
   }
   return cudaSuccess;
 }
 
-}  // namespace vk
-
-namespace vk {
 cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, cudaStream_t s) {
   otf_ramp_kernel<<<148 * 8, 256, 0, s>>>(otf, Hx, plane, Wx, cx);
   return cudaGetLastError();
 }
+
 }  // namespace vk

@@ -315,7 +315,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
   if (p->fy)
-    launch(p->fy->yk, grid, p->fy->NTx, p->fy->smem_x, s, &a);
+    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_x, s, &a);
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
