@@ -11,10 +11,14 @@
 // i.e. the Stockham recurrence with Ns = 1 then Ns = R1, so the output is in
 // natural order.  Each radix-R DFT runs entirely in registers as a nested
 // Cooley-Tukey over R = A*B with compile-time twiddles (constexpr sin/cos in
-// double, rounded once to float).  Lines are interleaved in shared memory
-// exactly as in fft_core.cuh (element i of line l at i*LP + l, LP = L + 1), so
-// a warp always touches consecutive words.  Pass-2 twiddles come from a
-// per-CTA shared table tw[m] = w_N^m (double-evaluated).
+// double, rounded once to float).  Lines are interleaved in shared memory with
+// an XOR swizzle instead of padding: element i of line l lives at
+//     sw<L>(i, l) = i*L + (l ^ (i & (L-1)))
+// so a row (fixed i, L lines) is a permutation of L consecutive float2 (the
+// Stockham passes and kx-row staging are conflict-free) and a column (fixed l,
+// consecutive i — the transposed global<->shared staging) spreads over all
+// banks for 8-byte accesses.  Pass-2 twiddles come from a per-CTA shared
+// table tw[m] = w_N^m (double-evaluated).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -147,25 +151,29 @@ __device__ __forceinline__ void load_twiddles(float2* tw_s, const float2* __rest
   for (int i = threadIdx.x; i < n; i += blockDim.x) tw_s[i] = tw_g[i];
 }
 
-// In-place two-pass transform of L interleaved lines (pitch LP = L + 1) of
+template <int L>
+__device__ __forceinline__ int sw(int i, int l) {
+  return i * L + (l ^ (i & (L - 1)));
+}
+
+// In-place two-pass transform of L interleaved (swizzled) lines of
 // length N = R1*R2 held in `buf` (natural order in and out).  NT = blockDim.x
 // must cover every pass-1 butterfly with one thread (NT >= L*R2) so pass 1 can
 // stage its inputs in registers, sync, and overwrite in place; pass 2 reads
 // and writes the same index set per thread.  Caller syncs before.
 template <int R1, int R2, int L, int NT, bool INV>
 __device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __restrict__ tw) {
-  constexpr int LP = L + 1;
   static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
   {
     const int t = threadIdx.x;
     const int l = t % L, j = t / L;
     const bool act = t < L * R2;
     float2 v[R1];
-    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l]; });
+    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[sw<L>(j + decltype(r)::value * R2, l)]; });
     __syncthreads();
     if (act) {
       rdft<R1, INV>(v);
-      static_for<0, R1>([&](auto q) { buf[(j * R1 + decltype(q)::value) * LP + l] = v[decltype(q)::value]; });
+      static_for<0, R1>([&](auto q) { buf[sw<L>(j * R1 + decltype(q)::value, l)] = v[decltype(q)::value]; });
     }
     __syncthreads();
   }
@@ -173,15 +181,15 @@ __device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __r
   for (int t = threadIdx.x; t < L * R1; t += NT) {
     const int l = t % L, j = t / L;
     float2 v[R2];
-    v[0] = buf[j * LP + l];
+    v[0] = buf[sw<L>(j, l)];
     static_for<1, R2>([&](auto r) {
       constexpr int rr = decltype(r)::value;
       const float2 w = tw[rr * j];
-      const float2 x = buf[(j + rr * R1) * LP + l];
+      const float2 x = buf[sw<L>(j + rr * R1, l)];
       v[rr] = INV ? cmulc(x, w) : cmul(x, w);
     });
     rdft<R2, INV>(v);
-    static_for<0, R2>([&](auto q) { buf[(j + decltype(q)::value * R1) * LP + l] = v[decltype(q)::value]; });
+    static_for<0, R2>([&](auto q) { buf[sw<L>(j + decltype(q)::value * R1, l)] = v[decltype(q)::value]; });
   }
   __syncthreads();
 }

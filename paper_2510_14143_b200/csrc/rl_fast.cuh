@@ -3,7 +3,7 @@
 // these differences:
 //
 //  * the line transform is fft_reg.cuh's two-pass register FFT, in place in
-//    ONE shared buffer;
+//    ONE shared buffer with the XOR-swizzled line layout sw<L>(i, l);
 //  * the x crop offset cx (deconv.cpp:59-72) is realised as a phase ramp
 //    exp(+2 pi i cx kx / Wx) folded into both OTFs at plan creation, so a
 //    P-domain row lives at slots [cx, cx+Px) of its length-Wx line before the
@@ -11,15 +11,19 @@
 //    reads the model and writes the ratio / update into the same slot.
 //    (Circular shift by cx, then by -cx: exact; the linear-convolution
 //    support [0, P+K-1) still fits inside Wx.)
+//  * the x-pass epilogue works on whole row PAIRS (the re/im halves of one
+//    packed line) so every shared access is 8 bytes and conflict-free;
 //  * memory-level parallelism: pure copies global->shared use cp.async
 //    (LDGSTS) issued all at once; loads that feed arithmetic are batched
-//    U-deep per thread before use; the z-pass OTF tile is prefetched with
-//    cp.async while the forward transform runs.
+//    U-deep per thread before use; OTF tiles are prefetched with cp.async
+//    while the forward transform runs.
 #pragma once
 #include "fft_reg.cuh"
 #include "rl_passes.cuh"
 
 namespace vk {
+
+using reg::sw;
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
@@ -27,23 +31,25 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
 }
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
 template <int R1, int R2, int L, bool OTF_PREFETCH = false>
 struct FastCfg {
+  static_assert((L & (L - 1)) == 0, "L must be a power of two (swizzle)");
   static constexpr int N = R1 * R2;
-  static constexpr int LP = L + 1;
   static constexpr int NT = ((L * (R1 > R2 ? R1 : R2)) + 31) / 32 * 32;
-  static constexpr size_t smem = (size_t)(N * LP + N + (OTF_PREFETCH ? N * L : 0)) * sizeof(float2);
+  static constexpr size_t smem = (size_t)(N * L + N + (OTF_PREFETCH ? N * L : 0)) * sizeof(float2);
 };
 
 template <int R1, int R2, int L>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
     xpass_fast(const XArgs a) {
   using C = FastCfg<R1, R2, L>;
-  constexpr int N = C::N, LP = C::LP, NT = C::NT;
+  constexpr int N = C::N, NT = C::NT;
   constexpr int Hx = N / 2 + 1;
   constexpr int NW = NT / 32;
   constexpr int U = 4;
+  constexpr int CH = 32 * U;  // samples per work item
   extern __shared__ float2 smem[];
   float2* tw = smem;
   float2* A = smem + N;
@@ -54,25 +60,26 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   const Geom& g = a.g;
 
   if (a.mode == XM_FWD) {
-    // real rows [xoff, xoff+len) of each line, zero elsewhere; one warp per row
-    for (int r = warp; r < 2 * L; r += NW) {
-      const int y = y0 + r;
-      const bool yok = y < a.rows_y;
-      const float* row = a.src + ((size_t)z * a.rows_y + (yok ? y : 0)) * a.len;
-      float* dst = reinterpret_cast<float*>(A) + 2 * (r % L) + (r / L);
-      for (int x0 = 0; x0 < N; x0 += 32 * U) {
-        float v[U];
+    // real rows (l, L+l) -> line l, samples at slots [xoff, xoff+len)
+    const int nch = (N + CH - 1) / CH;
+    for (int item = warp; item < L * nch; item += NW) {
+      const int l = item / nch, x0 = (item % nch) * CH;
+      const int ya = y0 + l, yb = y0 + L + l;
+      const bool va = ya < a.rows_y, vb = yb < a.rows_y;
+      const float* ra = a.src + ((size_t)z * a.rows_y + (va ? ya : 0)) * a.len;
+      const float* rb = a.src + ((size_t)z * a.rows_y + (vb ? yb : 0)) * a.len;
+      float pa[U], pb[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int x = x0 + u * 32 + lane;
-          const int xs = x - a.xoff;
-          v[u] = (yok && x < N && xs >= 0 && xs < a.len) ? __ldg(&row[xs]) * a.scale : 0.f;
-        }
+      for (int u = 0; u < U; ++u) {
+        const int xs = x0 + u * 32 + lane - a.xoff;
+        const bool in = xs >= 0 && xs < a.len;
+        pa[u] = (va && in) ? __ldg(&ra[xs]) * a.scale : 0.f;
+        pb[u] = (vb && in) ? __ldg(&rb[xs]) * a.scale : 0.f;
+      }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int x = x0 + u * 32 + lane;
-          if (x < N) dst[2 * x * LP] = v[u];
-        }
+      for (int u = 0; u < U; ++u) {
+        const int x = x0 + u * 32 + lane;
+        if (x < N) A[sw<L>(x, l)] = make_float2(pa[u], pb[u]);
       }
     }
   } else {
@@ -96,88 +103,108 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
         if (idx >= Hx * L) break;
         const int kx = idx / L, l = idx % L;
         if (kx == 0 || 2 * kx == N) {
-          A[kx * LP + l] = make_float2(xa[u].x, xb[u].x);  // imaginary parts of DC/Nyquist dropped (c2r)
+          A[sw<L>(kx, l)] = make_float2(xa[u].x, xb[u].x);  // imaginary parts of DC/Nyquist dropped (c2r)
         } else {
-          A[kx * LP + l] = make_float2(xa[u].x - xb[u].y, xa[u].y + xb[u].x);
-          A[(N - kx) * LP + l] = make_float2(xa[u].x + xb[u].y, xb[u].x - xa[u].y);
+          A[sw<L>(kx, l)] = make_float2(xa[u].x - xb[u].y, xa[u].y + xb[u].x);
+          A[sw<L>(N - kx, l)] = make_float2(xa[u].x + xb[u].y, xb[u].x - xa[u].y);
         }
       }
     }
     __syncthreads();
     reg::fft2<R1, R2, L, NT, true>(A, tw);
 
-    double accv[3] = {0.0, 0.0, 0.0};
     const bool last = a.mode == XM_UPDATE_LAST;
     const bool ratio = a.mode == XM_RATIO;
-    // one warp per row, U x 32 samples in flight per lane
-    for (int r = warp; r < 2 * L; r += NW) {
-      const int y = y0 + r;
-      const int l = r % L, hi = r / L;
-      float* slots = reinterpret_cast<float*>(A) + 2 * l + hi;  // slot(x) = slots[2 * (x + cx) * LP]
-      if (y >= g.Py) {
-        for (int x = lane; x < g.Px; x += 32) slots[2 * (x + g.cx) * LP] = 0.f;
-        continue;
+    double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
+    // work item = (line l, chunk of CH samples); one warp per item, U samples
+    // of both rows of the line per lane
+    const int nch = (g.Px + CH - 1) / CH;
+    for (int item = warp; item < L * nch; item += NW) {
+      const int l = item / nch, x0 = (item % nch) * CH;
+      const int ya = y0 + l, yb = y0 + L + l;
+      const bool va = ya < g.Py, vb = yb < g.Py;
+      const int iz = z - g.oz, iya = ya - g.oy, iyb = yb - g.oy;
+      const bool zin = iz >= 0 && iz < g.Iz;
+      const bool ina = va && zin && iya >= 0 && iya < g.Iy, inb = vb && zin && iyb >= 0 && iyb < g.Iy;
+      const size_t zoff = (size_t)clampi(iz, 0, g.Iz - 1) * g.Iy;
+      const size_t oa_off = (zoff + clampi(iya, 0, g.Iy - 1)) * g.Ix;
+      const size_t ob_off = (zoff + clampi(iyb, 0, g.Iy - 1)) * g.Ix;
+      const float* oa = a.obs + oa_off;
+      const float* ob = a.obs + ob_off;
+      float* ea = a.est + ((size_t)z * g.Py + (va ? ya : 0)) * g.Px;
+      float* eb = a.est + ((size_t)z * g.Py + (vb ? yb : 0)) * g.Px;
+      float2 m[U];
+      float o_a[U], o_b[U], e_a[U], e_b[U];
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int x = x0 + u * 32 + lane;
+        const bool ok = x < g.Px;
+        const int xo = clampi(x - g.ox, 0, g.Ix - 1);
+        m[u] = ok ? A[sw<L>(x + g.cx, l)] : make_float2(0.f, 0.f);
+        o_a[u] = (ok && va) ? __ldg(&oa[xo]) : 0.f;
+        o_b[u] = (ok && vb) ? __ldg(&ob[xo]) : 0.f;
+        e_a[u] = (!ratio && ok && va) ? ea[x] : 0.f;
+        e_b[u] = (!ratio && ok && vb) ? eb[x] : 0.f;
       }
-      const int iz = z - g.oz, iy = y - g.oy;
-      const bool zyin = iz >= 0 && iz < g.Iz && iy >= 0 && iy < g.Iy;
-      const size_t orow_off = ((size_t)clampi(iz, 0, g.Iz - 1) * g.Iy + clampi(iy, 0, g.Iy - 1)) * g.Ix;
-      const float* orow = a.obs + orow_off;
-      float* erow = a.est + ((size_t)z * g.Py + y) * g.Px;
-      for (int x0 = 0; x0 < g.Px; x0 += 32 * U) {
-        float m[U], o[U], e[U];
+      float f0 = 0.f, f1 = 0.f, f2 = 0.f;
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int x = x0 + u * 32 + lane;
-          const bool ok = x < g.Px;
-          m[u] = ok ? slots[2 * (x + g.cx) * LP] : 0.f;
-          o[u] = ok ? __ldg(&orow[clampi(x - g.ox, 0, g.Ix - 1)]) : 0.f;
-          e[u] = (!ratio && ok) ? erow[x] : 0.f;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int x = x0 + u * 32 + lane;
-          if (x >= g.Px) break;
-          const int ix = x - g.ox;
-          const bool inside = zyin && ix >= 0 && ix < g.Ix;
-          float val;
-          if (ratio) {
-            const float mm = fmaxf(m[u], kEps);
-            val = o[u] / mm;
-            if (inside) accv[0] += (double)o[u] * (double)logf(mm) - (double)mm;
-          } else {
-            val = fmaxf(e[u] * m[u], 0.f);
-            if (!last) erow[x] = val;
-            if (inside) {
-              accv[0] += val;
-              accv[1] += (double)val * val;
-              accv[2] += (double)val * o[u];
-              if (last) a.out[orow_off + ix] = val;
-            }
+      for (int u = 0; u < U; ++u) {
+        const int x = x0 + u * 32 + lane;
+        if (x >= g.Px) break;
+        const int ix = x - g.ox;
+        const bool xin = ix >= 0 && ix < g.Ix;
+        float2 val;
+        if (ratio) {
+          const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
+          val = make_float2(va ? o_a[u] / ma : 0.f, vb ? o_b[u] / mb : 0.f);
+          if (xin && ina) f0 += fmaf(o_a[u], logf(ma), -ma);
+          if (xin && inb) f0 += fmaf(o_b[u], logf(mb), -mb);
+        } else {
+          val = make_float2(va ? fmaxf(e_a[u] * m[u].x, 0.f) : 0.f, vb ? fmaxf(e_b[u] * m[u].y, 0.f) : 0.f);
+          if (!last) {
+            if (va) ea[x] = val.x;
+            if (vb) eb[x] = val.y;
           }
-          slots[2 * (x + g.cx) * LP] = val;
+          if (xin && ina) {
+            f0 += val.x;
+            f1 = fmaf(val.x, val.x, f1);
+            f2 = fmaf(val.x, o_a[u], f2);
+            if (last) a.out[oa_off + ix] = val.x;
+          }
+          if (xin && inb) {
+            f0 += val.y;
+            f1 = fmaf(val.y, val.y, f1);
+            f2 = fmaf(val.y, o_b[u], f2);
+            if (last) a.out[ob_off + ix] = val.y;
+          }
         }
+        A[sw<L>(x + g.cx, l)] = val;
       }
+      acc0 += f0;
+      acc1 += f1;
+      acc2 += f2;
     }
     if (ratio) {
-      double v1[1] = {accv[0]};
+      double v1[1] = {acc0};
       block_accumulate<1>(v1, a.acc);
     } else {
-      block_accumulate<3>(accv, a.acc + 1);
+      double v3[3] = {acc0, acc1, acc2};
+      block_accumulate<3>(v3, a.acc + 1);
     }
     if (last) return;
     // zero the slots outside [cx, cx+Px) before the forward transform
     for (int idx = threadIdx.x; idx < (N - g.Px) * L; idx += NT) {
       const int s = idx / L, l = idx % L;
       const int x = s < g.cx ? s : s + g.Px;
-      A[x * LP + l] = make_float2(0.f, 0.f);
+      A[sw<L>(x, l)] = make_float2(0.f, 0.f);
     }
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false>(A, tw);
   for (int idx = threadIdx.x; idx < Hx * L; idx += NT) {
     const int kx = idx / L, l = idx % L;
-    const float2 zk = A[kx * LP + l];
-    const float2 zn = A[(kx == 0 ? 0 : N - kx) * LP + l];
+    const float2 zk = A[sw<L>(kx, l)];
+    const float2 zn = A[sw<L>(kx == 0 ? 0 : N - kx, l)];
     const float2 xa = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
     const float2 xb = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
     const size_t row = ((size_t)kx * a.rows_z + z) * a.rows_y;
@@ -190,11 +217,11 @@ template <int R1, int R2, int L>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     ypass_fast(const YArgs a) {
   using C = FastCfg<R1, R2, L, true>;
-  constexpr int N = C::N, LP = C::LP, NT = C::NT;
+  constexpr int N = C::N, NT = C::NT;
   extern __shared__ float2 smem[];
   float2* tw = smem;
   float2* A = smem + N;
-  float2* O = A + N * LP;  // OTF tile [l][k] (CONV only)
+  float2* O = A + N * L;  // OTF tile [l][k] (CONV only)
   const int line0 = blockIdx.x * L;
   // async copies: the L input rows (zero padding written directly)
   for (int l = 0; l < L; ++l) {
@@ -203,9 +230,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     const float2* in = a.in + (size_t)(ok ? line : 0) * a.in_pitch;
     for (int i = threadIdx.x; i < N; i += NT) {
       if (ok && i < a.n_in)
-        cp_async8(&A[i * LP + l], &in[i]);
+        cp_async8(&A[sw<L>(i, l)], &in[i]);
       else
-        A[i * LP + l] = make_float2(0.f, 0.f);
+        A[sw<L>(i, l)] = make_float2(0.f, 0.f);
     }
   }
   cp_async_commit();
@@ -220,7 +247,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   }
   reg::load_twiddles(tw, a.plan.tw, N);
   if (a.mode == YM_CONV)
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");  // input rows landed, OTF may still fly
+    cp_async_wait_1();  // input rows landed, OTF may still fly
   else
     cp_async_wait_all();
   __syncthreads();
@@ -233,7 +260,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
       __syncthreads();
       for (int idx = threadIdx.x; idx < N * L; idx += NT) {
         const int k = idx / L, l = idx % L;
-        A[k * LP + l] = cmul(A[k * LP + l], O[l * N + k]);
+        A[sw<L>(k, l)] = cmul(A[sw<L>(k, l)], O[l * N + k]);
       }
       __syncthreads();
       reg::fft2<R1, R2, L, NT, true>(A, tw);
@@ -243,7 +270,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     const int line = line0 + l;
     if (line >= a.nlines) break;
     float2* out = a.out + (size_t)line * a.out_pitch;
-    for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[(j + a.out_off) * LP + l];
+    for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[sw<L>(j + a.out_off, l)];
   }
 }
 
@@ -251,11 +278,11 @@ template <int R1, int R2, int L>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     zpass_fast(const ZArgs a) {
   using C = FastCfg<R1, R2, L, true>;
-  constexpr int N = C::N, LP = C::LP, NT = C::NT;
+  constexpr int N = C::N, NT = C::NT;
   extern __shared__ float2 smem[];
   float2* tw = smem;
   float2* A = smem + N;
-  float2* O = A + N * LP;  // OTF tile, same [kz][l] layout as A (pitch L)
+  float2* O = A + N * L;  // OTF tile, [kz][l] row-major (pitch L)
   const int kx = blockIdx.y;
   const int ky0 = blockIdx.x * L;
   const size_t plane = (size_t)kx * a.zrows * a.Wy;
@@ -264,9 +291,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     const int z = idx / L, l = idx % L;
     const int ky = ky0 + l;
     if (z < a.n_in && ky < a.Wy)
-      cp_async8(&A[z * LP + l], &a.S[plane + (size_t)z * a.Wy + ky]);
+      cp_async8(&A[sw<L>(z, l)], &a.S[plane + (size_t)z * a.Wy + ky]);
     else
-      A[z * LP + l] = make_float2(0.f, 0.f);
+      A[sw<L>(z, l)] = make_float2(0.f, 0.f);
   }
   cp_async_commit();
   const bool conv = a.mode == ZM_CONV;
@@ -280,7 +307,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   }
   reg::load_twiddles(tw, a.plan.tw, N);
   if (conv)
-    asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    cp_async_wait_1();
   else
     cp_async_wait_all();
   __syncthreads();
@@ -289,7 +316,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     for (int idx = threadIdx.x; idx < N * L; idx += NT) {
       const int kz = idx / L, l = idx % L;
       const int ky = ky0 + l;
-      if (ky < a.Wy) a.otf_out[oplane + (size_t)kz * a.Wy + ky] = A[kz * LP + l];
+      if (ky < a.Wy) a.otf_out[oplane + (size_t)kz * a.Wy + ky] = A[sw<L>(kz, l)];
     }
     return;
   }
@@ -297,14 +324,14 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   __syncthreads();
   for (int idx = threadIdx.x; idx < N * L; idx += NT) {
     const int kz = idx / L, l = idx % L;
-    A[kz * LP + l] = cmul(A[kz * LP + l], O[idx]);
+    A[sw<L>(kz, l)] = cmul(A[sw<L>(kz, l)], O[idx]);
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true>(A, tw);
   for (int idx = threadIdx.x; idx < a.n_out * L; idx += NT) {
     const int z = idx / L, l = idx % L;
     const int ky = ky0 + l;
-    if (ky < a.Wy) a.S[plane + (size_t)z * a.Wy + ky] = A[(z + a.out_off) * LP + l];
+    if (ky < a.Wy) a.S[plane + (size_t)z * a.Wy + ky] = A[sw<L>(z + a.out_off, l)];
   }
 }
 
