@@ -68,7 +68,7 @@ class Unsupported(Error):
     pass
 
 
-KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv")  # vk_kernel_kind
+KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv", "yz_dataflow")  # vk_kernel_kind
 
 _STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: DegenerateReference,
            6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported}

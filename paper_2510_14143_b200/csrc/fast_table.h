@@ -3,6 +3,8 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include "rl_passes.cuh"
+
 namespace vk {
 
 struct FastEntry {
@@ -22,5 +24,40 @@ cudaError_t fast_init_attributes();
 
 // OTF *= exp(+2 pi i cx kx / Wx) for every kx plane (layout [Hx][plane]).
 cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, cudaStream_t s);
+
+}  // namespace vk
+
+namespace vk {
+
+// One-launch 3D y/z convolution (rl_dataflow.cuh): task codes and arguments.
+enum DfTask : unsigned { DF_YF = 0, DF_Z = 1, DF_YI = 2 };
+
+__host__ __device__ inline unsigned df_encode(unsigned type, unsigned plane, unsigned chunk) {
+  return (type << 30) | (plane << 14) | chunk;
+}
+
+struct DfArgs {
+  const float2* twy;
+  const float2* twz;
+  Geom g;
+  float2* SA;         // [Hx][Pz][Py]
+  float2* ring;       // [R][Pz][Wy]
+  const float2* otf;  // [Hx][Wz][Wy]
+  int R;
+  const unsigned* tasks;
+  int ntasks;
+  int* ctr;           // [0] next task, then done counters [3][Hx] (Yf, Z, Yi)
+  int nYf, nZ, nYi;
+};
+
+// One-launch 3D y/z convolution kernels by (Wy, Wz).
+struct DfEntry {
+  int Ny, Nz;
+  int Ly, Lz;
+  int NT;
+  size_t smem;
+  const void* k;  // yzconv_dataflow<...>(DfArgs)
+};
+const DfEntry* df_lookup(int ny, int nz);
 
 }  // namespace vk

@@ -4,7 +4,7 @@
 // length runs the generic Stockham kernels of rl_passes.cuh.
 #define VK_NO_GENERIC_KERNELS
 #include "fast_table.h"
-#include "rl_fast.cuh"
+#include "rl_dataflow.cuh"
 
 namespace vk {
 
@@ -33,7 +33,7 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16>(),  // 192
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 8, 8>(),    // 576
+    make_entry<24, 24, 4, 8>(),    // 576
     make_entry<30, 36, 8, 4>(),    // 1080
     make_entry<45, 48, 4, 2>(),    // 2160
 };
@@ -46,7 +46,29 @@ const FastEntry* fast_lookup(int n) {
   return nullptr;
 }
 
+template <int YR1, int YR2, int YL, int ZR1, int ZR2, int ZL>
+DfEntry make_df() {
+  using C = DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>;
+  return DfEntry{C::NY, C::NZ, YL, ZL, C::NT, C::smem, (const void*)yzconv_dataflow<YR1, YR2, YL, ZR1, ZR2, ZL>};
+}
+
+const DfEntry kDfTable[] = {
+    make_df<16, 18, 16, 8, 12, 16>(),   // C1/C3 grid: Wy 288, Wz 96
+    make_df<24, 24, 8, 12, 16, 16>(),   // C2 grid: Wy 576, Wz 192
+    make_df<30, 36, 8, 12, 12, 16>(),   // C4 grid: Wy 1080, Wz 144
+};
+
+const DfEntry* df_lookup(int ny, int nz) {
+  for (const auto& e : kDfTable)
+    if (e.Ny == ny && e.Nz == nz) return &e;
+  return nullptr;
+}
+
 cudaError_t fast_init_attributes() {
+  for (const auto& e : kDfTable) {
+    cudaError_t r = cudaFuncSetAttribute(e.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
+    if (r) return r;
+  }
   for (const auto& e : kTable) {
     cudaError_t r;
     if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_x))) return r;

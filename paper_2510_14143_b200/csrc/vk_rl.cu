@@ -181,6 +181,13 @@ struct vk_rl_plan_s {
   const vk::FastEntry* fx = nullptr;
   const vk::FastEntry* fy = nullptr;
   const vk::FastEntry* fz = nullptr;
+  // one-launch y/z convolution (3D fast grids), see rl_dataflow.cuh
+  const vk::DfEntry* df = nullptr;
+  int df_blocks = 0, df_R = 0, df_ntasks = 0, df_nyf = 0, df_nz = 0;
+  DevBuf<float2> ring;
+  DevBuf<unsigned> df_tasks;
+  DevBuf<int> df_ctr;
+  size_t df_window = 0;
   int xL = 1, yL = 1, zL = 1;
   size_t xs = 0, ys = 0, zs = 0;
 
@@ -349,9 +356,57 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
 // 'same' linear convolution of the x-transformed P-domain field held in SA
 // with `otf` (deconv.cpp:135-147 minus the x transforms, which live in the
 // fused X-pass).  Result back in SA.
+void conv_dataflow(vk_rl_plan p, cudaStream_t s, const float2* otf) {
+  const Geom& g = p->g;
+  vk::DfArgs a{};
+  a.twy = p->twy.p;
+  a.twz = p->twz.p;
+  a.g = g;
+  a.SA = p->SA.p;
+  a.ring = p->ring.p;
+  a.otf = otf;
+  a.R = p->df_R;
+  a.tasks = p->df_tasks.p;
+  a.ntasks = p->df_ntasks;
+  a.ctr = p->df_ctr.p;
+  a.nYf = p->df_nyf;
+  a.nZ = p->df_nz;
+  a.nYi = p->df_nyf;
+  ck(cudaMemsetAsync(p->df_ctr.p, 0, p->df_ctr.n * sizeof(int), s), "dataflow counters");
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p->df_blocks);
+  cfg.blockDim = dim3(p->df->NT);
+  cfg.dynamicSmemBytes = p->df->smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  int nat = 1;
+  if (p->df_window) {
+    at[1].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[1].val.accessPolicyWindow.base_ptr = p->ring.p;
+    at[1].val.accessPolicyWindow.num_bytes = p->df_window;
+    at[1].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    nat = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = nat;
+  void* args[] = {&a};
+  const size_t t = prof_begin(p, s);
+  ck(cudaLaunchKernelExC(&cfg, p->df->k, args), "dataflow launch");
+  launch_check(p, "yz dataflow");
+  prof_end(p, s, VK_KIND_YZ_DATAFLOW, t);
+}
+
 void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   const Geom& g = p->g;
   const int nl = g.Hx * g.Pz;
+  if (p->df) {
+    conv_dataflow(p, s, otf);
+    return;
+  }
   if (g.Wz == 1) {
     y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, g.cy, p->SA.p, p->SA.p, otf);
     return;
@@ -375,6 +430,61 @@ void build_otf(vk_rl_plan p, const float* d_psf, float2* otf_dst) {
   }
   y_pass(p, s, vk::YM_FWD, nl, p->Ky, p->Ky, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
   z_pass(p, s, vk::ZM_FWD_OUT, p->Kz, p->Kz, 0, 0, p->SB.p, nullptr, otf_dst);
+}
+
+// Task list, ring and counters of the one-launch y/z convolution.  Lag D (in
+// planes) ~ the number of planes whose tasks the resident CTAs hold at once;
+// ring R = 2D + 2 slots (task-order invariant R > 2D, see rl_dataflow.cuh).
+void setup_dataflow(vk_rl_plan p) {
+  const Geom& g = p->g;
+  const vk::DfEntry* d = p->df;
+  int dev = 0, nsm = 0, per_sm = 0;
+  ck(cudaGetDevice(&dev), "device");
+  ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
+  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d->k, d->NT, d->smem), "occupancy");
+  if (per_sm < 1) {
+    p->df = nullptr;
+    return;
+  }
+  p->df_blocks = per_sm * nsm;
+  p->df_nyf = (g.Pz + d->Ly - 1) / d->Ly;
+  p->df_nz = (g.Wy + d->Lz - 1) / d->Lz;
+  const int per_plane = 2 * p->df_nyf + p->df_nz;
+  const char* lag_env = std::getenv("VK_RL_DF_LAG");
+  int D = lag_env ? std::atoi(lag_env) : (p->df_blocks + per_plane - 1) / per_plane + 1;
+  D = std::max(1, std::min(D, g.Hx));
+  p->df_R = std::min(2 * D + 2, g.Hx);
+  if (p->df_R < g.Hx && p->df_R <= 2 * D) p->df_R = std::min(2 * D + 1, g.Hx);
+  std::vector<unsigned> tasks;
+  tasks.reserve((size_t)g.Hx * per_plane);
+  for (int step = 0; step < g.Hx + 2 * D; ++step) {
+    if (step < g.Hx)
+      for (int c = 0; c < p->df_nyf; ++c) tasks.push_back(vk::df_encode(vk::DF_YF, step, c));
+    if (step - D >= 0 && step - D < g.Hx)
+      for (int c = 0; c < p->df_nz; ++c) tasks.push_back(vk::df_encode(vk::DF_Z, step - D, c));
+    if (step - 2 * D >= 0 && step - 2 * D < g.Hx)
+      for (int c = 0; c < p->df_nyf; ++c) tasks.push_back(vk::df_encode(vk::DF_YI, step - 2 * D, c));
+  }
+  p->df_ntasks = (int)tasks.size();
+  p->df_tasks.alloc(tasks.size(), "dataflow tasks");
+  ck(cudaMemcpy(p->df_tasks.p, tasks.data(), tasks.size() * sizeof(unsigned), cudaMemcpyHostToDevice), "tasks");
+  p->df_ctr.alloc(1 + 3 * (size_t)g.Hx, "dataflow counters");
+  const size_t slot = (size_t)g.Pz * g.Wy;
+  p->ring.alloc((size_t)p->df_R * slot, "dataflow ring");
+  // keep the ring L2-resident (persisting window), within the device limits
+  int max_persist = 0, max_window = 0;
+  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+  const char* nopersist = std::getenv("VK_RL_NO_L2_PERSIST");
+  if (max_persist > 0 && max_window > 0 && !(nopersist && nopersist[0] == '1')) {
+    const size_t bytes = p->ring.n * sizeof(float2);
+    size_t cur = 0;
+    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+    const size_t want = std::min<size_t>(bytes, (size_t)max_persist);
+    if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+    p->df_window = std::min<size_t>(bytes, (size_t)max_window);
+    cudaGetLastError();
+  }
 }
 
 void to3(int rank, const uint64_t* in, uint64_t* out3) {
@@ -466,6 +576,8 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->fx = vk::fast_lookup(g.Wx);
       p->fy = vk::fast_lookup(g.Wy);
       p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
+      const char* nodf = std::getenv("VK_RL_NO_DATAFLOW");
+      if (p->fy && p->fz && !(nodf && nodf[0] == '1')) p->df = vk::df_lookup(g.Wy, g.Wz);
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
@@ -491,6 +603,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->otf.alloc(so, "otf");
     p->otf_flip.alloc(so, "otf_flip");
     p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
+    if (p->df) setup_dataflow(p);
     p->stats.alloc(1, "stats");
 
     // Both spectra: psf and std::reverse(psf) == flip about every axis.
@@ -709,6 +822,7 @@ uint64_t alg_bytes(vk_rl_plan p, int kind) {
     case VK_KIND_Z_CONV: return 16 * Sb + 8 * So;
     case VK_KIND_Y_INV: return 8 * Sb + 8 * Sp;
     case VK_KIND_Y_CONV: return 16 * Sp + 8 * So;
+    case VK_KIND_YZ_DATAFLOW: return 16 * Sp + 8 * So;
     default: return 0;
   }
 }

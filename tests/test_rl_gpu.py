@@ -199,6 +199,46 @@ def test_fast_lengths_vs_oracle_and_generic(name):
     assert rel_l2(r1.estimate, its[0]) <= TOL_1
 
 
+def _with_env(env, fn):
+    old = {k: os.environ.get(k) for k in env}
+    os.environ.update(env)
+    try:
+        return fn()
+    finally:
+        for k, v in old.items():
+            if v is None:
+                os.environ.pop(k, None)
+            else:
+                os.environ[k] = v
+
+
+@pytest.mark.parametrize("name,shape,mk", [
+    ("c1_grid_288x96", (64, 256, 256), lambda: O.gaussian_psf((15, 15, 15), 1.75)),
+    ("c2_grid_576x192", (128, 60, 512), lambda: O.widefield_psf(31)),
+    ("c4_grid_1080x144", (100, 1000, 20), lambda: O.gaussian_psf((21, 21, 21), 2.5)),
+])
+def test_dataflow_yz_conv_matches_three_pass(name, shape, mk):
+    """The one-launch y/z convolution (persistent dataflow kernel, ring of
+    planes with completion counters) against the 3-launch path, with the
+    default lag and with lag 1 (ring of 4 planes: maximal slot reuse)."""
+    psf = mk()
+    obs = synth.blurred(synth.blobs(shape, 30, 5, 9, seed=11), psf)
+    rule = fixed_rule(3)
+    ref = _with_env({"VK_RL_NO_DATAFLOW": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    df = vk.richardson_lucy(obs, psf, rule)
+    tight = _with_env({"VK_RL_DF_LAG": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    assert rel_l2(df.estimate, ref.estimate) <= 1e-6
+    assert rel_l2(tight.estimate, ref.estimate) <= 1e-6
+    plan = vk.RlPlan(shape, psf)
+    plan.profile(True)
+    plan.run(obs, rule)
+    prof = plan.profile_read()
+    assert prof["yz_dataflow"][1] == 2 * 3, prof  # two convolutions per iteration, one launch each
+    its, _ = run_oracle(obs, psf, 1)
+    r1 = vk.richardson_lucy(obs, psf, fixed_rule(1))
+    assert rel_l2(r1.estimate, its[0]) <= TOL_1
+
+
 def test_c2_full_size_first_iterations():
     """C2 at full size (128x512x512, 31^3 widefield): the benchmark's own grid
     (192 x 576 x 576) through the fast kernels, 2 iterations vs the oracle."""
