@@ -324,6 +324,7 @@ def main():
         "config": {"workload": cfg["label"] + (" per GPU" if ws > 1 else ""), "image": list(shape),
                    "psf": list(psf.shape), "iters_per_step": iters, "fft_shape": list(g),
                    "padded_domain": list(P), "parallelism": f"independent volumes x{ws}",
+                   "plan": plan.describe(),
                    "l2": "inputs larger than L2 (spectrum %.0f MB, observed %.0f MB > 126 MB)"
                          % (s_p * 8 / 1e6, n_img * 4 / 1e6)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

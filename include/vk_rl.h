@@ -95,6 +95,10 @@ vk_status vk_rl_plan_create(int device, int rank, const uint64_t* shape, int psf
 vk_status vk_rl_plan_shapes(vk_rl_plan plan, int* rank, uint64_t* image_shape,
                             uint64_t* domain_shape, uint64_t* fft_shape);
 
+/* Human-readable execution plan: FFT grid, kernel variant per axis, y/z
+ * convolution strategy (for logs and the bench's config record). */
+vk_status vk_rl_plan_describe(vk_rl_plan plan, char* buf, int len);
+
 /* Bytes of device memory the plan holds. */
 vk_status vk_rl_plan_device_bytes(vk_rl_plan plan, uint64_t* bytes);
 

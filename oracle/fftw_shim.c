@@ -136,6 +136,40 @@ static void line_fft(const line_plan* p, cpx* x, cpx* work, int sign) {
         dst[base + 2 * Ns].im = a0.im - a2.im;
         dst[base + 3 * Ns].re = a1.re - b3.re;
         dst[base + 3 * Ns].im = a1.im - b3.im;
+      } else if (R == 3) {
+        const double c = -0.5, sn = (sign < 0 ? -1.0 : 1.0) * 0.86602540378443864676;
+        cpx a = {v[1].re + v[2].re, v[1].im + v[2].im};
+        cpx b = {v[1].re - v[2].re, v[1].im - v[2].im};
+        cpx t = {v[0].re + c * a.re, v[0].im + c * a.im};
+        /* i*sn*b */
+        cpx u = {-sn * b.im, sn * b.re};
+        dst[base].re = v[0].re + a.re;
+        dst[base].im = v[0].im + a.im;
+        dst[base + Ns].re = t.re + u.re;
+        dst[base + Ns].im = t.im + u.im;
+        dst[base + 2 * Ns].re = t.re - u.re;
+        dst[base + 2 * Ns].im = t.im - u.im;
+      } else if (R == 5) {
+        const double c1 = 0.30901699437494742410, c2 = -0.80901699437494742410;
+        const double sg = sign < 0 ? -1.0 : 1.0;
+        const double s1 = sg * 0.95105651629515357212, s2 = sg * 0.58778525229247312917;
+        cpx a1 = {v[1].re + v[4].re, v[1].im + v[4].im}, b1 = {v[1].re - v[4].re, v[1].im - v[4].im};
+        cpx a2 = {v[2].re + v[3].re, v[2].im + v[3].im}, b2 = {v[2].re - v[3].re, v[2].im - v[3].im};
+        cpx t1 = {v[0].re + c1 * a1.re + c2 * a2.re, v[0].im + c1 * a1.im + c2 * a2.im};
+        cpx t2 = {v[0].re + c2 * a1.re + c1 * a2.re, v[0].im + c2 * a1.im + c1 * a2.im};
+        /* u = i*(s1 b1 + s2 b2), w = i*(s2 b1 - s1 b2) */
+        cpx u = {-(s1 * b1.im + s2 * b2.im), s1 * b1.re + s2 * b2.re};
+        cpx w = {-(s2 * b1.im - s1 * b2.im), s2 * b1.re - s1 * b2.re};
+        dst[base].re = v[0].re + a1.re + a2.re;
+        dst[base].im = v[0].im + a1.im + a2.im;
+        dst[base + Ns].re = t1.re + u.re;
+        dst[base + Ns].im = t1.im + u.im;
+        dst[base + 4 * Ns].re = t1.re - u.re;
+        dst[base + 4 * Ns].im = t1.im - u.im;
+        dst[base + 2 * Ns].re = t2.re + w.re;
+        dst[base + 2 * Ns].im = t2.im + w.im;
+        dst[base + 3 * Ns].re = t2.re - w.re;
+        dst[base + 3 * Ns].im = t2.im - w.im;
       } else {
         const cpx* rt = p->root[s];
         for (int q = 0; q < R; ++q) {

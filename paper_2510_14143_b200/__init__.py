@@ -123,6 +123,8 @@ def lib() -> ctypes.CDLL:
                  "vk_rl_plan_destroy", "vk_rl_run", "vk_rl_run_device", "vk_rl_run_batch", "vk_rl_step",
                  "vk_rl_step_device", "vk_richardson_lucy", "vk_rl_step_psf"):
         getattr(L, name).restype = st
+    L.vk_rl_plan_describe.argtypes = [_vp, ctypes.c_char_p, i]
+    L.vk_rl_plan_describe.restype = st
     L.vk_rl_plan_profile.argtypes = [_vp, i]
     L.vk_rl_plan_profile_read.argtypes = [_vp, i, _dp, _u64p, _u64p, i]
     L.vk_rl_plan_profile.restype = st
@@ -250,6 +252,12 @@ class _Plan:
         v = ctypes.c_uint64(0)
         _check(lib().vk_rl_plan_launches(self._h, ctypes.byref(v)))
         return int(v.value)
+
+    def describe(self) -> str:
+        """Execution plan chosen for this shape (kernel variant per axis, y/z strategy)."""
+        buf = ctypes.create_string_buffer(512)
+        _check(lib().vk_rl_plan_describe(self._h, buf, 512))
+        return buf.value.decode()
 
     def profile(self, enable: bool = True) -> None:
         """CUDA-event timing of every launch, by kernel kind (vk_rl_plan_profile)."""

@@ -151,6 +151,15 @@ __device__ __forceinline__ void load_twiddles(float2* tw_s, const float2* __rest
   for (int i = threadIdx.x; i < n; i += blockDim.x) tw_s[i] = tw_g[i];
 }
 
+// threadIdx.x through a volatile asm: index math derived from it cannot be
+// hoisted out of a persistent task loop (which otherwise keeps every unrolled
+// shared-memory address of the transform live in registers across tasks).
+__device__ __forceinline__ int fresh_tid() {
+  int t;
+  asm volatile("mov.u32 %0, %%tid.x;" : "=r"(t));
+  return t;
+}
+
 template <int L>
 __device__ __forceinline__ int sw(int i, int l) {
   return i * L + (l ^ (i & (L - 1)));
@@ -165,7 +174,7 @@ template <int R1, int R2, int L, int NT, bool INV>
 __device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __restrict__ tw) {
   static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
   {
-    const int t = threadIdx.x;
+    const int t = fresh_tid();
     const int l = t % L, j = t / L;
     const bool act = t < L * R2;
     float2 v[R1];
@@ -178,7 +187,7 @@ __device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __r
     __syncthreads();
   }
 #pragma unroll 1
-  for (int t = threadIdx.x; t < L * R1; t += NT) {
+  for (int t = fresh_tid(); t < L * R1; t += NT) {
     const int l = t % L, j = t / L;
     float2 v[R2];
     v[0] = buf[sw<L>(j, l)];

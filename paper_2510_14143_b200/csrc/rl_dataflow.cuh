@@ -12,11 +12,13 @@
 //   Yi(p, c)  y-inverse of rows [c*LY, ...): ring -> S_A (cropped)
 //
 // with per-plane completion counters: Z(p,*) waits for all Yf(p,*), Yi(p,*)
-// for all Z(p,*), and Yf(p,*) for Yi(p-R,*) (ring slot reuse).  CTAs grab task
-// indices from one atomic counter; the host orders the task list by "step"
+// for all Z(p,*), and Yf(p,*) for Yi(p-R,*) (ring slot reuse).  One CTA per
+// task; each CTA takes a ticket from one atomic counter when it starts and
+// runs task[ticket].  The host orders the task list by "step"
 // s = {Yf(s), Z(s-D), Yi(s-2D)} with R > 2D, so every task only waits on
-// tasks that precede it in the list and were therefore already taken by a
-// resident CTA: no deadlock with a cooperative (all-resident) grid.
+// tasks with smaller tickets, i.e. on CTAs that started before it: no
+// deadlock whatever the hardware's CTA dispatch order (the decoupled
+// look-back argument), and no co-residency requirement.
 //
 // The ring (R planes, ~17-23 MB) is the only intermediate and is marked
 // L2-persisting by the host, so S_B traffic stays on chip: HBM sees S_A read +
@@ -38,7 +40,10 @@ struct DfCfg {
   static constexpr int NT = FastCfg<YR1, YR2, YL>::NT > FastCfg<ZR1, ZR2, ZL>::NT ? FastCfg<YR1, YR2, YL>::NT
                                                                                   : FastCfg<ZR1, ZR2, ZL>::NT;
   static constexpr int WORK = NY * YL > 2 * NZ * ZL ? NY * YL : 2 * NZ * ZL;
-  static constexpr size_t smem = (size_t)(NY + NZ + WORK) * sizeof(float2);
+  static constexpr size_t smem = (size_t)((NY > NZ ? NY : NZ) + WORK) * sizeof(float2);
+  // resident CTAs per SM the register budget is sized for (smem-limited)
+  static constexpr int MINB_SMEM = (int)((227u * 1024u) / (smem + 1024u));
+  static constexpr int MINB = MINB_SMEM < 1 ? 1 : (MINB_SMEM > 4 ? 4 : MINB_SMEM);
 };
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -55,7 +60,7 @@ __device__ __forceinline__ void df_y_task(float2* A, const float2* tw, const flo
   constexpr int N = R1 * R2;
   for (int l = 0; l < L; ++l) {
     const float2* row = in + (size_t)(l < nv ? l : 0) * in_pitch;
-    for (int i = threadIdx.x; i < N; i += NT) {
+    for (int i = reg::fresh_tid(); i < N; i += NT) {
       if (l < nv && i < n_in)
         cp_async8(&A[sw<L>(i, l)], &row[i]);
       else
@@ -68,7 +73,7 @@ __device__ __forceinline__ void df_y_task(float2* A, const float2* tw, const flo
   reg::fft2<R1, R2, L, NT, INV>(A, tw);
   for (int l = 0; l < nv; ++l) {
     float2* o = out + (size_t)l * out_pitch;
-    for (int j = threadIdx.x; j < n_out; j += NT) o[j] = A[sw<L>(j + out_off, l)];
+    for (int j = reg::fresh_tid(); j < n_out; j += NT) o[j] = A[sw<L>(j + out_off, l)];
   }
 }
 
@@ -77,7 +82,7 @@ template <int R1, int R2, int L, int NT>
 __device__ __forceinline__ void df_z_task(float2* A, float2* O, const float2* tw, float2* plane, int Wy, int n_in,
                                           int n_out, int out_off, const float2* otf_plane, int ky0) {
   constexpr int N = R1 * R2;
-  for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+  for (int idx = reg::fresh_tid(); idx < N * L; idx += NT) {
     const int z = idx / L, l = idx % L;
     const int ky = ky0 + l;
     if (z < n_in && ky < Wy)
@@ -86,7 +91,7 @@ __device__ __forceinline__ void df_z_task(float2* A, float2* O, const float2* tw
       A[sw<L>(z, l)] = make_float2(0.f, 0.f);
   }
   cp_async_commit();
-  for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+  for (int idx = reg::fresh_tid(); idx < N * L; idx += NT) {
     const int kz = idx / L, l = idx % L;
     const int ky = ky0 + l;
     if (ky < Wy) cp_async8(&O[idx], &otf_plane[(size_t)kz * Wy + ky]);
@@ -97,13 +102,13 @@ __device__ __forceinline__ void df_z_task(float2* A, float2* O, const float2* tw
   reg::fft2<R1, R2, L, NT, false>(A, tw);
   cp_async_wait_all();
   __syncthreads();
-  for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+  for (int idx = reg::fresh_tid(); idx < N * L; idx += NT) {
     const int kz = idx / L, l = idx % L;
     A[sw<L>(kz, l)] = cmul(A[sw<L>(kz, l)], O[idx]);
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true>(A, tw);
-  for (int idx = threadIdx.x; idx < n_out * L; idx += NT) {
+  for (int idx = reg::fresh_tid(); idx < n_out * L; idx += NT) {
     const int z = idx / L, l = idx % L;
     const int ky = ky0 + l;
     if (ky < Wy) plane[(size_t)z * Wy + ky] = A[sw<L>(z + out_off, l)];
@@ -111,71 +116,71 @@ __device__ __forceinline__ void df_z_task(float2* A, float2* O, const float2* tw
 }
 
 template <int YR1, int YR2, int YL, int ZR1, int ZR2, int ZL>
-__global__ void __launch_bounds__(DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>::NT)
+__global__ void __launch_bounds__(DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>::NT, DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>::MINB)
     yzconv_dataflow(const DfArgs a) {
   using C = DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>;
   constexpr int NY = C::NY, NZ = C::NZ, NT = C::NT;
   extern __shared__ float2 smem[];
-  float2* twy = smem;
-  float2* twz = smem + NY;
-  float2* W = twz + NZ;
+  float2* tw = smem;              // the twiddle table of the task's transform
+  float2* W = smem + (NY > NZ ? NY : NZ);
   __shared__ int s_task;
-  reg::load_twiddles(twy, a.twy, NY);
-  reg::load_twiddles(twz, a.twz, NZ);
   const Geom& g = a.g;
-  int* next = a.ctr;
   int* const done0 = a.ctr + 1;  // done counters of task type t live at done0 + t*Hx
-  const size_t slot_elems = (size_t)g.Pz * g.Wy;
-  for (;;) {
-    if (threadIdx.x == 0) s_task = atomicAdd(next, 1);
-    __syncthreads();
-    const int t = s_task;
-    if (t >= a.ntasks) break;
-    const unsigned code = a.tasks[t];
-    const unsigned type = code >> 30, p = (code >> 14) & 0xffffu, c = code & 0x3fffu;
-    if (threadIdx.x == 0) {
-      const int* dep = nullptr;
-      int need = 0;
-      if (type == DF_YF) {
-        if ((int)p >= a.R) {
-          dep = done0 + DF_YI * g.Hx + (p - a.R);
-          need = a.nYi;
-        }
-      } else if (type == DF_Z) {
-        dep = done0 + DF_YF * g.Hx + p;
-        need = a.nYf;
-      } else {
-        dep = done0 + DF_Z * g.Hx + p;
-        need = a.nZ;
-      }
-      if (dep) {
-        unsigned ns = 32;
-        while (ld_acquire(dep) < need) {
-          __nanosleep(ns);
-          ns = ns < 1024 ? ns * 2 : ns;
-        }
-      }
-      __threadfence();  // acquire side; also drops stale L1 lines of reused ring slots
-    }
-    __syncthreads();
-    float2* slot = a.ring + (size_t)(p % a.R) * slot_elems;
+  // one task per CTA; the ticket is taken when the CTA starts, so every
+  // dependency belongs to a CTA that started earlier (no deadlock, no
+  // co-residency requirement).
+  if (threadIdx.x == 0) s_task = atomicAdd(a.ctr, 1);
+  __syncthreads();
+  const int t = s_task;
+  if (t >= a.ntasks) return;
+  const unsigned code = a.tasks[t];
+  const unsigned type = code >> 30, p = (code >> 14) & 0xffffu, c = code & 0x3fffu;
+  if (type == DF_Z)
+    reg::load_twiddles(tw, a.twz, NZ);
+  else
+    reg::load_twiddles(tw, a.twy, NY);
+  if (threadIdx.x == 0) {
+    const int* dep = nullptr;
+    int need = 0;
     if (type == DF_YF) {
-      const int z0 = c * YL, nv = min(YL, g.Pz - z0);
-      df_y_task<YR1, YR2, YL, NT, false>(W, twy, a.SA + ((size_t)p * g.Pz + z0) * g.Py, g.Py, g.Py, nv,
-                                         slot + (size_t)z0 * g.Wy, g.Wy, g.Wy, 0);
+      if ((int)p >= a.R) {
+        dep = done0 + DF_YI * g.Hx + (p - a.R);
+        need = a.nYi;
+      }
     } else if (type == DF_Z) {
-      df_z_task<ZR1, ZR2, ZL, NT>(W, W + NZ * ZL, twz, slot, g.Wy, g.Pz, g.Pz, g.cz,
-                                  a.otf + (size_t)p * NZ * g.Wy, c * ZL);
+      dep = done0 + DF_YF * g.Hx + p;
+      need = a.nYf;
     } else {
-      const int z0 = c * YL, nv = min(YL, g.Pz - z0);
-      df_y_task<YR1, YR2, YL, NT, true>(W, twy, slot + (size_t)z0 * g.Wy, g.Wy, g.Wy, nv,
-                                        a.SA + ((size_t)p * g.Pz + z0) * g.Py, g.Py, g.Py, g.cy);
+      dep = done0 + DF_Z * g.Hx + p;
+      need = a.nZ;
     }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      atomicAdd(done0 + type * g.Hx + p, 1);
+    if (dep) {
+      unsigned ns = 32;
+      while (ld_acquire(dep) < need) {
+        __nanosleep(ns);
+        ns = ns < 512 ? ns * 2 : ns;
+      }
     }
+    __threadfence();  // acquire side; also drops stale L1 lines of reused ring slots
+  }
+  __syncthreads();
+  float2* slot = a.ring + (size_t)(p % a.R) * g.Pz * g.Wy;
+  if (type == DF_YF) {
+    const int z0 = c * YL, nv = min(YL, g.Pz - z0);
+    df_y_task<YR1, YR2, YL, NT, false>(W, tw, a.SA + ((size_t)p * g.Pz + z0) * g.Py, g.Py, g.Py, nv,
+                                       slot + (size_t)z0 * g.Wy, g.Wy, g.Wy, 0);
+  } else if (type == DF_Z) {
+    df_z_task<ZR1, ZR2, ZL, NT>(W, W + NZ * ZL, tw, slot, g.Wy, g.Pz, g.Pz, g.cz,
+                                a.otf + (size_t)p * NZ * g.Wy, c * ZL);
+  } else {
+    const int z0 = c * YL, nv = min(YL, g.Pz - z0);
+    df_y_task<YR1, YR2, YL, NT, true>(W, tw, slot + (size_t)z0 * g.Wy, g.Wy, g.Wy, nv,
+                                      a.SA + ((size_t)p * g.Pz + z0) * g.Py, g.Py, g.Py, g.cy);
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(done0 + type * g.Hx + p, 1);
   }
 }
 

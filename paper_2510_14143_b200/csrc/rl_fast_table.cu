@@ -33,7 +33,7 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16>(),  // 192
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 4, 8>(),    // 576
+    make_entry<24, 24, 8, 8>(),    // 576
     make_entry<30, 36, 8, 4>(),    // 1080
     make_entry<45, 48, 4, 2>(),    // 2160
 };
@@ -53,9 +53,9 @@ DfEntry make_df() {
 }
 
 const DfEntry kDfTable[] = {
-    make_df<16, 18, 16, 8, 12, 16>(),   // C1/C3 grid: Wy 288, Wz 96
-    make_df<24, 24, 8, 12, 16, 16>(),   // C2 grid: Wy 576, Wz 192
-    make_df<30, 36, 8, 12, 12, 16>(),   // C4 grid: Wy 1080, Wz 144
+    make_df<16, 18, 8, 8, 12, 16>(),    // C1/C3 grid: Wy 288, Wz 96
+    make_df<24, 24, 8, 12, 16, 8>(),    // C2 grid: Wy 576, Wz 192
+    make_df<30, 36, 4, 12, 12, 8>(),    // C4 grid: Wy 1080, Wz 144
 };
 
 const DfEntry* df_lookup(int ny, int nz) {

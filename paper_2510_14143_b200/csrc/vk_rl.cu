@@ -183,7 +183,7 @@ struct vk_rl_plan_s {
   const vk::FastEntry* fz = nullptr;
   // one-launch y/z convolution (3D fast grids), see rl_dataflow.cuh
   const vk::DfEntry* df = nullptr;
-  int df_blocks = 0, df_R = 0, df_ntasks = 0, df_nyf = 0, df_nz = 0;
+  int df_blocks = 0, df_R = 0, df_D = 0, df_ntasks = 0, df_nyf = 0, df_nz = 0;
   DevBuf<float2> ring;
   DevBuf<unsigned> df_tasks;
   DevBuf<int> df_ctr;
@@ -374,22 +374,20 @@ void conv_dataflow(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   a.nYi = p->df_nyf;
   ck(cudaMemsetAsync(p->df_ctr.p, 0, p->df_ctr.n * sizeof(int), s), "dataflow counters");
   cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p->df_blocks);
+  cfg.gridDim = dim3(p->df_ntasks);  // one CTA per task, ticket-ordered (rl_dataflow.cuh)
   cfg.blockDim = dim3(p->df->NT);
   cfg.dynamicSmemBytes = p->df->smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[2];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  int nat = 1;
+  cudaLaunchAttribute at[1];
+  int nat = 0;
   if (p->df_window) {
-    at[1].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[1].val.accessPolicyWindow.base_ptr = p->ring.p;
-    at[1].val.accessPolicyWindow.num_bytes = p->df_window;
-    at[1].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[1].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[1].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    nat = 2;
+    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+    at[0].val.accessPolicyWindow.base_ptr = p->ring.p;
+    at[0].val.accessPolicyWindow.num_bytes = p->df_window;
+    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+    nat = 1;
   }
   cfg.attrs = at;
   cfg.numAttrs = nat;
@@ -453,8 +451,11 @@ void setup_dataflow(vk_rl_plan p) {
   const char* lag_env = std::getenv("VK_RL_DF_LAG");
   int D = lag_env ? std::atoi(lag_env) : (p->df_blocks + per_plane - 1) / per_plane + 1;
   D = std::max(1, std::min(D, g.Hx));
-  p->df_R = std::min(2 * D + 2, g.Hx);
-  if (p->df_R < g.Hx && p->df_R <= 2 * D) p->df_R = std::min(2 * D + 1, g.Hx);
+  p->df_D = D;
+  // Yf(p) reuses the slot of Yi(p-R), which sits R-2D steps earlier in the list;
+  // keep that distance >= D so the slot is normally free when Yf starts.
+  const char* ring_env = std::getenv("VK_RL_DF_RING");
+  p->df_R = std::min(ring_env ? std::max(std::atoi(ring_env), 2 * D + 1) : 3 * D + 2, g.Hx);
   std::vector<unsigned> tasks;
   tasks.reserve((size_t)g.Hx * per_plane);
   for (int step = 0; step < g.Hx + 2 * D; ++step) {
@@ -576,8 +577,14 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->fx = vk::fast_lookup(g.Wx);
       p->fy = vk::fast_lookup(g.Wy);
       p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
+      // The one-launch dataflow convolution halves HBM traffic but measured
+      // slower than the 3-launch path at C2 (0.55 vs 0.41 ms per convolution,
+      // profiles/r01/sweep_c2.log): the passes are latency/issue-bound, not
+      // HBM-bound, yet.  Opt-in until that flips.
+      const char* df_env = std::getenv("VK_RL_DATAFLOW");
       const char* nodf = std::getenv("VK_RL_NO_DATAFLOW");
-      if (p->fy && p->fz && !(nodf && nodf[0] == '1')) p->df = vk::df_lookup(g.Wy, g.Wz);
+      if (p->fy && p->fz && df_env && df_env[0] == '1' && !(nodf && nodf[0] == '1'))
+        p->df = vk::df_lookup(g.Wy, g.Wz);
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
@@ -868,6 +875,28 @@ vk_status vk_rl_plan_launches(vk_rl_plan p, uint64_t* launches) {
   return guarded([&] {
     if (!p || !launches) fail(VK_ERR_ARG, "NULL argument");
     *launches = p->launches;
+  });
+}
+
+vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
+  return guarded([&] {
+    if (!p || !buf || len <= 0) fail(VK_ERR_ARG, "NULL argument");
+    const Geom& g = p->g;
+    auto axis = [](const char* n, const vk::FastEntry* f, int L) {
+      return std::string(n) + (f ? ":fast(L=" + std::to_string(L) + ")" : ":generic");
+    };
+    std::string s = "W=" + std::to_string(g.Wz) + "x" + std::to_string(g.Wy) + "x" + std::to_string(g.Wx) +
+                    " P=" + std::to_string(g.Pz) + "x" + std::to_string(g.Py) + "x" + std::to_string(g.Px) + " " +
+                    axis("x", p->fx, p->fx ? p->fx->Lx : p->xL) + " " + axis("y", p->fy, p->fy ? p->fy->Lx : p->yL) +
+                    " " + axis("z", p->fz, p->fz ? p->fz->Lz : p->zL) + " yz:";
+    if (p->df)
+      s += "dataflow(blocks=" + std::to_string(p->df_blocks) + ",D=" + std::to_string(p->df_D) +
+           ",R=" + std::to_string(p->df_R) + ",tasks=" + std::to_string(p->df_ntasks) +
+           ",l2_window=" + std::to_string(p->df_window) + ")";
+    else
+      s += g.Wz > 1 ? "3-pass" : "y-conv";
+    std::strncpy(buf, s.c_str(), (size_t)len - 1);
+    buf[len - 1] = 0;
   });
 }
 

@@ -214,7 +214,7 @@ def _with_env(env, fn):
 
 @pytest.mark.parametrize("name,shape,mk", [
     ("c1_grid_288x96", (64, 256, 256), lambda: O.gaussian_psf((15, 15, 15), 1.75)),
-    ("c2_grid_576x192", (128, 60, 512), lambda: O.widefield_psf(31)),
+    ("c2_grid_576x192", (128, 512, 60), lambda: O.widefield_psf(31)),
     ("c4_grid_1080x144", (100, 1000, 20), lambda: O.gaussian_psf((21, 21, 21), 2.5)),
 ])
 def test_dataflow_yz_conv_matches_three_pass(name, shape, mk):
@@ -225,11 +225,12 @@ def test_dataflow_yz_conv_matches_three_pass(name, shape, mk):
     obs = synth.blurred(synth.blobs(shape, 30, 5, 9, seed=11), psf)
     rule = fixed_rule(3)
     ref = _with_env({"VK_RL_NO_DATAFLOW": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
-    df = vk.richardson_lucy(obs, psf, rule)
-    tight = _with_env({"VK_RL_DF_LAG": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    df = _with_env({"VK_RL_DATAFLOW": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    tight = _with_env({"VK_RL_DATAFLOW": "1", "VK_RL_DF_LAG": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
     assert rel_l2(df.estimate, ref.estimate) <= 1e-6
     assert rel_l2(tight.estimate, ref.estimate) <= 1e-6
-    plan = vk.RlPlan(shape, psf)
+    plan = _with_env({"VK_RL_DATAFLOW": "1"}, lambda: vk.RlPlan(shape, psf))
+    assert "dataflow" in plan.describe(), plan.describe()
     plan.profile(True)
     plan.run(obs, rule)
     prof = plan.profile_read()
