@@ -157,7 +157,8 @@ typedef enum vk_kernel_kind {
   VK_KIND_Y_INV = 5,    /* y-pass inverse                               */
   VK_KIND_Y_CONV = 6,   /* y-pass forward * OTF * inverse (rank <= 2)   */
   VK_KIND_YZ_DATAFLOW = 7, /* one-launch y fwd -> z*OTF*z -> y inv (3D) */
-  VK_KIND_COUNT = 8
+  VK_KIND_YZ_CLUSTER = 8,  /* same, fused on thread-block clusters (DSMEM) */
+  VK_KIND_COUNT = 9
 } vk_kernel_kind;
 
 /* Enable/disable CUDA-event timing of every launch on this plan (events are

@@ -27,7 +27,7 @@ from typing import List, Optional, Sequence
 import numpy as np
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "libvkrl.so")
+LIB_PATH = os.environ.get("VK_RL_LIB") or os.path.join(_HERE, "lib", "libvkrl.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "vk_rl.h")
 
 
@@ -68,7 +68,8 @@ class Unsupported(Error):
     pass
 
 
-KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv", "yz_dataflow")  # vk_kernel_kind
+KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv", "yz_dataflow",
+                "yz_cluster")  # vk_kernel_kind
 
 _STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: DegenerateReference,
            6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported}

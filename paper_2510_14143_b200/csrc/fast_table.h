@@ -17,6 +17,8 @@ struct FastEntry {
   int Lz, NTz;          // z-pass
   size_t smem_z;
   const void* zk;       // zpass_fast<R1,R2,Lz>(ZArgs)
+  size_t smem_zp;
+  const void* zpk;      // zpass_pipe<R1,R2,Lz>(ZArgs): persistent, double-buffered
 };
 
 const FastEntry* fast_lookup(int n);
@@ -59,5 +61,23 @@ struct DfEntry {
   const void* k;  // yzconv_dataflow<...>(DfArgs)
 };
 const DfEntry* df_lookup(int ny, int nz);
+
+// Cluster-fused 3D y/z convolution kernels (rl_cluster.cuh) by (Wy, Wz).
+struct ClArgs {
+  const float2* twy;
+  const float2* twz;
+  Geom g;
+  float2* SA;         // [Hx][Pz][Py], read and written in place
+  const float2* otf;  // [Hx][Wz][Wy]
+};
+struct ClEntry {
+  int Ny, Nz;
+  int C;     // cluster size (CTAs, one per SM)
+  int RZ;    // max z rows per CTA: requires ceil(Pz / C) <= RZ
+  int NT;
+  size_t smem;
+  const void* k;  // yzconv_cluster<...>(ClArgs)
+};
+const ClEntry* cl_lookup(int ny, int nz, int pz);
 
 }  // namespace vk

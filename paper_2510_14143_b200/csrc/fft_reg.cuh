@@ -12,13 +12,16 @@
 // natural order.  Each radix-R DFT runs entirely in registers as a nested
 // Cooley-Tukey over R = A*B with compile-time twiddles (constexpr sin/cos in
 // double, rounded once to float).  Lines are interleaved in shared memory with
-// an XOR swizzle instead of padding: element i of line l lives at
-//     sw<L>(i, l) = i*L + (l ^ (i & (L-1)))
-// so a row (fixed i, L lines) is a permutation of L consecutive float2 (the
-// Stockham passes and kx-row staging are conflict-free) and a column (fixed l,
-// consecutive i — the transposed global<->shared staging) spreads over all
-// banks for 8-byte accesses.  Pass-2 twiddles come from a per-CTA shared
-// table tw[m] = w_N^m (double-evaluated).
+// a one-element pad: element i of line l lives at
+//     sw<L>(i, l) = i*(L+1) + l
+// A row (fixed i, L lines) is L consecutive float2 (Stockham passes, kx-row
+// staging) and a column (fixed l, consecutive i: the transposed
+// global<->shared staging) strides 2L+2 words, which covers all 32 banks per
+// half-warp for 8-byte accesses.  Unlike an XOR swizzle, every address in an
+// unrolled pass is a per-thread base plus a compile-time immediate, which
+// removes most integer address arithmetic from the transforms (measured:
+// ~45% of zpass instructions were LEA/IADD3/LOP3 with the swizzle).  Pass-2
+// twiddles come from a per-CTA shared table tw[m] = w_N^m (double-evaluated).
 #pragma once
 #include <cuda_runtime.h>
 
@@ -151,6 +154,19 @@ __device__ __forceinline__ void load_twiddles(float2* tw_s, const float2* __rest
   for (int i = threadIdx.x; i < n; i += blockDim.x) tw_s[i] = tw_g[i];
 }
 
+// Pass-2 twiddles of fft2<R1, R2> laid out by butterfly: tw_s[j*R2 + r] =
+// w_N^{r j} (j < R1, r < R2) gathered from the natural table tw_g[m] = w_N^m
+// (r j < N, no reduction needed).  A pass-2 butterfly then reads its R2-1
+// twiddles at one base address plus compile-time offsets instead of holding
+// R2-1 separate address registers.
+template <int R1, int R2>
+__device__ __forceinline__ void load_twiddles2(float2* tw_s, const float2* __restrict__ tw_g) {
+  for (int i = threadIdx.x; i < R1 * R2; i += blockDim.x) {
+    const int j = i / R2, r = i - j * R2;
+    tw_s[i] = tw_g[r * j];
+  }
+}
+
 // threadIdx.x through a volatile asm: index math derived from it cannot be
 // hoisted out of a persistent task loop (which otherwise keeps every unrolled
 // shared-memory address of the transform live in registers across tasks).
@@ -162,7 +178,7 @@ __device__ __forceinline__ int fresh_tid() {
 
 template <int L>
 __device__ __forceinline__ int sw(int i, int l) {
-  return i * L + (l ^ (i & (L - 1)));
+  return i * (L + 1) + l;
 }
 
 // In-place two-pass transform of L interleaved (swizzled) lines of
@@ -170,19 +186,23 @@ __device__ __forceinline__ int sw(int i, int l) {
 // must cover every pass-1 butterfly with one thread (NT >= L*R2) so pass 1 can
 // stage its inputs in registers, sync, and overwrite in place; pass 2 reads
 // and writes the same index set per thread.  Caller syncs before.
-template <int R1, int R2, int L, int NT, bool INV>
-__device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __restrict__ tw) {
+template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1>
+__device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
   static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
+#ifdef VK_DEBUG_NOFFT  // experiment builds only: isolate the memory cost of a pass
+  __syncthreads();
+  return;
+#endif
   {
     const int t = fresh_tid();
     const int l = t % L, j = t / L;
     const bool act = t < L * R2;
     float2 v[R1];
-    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[sw<L>(j + decltype(r)::value * R2, l)]; });
+    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l]; });
     __syncthreads();
     if (act) {
       rdft<R1, INV>(v);
-      static_for<0, R1>([&](auto q) { buf[sw<L>(j * R1 + decltype(q)::value, l)] = v[decltype(q)::value]; });
+      static_for<0, R1>([&](auto q) { buf[(j * R1 + decltype(q)::value) * LP + l] = v[decltype(q)::value]; });
     }
     __syncthreads();
   }
@@ -190,15 +210,15 @@ __device__ __forceinline__ void fft2(float2* __restrict__ buf, const float2* __r
   for (int t = fresh_tid(); t < L * R1; t += NT) {
     const int l = t % L, j = t / L;
     float2 v[R2];
-    v[0] = buf[sw<L>(j, l)];
+    v[0] = buf[j * LP + l];
     static_for<1, R2>([&](auto r) {
       constexpr int rr = decltype(r)::value;
-      const float2 w = tw[rr * j];
-      const float2 x = buf[sw<L>(j + rr * R1, l)];
+      const float2 w = tw[j * R2 + rr];  // load_twiddles2 layout
+      const float2 x = buf[(j + rr * R1) * LP + l];
       v[rr] = INV ? cmulc(x, w) : cmul(x, w);
     });
     rdft<R2, INV>(v);
-    static_for<0, R2>([&](auto q) { buf[sw<L>(j + decltype(q)::value * R1, l)] = v[decltype(q)::value]; });
+    static_for<0, R2>([&](auto q) { buf[(j + decltype(q)::value * R1) * LP + l] = v[decltype(q)::value]; });
   }
   __syncthreads();
 }

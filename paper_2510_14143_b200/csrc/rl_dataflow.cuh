@@ -39,7 +39,8 @@ struct DfCfg {
   static constexpr int NY = YR1 * YR2, NZ = ZR1 * ZR2;
   static constexpr int NT = FastCfg<YR1, YR2, YL>::NT > FastCfg<ZR1, ZR2, ZL>::NT ? FastCfg<YR1, YR2, YL>::NT
                                                                                   : FastCfg<ZR1, ZR2, ZL>::NT;
-  static constexpr int WORK = NY * YL > 2 * NZ * ZL ? NY * YL : 2 * NZ * ZL;
+  static constexpr int WORK_Y = NY * (YL + 1), WORK_Z = NZ * (ZL + 1) + NZ * ZL;  // padded blocks (+ OTF tile)
+  static constexpr int WORK = WORK_Y > WORK_Z ? WORK_Y : WORK_Z;
   static constexpr size_t smem = (size_t)((NY > NZ ? NY : NZ) + WORK) * sizeof(float2);
   // resident CTAs per SM the register budget is sized for (smem-limited)
   static constexpr int MINB_SMEM = (int)((227u * 1024u) / (smem + 1024u));
@@ -136,9 +137,9 @@ __global__ void __launch_bounds__(DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>::NT, DfCfg<Y
   const unsigned code = a.tasks[t];
   const unsigned type = code >> 30, p = (code >> 14) & 0xffffu, c = code & 0x3fffu;
   if (type == DF_Z)
-    reg::load_twiddles(tw, a.twz, NZ);
+    reg::load_twiddles2<ZR1, ZR2>(tw, a.twz);
   else
-    reg::load_twiddles(tw, a.twy, NY);
+    reg::load_twiddles2<YR1, YR2>(tw, a.twy);
   if (threadIdx.x == 0) {
     const int* dep = nullptr;
     int need = 0;
@@ -170,7 +171,7 @@ __global__ void __launch_bounds__(DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>::NT, DfCfg<Y
     df_y_task<YR1, YR2, YL, NT, false>(W, tw, a.SA + ((size_t)p * g.Pz + z0) * g.Py, g.Py, g.Py, nv,
                                        slot + (size_t)z0 * g.Wy, g.Wy, g.Wy, 0);
   } else if (type == DF_Z) {
-    df_z_task<ZR1, ZR2, ZL, NT>(W, W + NZ * ZL, tw, slot, g.Wy, g.Pz, g.Pz, g.cz,
+    df_z_task<ZR1, ZR2, ZL, NT>(W, W + NZ * (ZL + 1), tw, slot, g.Wy, g.Pz, g.Pz, g.cz,
                                 a.otf + (size_t)p * NZ * g.Wy, c * ZL);
   } else {
     const int z0 = c * YL, nv = min(YL, g.Pz - z0);

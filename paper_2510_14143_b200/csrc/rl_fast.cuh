@@ -3,7 +3,7 @@
 // these differences:
 //
 //  * the line transform is fft_reg.cuh's two-pass register FFT, in place in
-//    ONE shared buffer with the XOR-swizzled line layout sw<L>(i, l);
+//    ONE shared buffer with the padded line layout sw<L>(i, l) = i*(L+1) + l;
 //  * the x crop offset cx (deconv.cpp:59-72) is realised as a phase ramp
 //    exp(+2 pi i cx kx / Wx) folded into both OTFs at plan creation, so a
 //    P-domain row lives at slots [cx, cx+Px) of its length-Wx line before the
@@ -35,10 +35,11 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 
 template <int R1, int R2, int L, bool OTF_PREFETCH = false>
 struct FastCfg {
-  static_assert((L & (L - 1)) == 0, "L must be a power of two (swizzle)");
+  static_assert((L & (L - 1)) == 0, "L must be a power of two (cheap line/index split)");
   static constexpr int N = R1 * R2;
   static constexpr int NT = ((L * (R1 > R2 ? R1 : R2)) + 31) / 32 * 32;
-  static constexpr size_t smem = (size_t)(N * L + N + (OTF_PREFETCH ? N * L : 0)) * sizeof(float2);
+  static constexpr int DATA = N * (L + 1);  // padded line block, see reg::sw
+  static constexpr size_t smem = (size_t)(DATA + N + (OTF_PREFETCH ? N * L : 0)) * sizeof(float2);
 };
 
 template <int R1, int R2, int L>
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   extern __shared__ float2 smem[];
   float2* tw = smem;
   float2* A = smem + N;
-  reg::load_twiddles(tw, a.plan.tw, N);
+  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
   const int z = blockIdx.y;
   const int y0 = blockIdx.x * 2 * L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -83,30 +84,37 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
       }
     }
   } else {
-    // Hermitian halves of row pair (l, L+l) -> Z[k] = Xa[k] + i Xb[k], k < N
+    // Hermitian halves of row pair (l, L+l) -> Z[k] = Xa[k] + i Xb[k], k < N.
+    // NT is a multiple of L, so a thread keeps one line l and strides kx by
+    // NT/L; spectrum offsets are 32-bit and incremental.
+    constexpr int KS = NT / L;  // kx stride per thread
     const float2 zero = make_float2(0.f, 0.f);
-    for (int base = threadIdx.x; base < Hx * L; base += NT * U) {
-      float2 xa[U], xb[U];
+    {
+      const int l = threadIdx.x & (L - 1);
+      const int ya = y0 + l, yb = y0 + L + l;
+      const bool va = ya < g.Py, vb = yb < g.Py;
+      const float2* Sa = a.S + ((unsigned)z * g.Py + (va ? ya : 0));
+      const float2* Sb = a.S + ((unsigned)z * g.Py + (vb ? yb : 0));
+      const unsigned plane = (unsigned)g.Pz * g.Py;
+      for (int kx0 = threadIdx.x / L; kx0 < Hx; kx0 += KS * U) {
+        float2 xa[U], xb[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = base + u * NT;
-        const int kx = idx / L, l = idx % L;
-        const size_t row = ((size_t)kx * g.Pz + z) * g.Py;
-        const int ya = y0 + l, yb = y0 + L + l;
-        const bool ok = idx < Hx * L;
-        xa[u] = (ok && ya < g.Py) ? a.S[row + ya] : zero;
-        xb[u] = (ok && yb < g.Py) ? a.S[row + yb] : zero;
-      }
+        for (int u = 0; u < U; ++u) {
+          const int kx = kx0 + u * KS;
+          const bool ok = kx < Hx;
+          xa[u] = (ok && va) ? Sa[(unsigned)kx * plane] : zero;
+          xb[u] = (ok && vb) ? Sb[(unsigned)kx * plane] : zero;
+        }
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int idx = base + u * NT;
-        if (idx >= Hx * L) break;
-        const int kx = idx / L, l = idx % L;
-        if (kx == 0 || 2 * kx == N) {
-          A[sw<L>(kx, l)] = make_float2(xa[u].x, xb[u].x);  // imaginary parts of DC/Nyquist dropped (c2r)
-        } else {
-          A[sw<L>(kx, l)] = make_float2(xa[u].x - xb[u].y, xa[u].y + xb[u].x);
-          A[sw<L>(N - kx, l)] = make_float2(xa[u].x + xb[u].y, xb[u].x - xa[u].y);
+        for (int u = 0; u < U; ++u) {
+          const int kx = kx0 + u * KS;
+          if (kx >= Hx) break;
+          if (kx == 0 || 2 * kx == N) {
+            A[sw<L>(kx, l)] = make_float2(xa[u].x, xb[u].x);  // imaginary parts of DC/Nyquist dropped (c2r)
+          } else {
+            A[sw<L>(kx, l)] = make_float2(xa[u].x - xb[u].y, xa[u].y + xb[u].x);
+            A[sw<L>(N - kx, l)] = make_float2(xa[u].x + xb[u].y, xb[u].x - xa[u].y);
+          }
         }
       }
     }
@@ -119,14 +127,26 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
     // work item = (line l, chunk of CH samples); one warp per item, U samples
     // of both rows of the line per lane
     const int nch = (g.Px + CH - 1) / CH;
-    for (int item = warp; item < L * nch; item += NW) {
-      const int l = item / nch, x0 = (item % nch) * CH;
+    // items (l, ch) walked with incremental carries instead of div/mod
+    int l = 0, ch = warp;
+    while (ch >= nch) {
+      ch -= nch;
+      ++l;
+    }
+    const int iz = z - g.oz;
+    const bool zin = iz >= 0 && iz < g.Iz;
+    const size_t zoff = (size_t)clampi(iz, 0, g.Iz - 1) * g.Iy;
+    for (; l < L; ch += NW) {
+      while (ch >= nch) {
+        ch -= nch;
+        ++l;
+      }
+      if (l >= L) break;
+      const int x0 = ch * CH;
       const int ya = y0 + l, yb = y0 + L + l;
       const bool va = ya < g.Py, vb = yb < g.Py;
-      const int iz = z - g.oz, iya = ya - g.oy, iyb = yb - g.oy;
-      const bool zin = iz >= 0 && iz < g.Iz;
+      const int iya = ya - g.oy, iyb = yb - g.oy;
       const bool ina = va && zin && iya >= 0 && iya < g.Iy, inb = vb && zin && iyb >= 0 && iyb < g.Iy;
-      const size_t zoff = (size_t)clampi(iz, 0, g.Iz - 1) * g.Iy;
       const size_t oa_off = (zoff + clampi(iya, 0, g.Iy - 1)) * g.Ix;
       const size_t ob_off = (zoff + clampi(iyb, 0, g.Iy - 1)) * g.Ix;
       const float* oa = a.obs + oa_off;
@@ -155,10 +175,12 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
         const bool xin = ix >= 0 && ix < g.Ix;
         float2 val;
         if (ratio) {
+          // fast reciprocal/log (<= 2 ulp / 2^-21 abs): the f32 path's own
+          // rounding (~1e-7 rel) dominates either way
           const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
-          val = make_float2(va ? o_a[u] / ma : 0.f, vb ? o_b[u] / mb : 0.f);
-          if (xin && ina) f0 += fmaf(o_a[u], logf(ma), -ma);
-          if (xin && inb) f0 += fmaf(o_b[u], logf(mb), -mb);
+          val = make_float2(va ? __fdividef(o_a[u], ma) : 0.f, vb ? __fdividef(o_b[u], mb) : 0.f);
+          if (xin && ina) f0 += fmaf(o_a[u], __logf(ma), -ma);
+          if (xin && inb) f0 += fmaf(o_b[u], __logf(mb), -mb);
         } else {
           val = make_float2(va ? fmaxf(e_a[u] * m[u].x, 0.f) : 0.f, vb ? fmaxf(e_b[u] * m[u].y, 0.f) : 0.f);
           if (!last) {
@@ -201,15 +223,21 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false>(A, tw);
-  for (int idx = threadIdx.x; idx < Hx * L; idx += NT) {
-    const int kx = idx / L, l = idx % L;
-    const float2 zk = A[sw<L>(kx, l)];
-    const float2 zn = A[sw<L>(kx == 0 ? 0 : N - kx, l)];
-    const float2 xa = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-    const float2 xb = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
-    const size_t row = ((size_t)kx * a.rows_z + z) * a.rows_y;
-    if (y0 + l < a.rows_y) a.S[row + y0 + l] = xa;
-    if (y0 + L + l < a.rows_y) a.S[row + y0 + L + l] = xb;
+  {
+    constexpr int KS = NT / L;
+    const int l = threadIdx.x & (L - 1);
+    const bool va = y0 + l < a.rows_y, vb = y0 + L + l < a.rows_y;
+    float2* Sa = a.S + ((unsigned)z * a.rows_y + y0 + l);
+    float2* Sb = Sa + L;
+    const unsigned plane = (unsigned)a.rows_z * a.rows_y;
+    for (int kx = threadIdx.x / L; kx < Hx; kx += KS) {
+      const float2 zk = A[sw<L>(kx, l)];
+      const float2 zn = A[sw<L>(kx == 0 ? 0 : N - kx, l)];
+      const float2 xa = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
+      const float2 xb = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
+      if (va) Sa[(unsigned)kx * plane] = xa;
+      if (vb) Sb[(unsigned)kx * plane] = xb;
+    }
   }
 }
 
@@ -221,7 +249,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   extern __shared__ float2 smem[];
   float2* tw = smem;
   float2* A = smem + N;
-  float2* O = A + N * L;  // OTF tile [l][k] (CONV only)
+  float2* O = A + C::DATA;  // OTF tile [l][k] (CONV only)
   const int line0 = blockIdx.x * L;
   // async copies: the L input rows (zero padding written directly)
   for (int l = 0; l < L; ++l) {
@@ -245,7 +273,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     }
     cp_async_commit();
   }
-  reg::load_twiddles(tw, a.plan.tw, N);
+  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
   if (a.mode == YM_CONV)
     cp_async_wait_1();  // input rows landed, OTF may still fly
   else
@@ -282,30 +310,40 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   extern __shared__ float2 smem[];
   float2* tw = smem;
   float2* A = smem + N;
-  float2* O = A + N * L;  // OTF tile, [kz][l] row-major (pitch L)
+  float2* O = A + C::DATA;  // OTF tile, [kz][l] row-major (pitch L)
+  // NT is a multiple of L: a thread owns one column l (ky = ky0 + l) and
+  // strides z by ZS = NT/L; offsets are 32-bit and compile-time unrolled.
+  constexpr int ZS = NT / L;
+  constexpr int IT = (N + ZS - 1) / ZS;
   const int kx = blockIdx.y;
-  const int ky0 = blockIdx.x * L;
-  const size_t plane = (size_t)kx * a.zrows * a.Wy;
-  const size_t oplane = (size_t)kx * N * a.Wy;
-  for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-    const int z = idx / L, l = idx % L;
-    const int ky = ky0 + l;
-    if (z < a.n_in && ky < a.Wy)
-      cp_async8(&A[sw<L>(z, l)], &a.S[plane + (size_t)z * a.Wy + ky]);
-    else
-      A[sw<L>(z, l)] = make_float2(0.f, 0.f);
+  const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
+  const int ky = blockIdx.x * L + l;
+  const bool kok = ky < a.Wy;
+  float2* col = a.S + ((unsigned)kx * a.zrows * a.Wy + (kok ? ky : 0));
+  const unsigned oplane = (unsigned)kx * N * a.Wy + (kok ? ky : 0);
+  const unsigned Wy = a.Wy;
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {
+    const int z = z0 + k * ZS;
+    if (z < N) {
+      if (kok && z < a.n_in)
+        cp_async8(&A[sw<L>(z, l)], &col[(unsigned)z * Wy]);
+      else
+        A[sw<L>(z, l)] = make_float2(0.f, 0.f);
+    }
   }
   cp_async_commit();
   const bool conv = a.mode == ZM_CONV;
   if (conv) {
-    for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-      const int kz = idx / L, l = idx % L;
-      const int ky = ky0 + l;
-      if (ky < a.Wy) cp_async8(&O[idx], &a.otf[oplane + (size_t)kz * a.Wy + ky]);
+    const float2* o = a.otf + oplane;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N && kok) cp_async8(&O[z * L + l], &o[(unsigned)z * Wy]);
     }
     cp_async_commit();
   }
-  reg::load_twiddles(tw, a.plan.tw, N);
+  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
   if (conv)
     cp_async_wait_1();
   else
@@ -313,26 +351,102 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false>(A, tw);
   if (!conv) {
-    for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-      const int kz = idx / L, l = idx % L;
-      const int ky = ky0 + l;
-      if (ky < a.Wy) a.otf_out[oplane + (size_t)kz * a.Wy + ky] = A[sw<L>(kz, l)];
+    float2* o = a.otf_out + oplane;
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N && kok) o[(unsigned)z * Wy] = A[sw<L>(z, l)];
     }
     return;
   }
   cp_async_wait_all();
   __syncthreads();
-  for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-    const int kz = idx / L, l = idx % L;
-    A[sw<L>(kz, l)] = cmul(A[sw<L>(kz, l)], O[idx]);
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {
+    const int z = z0 + k * ZS;
+    if (z < N) A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], O[z * L + l]);
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true>(A, tw);
-  for (int idx = threadIdx.x; idx < a.n_out * L; idx += NT) {
-    const int z = idx / L, l = idx % L;
-    const int ky = ky0 + l;
-    if (ky < a.Wy) a.S[plane + (size_t)z * a.Wy + ky] = A[sw<L>(z + a.out_off, l)];
+  if (kok) {
+    for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[sw<L>(z + a.out_off, l)];
   }
+}
+
+// Persistent, double-buffered z convolution: each CTA walks tiles
+// (kx, ky-chunk) with stride gridDim.x and keeps the NEXT tile's column block
+// and OTF block in flight (cp.async group) while it transforms the current
+// one, so HBM latency hides behind the FFT even at 2 CTAs per SM.
+template <int R1, int R2, int L>
+struct ZPipeCfg {
+  static constexpr int N = R1 * R2;
+  static constexpr int NT = FastCfg<R1, R2, L, true>::NT;
+  static constexpr int STAGE = N * (L + 1) + N * L;  // padded data block + OTF tile
+  static constexpr size_t smem = (size_t)(N + 2 * STAGE) * sizeof(float2);  // tw + 2 stages
+};
+
+template <int R1, int R2, int L>
+__global__ void __launch_bounds__(ZPipeCfg<R1, R2, L>::NT, 2)
+    zpass_pipe(const ZArgs a) {
+  using C = ZPipeCfg<R1, R2, L>;
+  constexpr int N = C::N, NT = C::NT;
+  constexpr int ZS = NT / L;
+  constexpr int IT = (N + ZS - 1) / ZS;
+  extern __shared__ float2 smem[];
+  float2* tw = smem;
+  float2* buf = smem + N;  // stage s: padded data at buf + s*STAGE, OTF tile right after
+  const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
+  const unsigned Wy = a.Wy;
+  const int nchunks = (a.Wy + L - 1) / L;
+  const int ntiles = nchunks * a.hx;
+  auto issue = [&](int tile, int stage) {
+    float2* A = buf + stage * C::STAGE;
+    float2* O = A + N * (L + 1);
+    const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
+    const bool kok = ky < a.Wy;
+    const float2* col = a.S + ((unsigned)kx * a.zrows * Wy + (kok ? ky : 0));
+    const float2* o = a.otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N) {
+        if (kok && z < a.n_in)
+          cp_async8(&A[sw<L>(z, l)], &col[(unsigned)z * Wy]);
+        else
+          A[sw<L>(z, l)] = make_float2(0.f, 0.f);
+        if (kok) cp_async8(&O[z * L + l], &o[(unsigned)z * Wy]);
+      }
+    }
+  };
+  int tile = blockIdx.x;
+  if (tile < ntiles) issue(tile, 0);
+  cp_async_commit();
+  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
+    const int stage = it & 1;
+    const int next = tile + gridDim.x;
+    if (next < ntiles) issue(next, stage ^ 1);
+    cp_async_commit();
+    cp_async_wait_1();  // the current tile's group has landed
+    __syncthreads();
+    float2* A = buf + stage * C::STAGE;
+    const float2* O = A + N * (L + 1);
+    reg::fft2<R1, R2, L, NT, false>(A, tw);
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N) A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], O[z * L + l]);
+    }
+    __syncthreads();
+    reg::fft2<R1, R2, L, NT, true>(A, tw);
+    const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
+    if (ky < a.Wy) {
+      float2* col = a.S + ((unsigned)kx * a.zrows * Wy + ky);
+      for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[sw<L>(z + a.out_off, l)];
+    }
+    __syncthreads();  // stage is refilled two tiles later
+  }
+  cp_async_wait_all();
 }
 
 // Phase ramp exp(+2 pi i cx kx / Wx) over an OTF laid out [Hx][Wz][Wy].

@@ -4,6 +4,7 @@
 // length runs the generic Stockham kernels of rl_passes.cuh.
 #define VK_NO_GENERIC_KERNELS
 #include "fast_table.h"
+#include "rl_cluster.cuh"
 #include "rl_dataflow.cuh"
 
 namespace vk {
@@ -24,6 +25,8 @@ FastEntry make_entry() {
   e.NTz = FastCfg<R1, R2, LZ, true>::NT;
   e.smem_z = FastCfg<R1, R2, LZ, true>::smem;
   e.zk = (const void*)zpass_fast<R1, R2, LZ>;
+  e.smem_zp = ZPipeCfg<R1, R2, LZ>::smem;
+  e.zpk = (const void*)zpass_pipe<R1, R2, LZ>;
   return e;
 }
 
@@ -58,6 +61,24 @@ const DfEntry kDfTable[] = {
     make_df<30, 36, 4, 12, 12, 8>(),    // C4 grid: Wy 1080, Wz 144
 };
 
+template <int YR1, int YR2, int ZR1, int ZR2, int C, int RZ, int ZG, int NT>
+ClEntry make_cl() {
+  using K = ClCfg<YR1, YR2, ZR1, ZR2, C, RZ, ZG, NT>;
+  return ClEntry{K::NY, K::NZ, C, RZ, NT, K::smem, (const void*)yzconv_cluster<YR1, YR2, ZR1, ZR2, C, RZ, ZG, NT>};
+}
+
+const ClEntry kClTable[] = {
+    make_cl<16, 18, 8, 12, 4, 20, 24, 384>(),    // C1/C3 grid: Wy 288, Wz 96, Pz <= 80
+    make_cl<24, 24, 12, 16, 12, 14, 24, 384>(),  // C2 grid: Wy 576, Wz 192, Pz <= 168
+    make_cl<30, 36, 12, 12, 12, 10, 30, 384>(),  // C4 grid: Wy 1080, Wz 144, Pz <= 120
+};
+
+const ClEntry* cl_lookup(int ny, int nz, int pz) {
+  for (const auto& e : kClTable)
+    if (e.Ny == ny && e.Nz == nz && (pz + e.C - 1) / e.C <= e.RZ) return &e;
+  return nullptr;
+}
+
 const DfEntry* df_lookup(int ny, int nz) {
   for (const auto& e : kDfTable)
     if (e.Ny == ny && e.Nz == nz) return &e;
@@ -65,6 +86,11 @@ const DfEntry* df_lookup(int ny, int nz) {
 }
 
 cudaError_t fast_init_attributes() {
+  for (const auto& e : kClTable) {
+    cudaError_t r = cudaFuncSetAttribute(e.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
+    if (r) return r;
+    if (e.C > 8 && (r = cudaFuncSetAttribute(e.k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1))) return r;
+  }
   for (const auto& e : kDfTable) {
     cudaError_t r = cudaFuncSetAttribute(e.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
     if (r) return r;
@@ -74,6 +100,10 @@ cudaError_t fast_init_attributes() {
     if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_x))) return r;
     if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yconv))) return r;
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
+    if ((r = cudaFuncSetAttribute(e.zpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zp))) return r;
+    // prefer the full shared-memory carveout: occupancy is smem-limited
+    for (const void* k : {e.xk, e.yk, e.zk, e.zpk})
+      if ((r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100))) return r;
   }
   return cudaSuccess;
 }

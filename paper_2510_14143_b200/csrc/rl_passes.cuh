@@ -87,6 +87,7 @@ struct ZArgs {
   float2* S;            // [Hx][zrows][Wy]
   const float2* otf;    // [Hx][Wz][Wy]
   float2* otf_out;      // FWD_OUT: [Hx][Wz][Wy]
+  int hx;               // number of kx planes (persistent kernels)
 };
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }

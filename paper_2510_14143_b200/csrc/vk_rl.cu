@@ -188,6 +188,10 @@ struct vk_rl_plan_s {
   DevBuf<unsigned> df_tasks;
   DevBuf<int> df_ctr;
   size_t df_window = 0;
+  int zpipe_blocks = 0;  // > 0: persistent double-buffered z convolution
+  // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
+  const vk::ClEntry* cl = nullptr;
+  int cl_clusters = 0;
   int xL = 1, yL = 1, zL = 1;
   size_t xs = 0, ys = 0, zs = 0;
 
@@ -343,6 +347,14 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   a.S = S;
   a.otf = otf;
   a.otf_out = otf_out;
+  a.hx = p->g.Hx;
+  if (p->fz && p->zpipe_blocks && mode == vk::ZM_CONV) {
+    const size_t t = prof_begin(p, s);
+    launch(p->fz->zpk, dim3(p->zpipe_blocks), p->fz->NTz, p->fz->smem_zp, s, &a);
+    launch_check(p, "zpass pipe");
+    prof_end(p, s, VK_KIND_Z_CONV, t);
+    return;
+  }
   dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
   const size_t t = prof_begin(p, s);
   if (p->fz)
@@ -398,9 +410,39 @@ void conv_dataflow(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   prof_end(p, s, VK_KIND_YZ_DATAFLOW, t);
 }
 
+void conv_cluster(vk_rl_plan p, cudaStream_t s, const float2* otf) {
+  vk::ClArgs a{};
+  a.twy = p->twy.p;
+  a.twz = p->twz.p;
+  a.g = p->g;
+  a.SA = p->SA.p;
+  a.otf = otf;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(p->cl_clusters * p->cl->C);
+  cfg.blockDim = dim3(p->cl->NT);
+  cfg.dynamicSmemBytes = p->cl->smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = p->cl->C;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  void* args[] = {&a};
+  const size_t t = prof_begin(p, s);
+  ck(cudaLaunchKernelExC(&cfg, p->cl->k, args), "cluster launch");
+  launch_check(p, "yz cluster");
+  prof_end(p, s, VK_KIND_YZ_CLUSTER, t);
+}
+
 void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   const Geom& g = p->g;
   const int nl = g.Hx * g.Pz;
+  if (p->cl) {
+    conv_cluster(p, s, otf);
+    return;
+  }
   if (p->df) {
     conv_dataflow(p, s, otf);
     return;
@@ -577,6 +619,42 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->fx = vk::fast_lookup(g.Wx);
       p->fy = vk::fast_lookup(g.Wy);
       p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
+      // Cluster/DSMEM fusion of the y/z convolution: opt-in.  Measured slower
+      // than the 3-launch path (C2: 2.07 vs 0.41 ms per convolution, C1: 0.15
+      // vs 0.06; profiles/r01/sweep_c2e.log) -- one CTA per SM with
+      // serialized load/transform/exchange phases cannot hide latency.
+      const char* cl_env = std::getenv("VK_RL_CLUSTER");
+      if (p->fy && p->fz && g.Wz > 1 && cl_env && cl_env[0] == '1') {
+        p->cl = vk::cl_lookup(g.Wy, g.Wz, g.Pz);
+        if (p->cl) {
+          cudaLaunchConfig_t cfg{};
+          cfg.blockDim = dim3(p->cl->NT);
+          cfg.dynamicSmemBytes = p->cl->smem;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = p->cl->C;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          cfg.gridDim = dim3(p->cl->C);
+          int ncl = 0;
+          if (cudaOccupancyMaxActiveClusters(&ncl, p->cl->k, &cfg) != cudaSuccess || ncl < 1) {
+            cudaGetLastError();
+            p->cl = nullptr;  // cluster shape not schedulable here: 3-launch path
+          } else {
+            p->cl_clusters = ncl;
+          }
+        }
+      }
+      const char* zp = std::getenv("VK_RL_ZPIPE");
+      if (p->fz && zp && zp[0] == '1') {
+        int nsm = 0, per = 0, dev = 0;
+        ck(cudaGetDevice(&dev), "device");
+        ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
+        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p->fz->zpk, p->fz->NTz, p->fz->smem_zp), "occ");
+        p->zpipe_blocks = per * nsm;
+      }
       // The one-launch dataflow convolution halves HBM traffic but measured
       // slower than the 3-launch path at C2 (0.55 vs 0.41 ms per convolution,
       // profiles/r01/sweep_c2.log): the passes are latency/issue-bound, not
@@ -830,6 +908,7 @@ uint64_t alg_bytes(vk_rl_plan p, int kind) {
     case VK_KIND_Y_INV: return 8 * Sb + 8 * Sp;
     case VK_KIND_Y_CONV: return 16 * Sp + 8 * So;
     case VK_KIND_YZ_DATAFLOW: return 16 * Sp + 8 * So;
+    case VK_KIND_YZ_CLUSTER: return 16 * Sp + 8 * So;
     default: return 0;
   }
 }
@@ -889,7 +968,10 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
                     " P=" + std::to_string(g.Pz) + "x" + std::to_string(g.Py) + "x" + std::to_string(g.Px) + " " +
                     axis("x", p->fx, p->fx ? p->fx->Lx : p->xL) + " " + axis("y", p->fy, p->fy ? p->fy->Lx : p->yL) +
                     " " + axis("z", p->fz, p->fz ? p->fz->Lz : p->zL) + " yz:";
-    if (p->df)
+    if (p->cl)
+      s += "cluster(C=" + std::to_string(p->cl->C) + ",clusters=" + std::to_string(p->cl_clusters) +
+           ",NT=" + std::to_string(p->cl->NT) + ",smem=" + std::to_string(p->cl->smem) + ")";
+    else if (p->df)
       s += "dataflow(blocks=" + std::to_string(p->df_blocks) + ",D=" + std::to_string(p->df_D) +
            ",R=" + std::to_string(p->df_R) + ",tasks=" + std::to_string(p->df_ntasks) +
            ",l2_window=" + std::to_string(p->df_window) + ")";

@@ -217,24 +217,26 @@ def _with_env(env, fn):
     ("c2_grid_576x192", (128, 512, 60), lambda: O.widefield_psf(31)),
     ("c4_grid_1080x144", (100, 1000, 20), lambda: O.gaussian_psf((21, 21, 21), 2.5)),
 ])
-def test_dataflow_yz_conv_matches_three_pass(name, shape, mk):
-    """The one-launch y/z convolution (persistent dataflow kernel, ring of
-    planes with completion counters) against the 3-launch path, with the
-    default lag and with lag 1 (ring of 4 planes: maximal slot reuse)."""
+def test_fused_yz_conv_matches_three_pass(name, shape, mk):
+    """The two one-launch y/z convolutions (opt-in) against the default
+    3-launch path: the ticket-ordered dataflow kernel (ring of planes with
+    completion counters; default lag and lag 1 = maximal slot reuse) and the
+    thread-block-cluster kernel (DSMEM transposes)."""
     psf = mk()
     obs = synth.blurred(synth.blobs(shape, 30, 5, 9, seed=11), psf)
     rule = fixed_rule(3)
-    ref = _with_env({"VK_RL_NO_DATAFLOW": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
-    df = _with_env({"VK_RL_DATAFLOW": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    ref = vk.richardson_lucy(obs, psf, rule)
+    for env, kind in (({"VK_RL_DATAFLOW": "1"}, "yz_dataflow"), ({"VK_RL_CLUSTER": "1"}, "yz_cluster")):
+        fused = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule))
+        assert rel_l2(fused.estimate, ref.estimate) <= 1e-6, env
+        plan = _with_env(env, lambda: vk.RlPlan(shape, psf))
+        assert kind.split("_")[1] in plan.describe(), plan.describe()
+        plan.profile(True)
+        plan.run(obs, rule)
+        prof = plan.profile_read()
+        assert prof[kind][1] == 2 * 3, prof  # two convolutions per iteration, one launch each
     tight = _with_env({"VK_RL_DATAFLOW": "1", "VK_RL_DF_LAG": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
-    assert rel_l2(df.estimate, ref.estimate) <= 1e-6
     assert rel_l2(tight.estimate, ref.estimate) <= 1e-6
-    plan = _with_env({"VK_RL_DATAFLOW": "1"}, lambda: vk.RlPlan(shape, psf))
-    assert "dataflow" in plan.describe(), plan.describe()
-    plan.profile(True)
-    plan.run(obs, rule)
-    prof = plan.profile_read()
-    assert prof["yz_dataflow"][1] == 2 * 3, prof  # two convolutions per iteration, one launch each
     its, _ = run_oracle(obs, psf, 1)
     r1 = vk.richardson_lucy(obs, psf, fixed_rule(1))
     assert rel_l2(r1.estimate, its[0]) <= TOL_1

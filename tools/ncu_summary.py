@@ -69,8 +69,43 @@ def launches(path):
         print(f"| {k} | {cnt[k]} | {tot[k]:.1f} | {tot[k] / cnt[k]:.1f} | {tot[k] / s:.3f} |")
 
 
-if __name__ == "__main__":
+if __name__ == "__main__" and sys.argv[1] != "--source":
     if sys.argv[1] == "--launches":
         launches(sys.argv[2])
     else:
         report(sys.argv[1])
+
+
+def source_hotspots(path, kernel_regex, top=25):
+    """Per CUDA source line: warp-instructions executed and stall samples
+    (needs a capture with --import-source on and -lineinfo)."""
+    raw = subprocess.run(["ncu", "-i", path, "--page", "source", "--csv", "--print-source", "cuda,sass",
+                          "-k", f"regex:{kernel_regex}"], capture_output=True, text=True).stdout
+    rows, cur_file, header = [], None, None
+    for r in csv.reader(io.StringIO(raw)):
+        if len(r) == 2 and r[0] in ("File Path", "File Name"):
+            cur_file = r[1].split("/")[-1]
+        elif r and r[0] == "Line No":
+            header = r
+        elif header and len(r) == len(header) and r[0].isdigit() and r[2] == "-":
+            d = dict(zip(header, r))
+            def num(k):
+                try:
+                    return float(d.get(k, "0").replace(",", ""))
+                except ValueError:
+                    return 0.0
+            stalls = {k: num(k) for k in header if k.startswith("stall_") and "Not Issued" not in k}
+            rows.append((cur_file, int(r[0]), r[1].strip()[:70], num("Instructions Executed"),
+                         num("Warp Stall Sampling (All Samples)"), stalls))
+    tot_i = sum(x[3] for x in rows) or 1
+    tot_s = sum(x[4] for x in rows) or 1
+    print(f"# source hotspots `{path}` kernel~{kernel_regex}: {tot_i:.3g} warp-instr, {tot_s:.0f} stall samples\n")
+    print("| file:line | instr % | stall % | top stalls | source |")
+    print("|---|---|---|---|---|")
+    for f, ln, src, ins, st, stalls in sorted(rows, key=lambda x: -x[4])[:top]:
+        ts = ", ".join(f"{k[6:]}={v:.0f}" for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:3] if v)
+        print(f"| {f}:{ln} | {100 * ins / tot_i:.1f} | {100 * st / tot_s:.1f} | {ts} | `{src}` |")
+
+
+if __name__ == "__main__" and len(sys.argv) > 3 and sys.argv[1] == "--source":
+    source_hotspots(sys.argv[2], sys.argv[3])
