@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define VK_RL_ABI_VERSION 1
+#define VK_RL_ABI_VERSION 2
 #define VK_MAX_RANK 3
 
 /* Status codes; each maps to one reference exception type
@@ -56,12 +56,15 @@ typedef enum vk_stop_metric {
   VK_METRIC_FRC_RESOLUTION = 2
 } vk_stop_metric;
 
-/* deconv::StoppingRule (deconv.hpp:35-40) */
+/* deconv::StoppingRule (deconv.hpp:35-40), plus the physical x spacing the
+ * reference takes from observed.spacing()->back() for the FRC metric
+ * (deconv.cpp:285-289); 0 means "no spacing" (= 1.0). */
 typedef struct vk_stop_rule {
   int metric; /* vk_stop_metric */
   double rel_tol;
   int patience;
   int max_iters;
+  double spacing;
 } vk_stop_rule;
 
 /* deconv::IterationTrace (deconv.hpp:49-59).  Arrays are caller-allocated

@@ -135,6 +135,59 @@ def si_psnr(x: np.ndarray, ref: np.ndarray) -> float:
     return 10.0 * math.log10(rng * rng / err)
 
 
+def frc_curve(a: np.ndarray, b: np.ndarray, ring_width: float = 1.0):
+    """metrics::frc (src/metrics.cpp:146-208): ring sums over the r2c
+    half-spectra with weight 2 for conjugate-pair kx planes."""
+    a = np.asarray(a, np.float32).astype(np.float64)
+    b = np.asarray(b, np.float32).astype(np.float64)
+    ax = tuple(range(a.ndim))
+    sa, sb = np.fft.rfftn(a, axes=ax), np.fft.rfftn(b, axes=ax)
+    shape = a.shape
+    n_max = max(shape)
+    bin_freq = ring_width / n_max
+    n_bins = int(math.floor(0.5 / bin_freq)) + 1
+    grids = np.meshgrid(*[np.arange(s) for s in sa.shape], indexing="ij")
+    nu2 = np.zeros(sa.shape)
+    for g, n in zip(grids, shape):
+        nu2 += (np.minimum(g, n - g) / n) ** 2
+    bins = np.rint(np.sqrt(nu2) / bin_freq)  # llround: ties away from zero
+    half = np.sqrt(nu2) / bin_freq - np.floor(np.sqrt(nu2) / bin_freq) == 0.5
+    bins = np.where(half, np.floor(np.sqrt(nu2) / bin_freq) + 1, bins).astype(np.int64)
+    kx = grids[-1]
+    selfc = (kx == 0) | ((shape[-1] % 2 == 0) & (kx == shape[-1] // 2))
+    w = np.where(selfc, 1.0, 2.0)
+    ok = bins < n_bins
+    num = np.bincount(bins[ok], (w * (sa * np.conj(sb)).real)[ok], n_bins)
+    da = np.bincount(bins[ok], (w * np.abs(sa) ** 2)[ok], n_bins)
+    db = np.bincount(bins[ok], (w * np.abs(sb) ** 2)[ok], n_bins)
+    den = np.sqrt(da * db)
+    corr = np.where(den > 0, num / np.where(den > 0, den, 1), 0.0)
+    return np.arange(n_bins) * bin_freq, corr
+
+
+def frc_resolution(freq, corr, spacing: float, threshold: float = 1.0 / 7.0) -> float:
+    """metrics::frc_resolution (src/metrics.cpp:210-239)."""
+    for j in range(1, len(corr)):
+        if corr[j] < threshold:
+            if j == 1 or corr[j - 1] < threshold:
+                nu = freq[j]
+            else:
+                nu = freq[j - 1] + (freq[j] - freq[j - 1]) * (corr[j - 1] - threshold) / (corr[j - 1] - corr[j])
+            return math.inf if nu <= 0 else spacing / nu
+    return math.inf
+
+
+def single_image_frc(img: np.ndarray, spacing: float = 1.0) -> float:
+    """even_view + metrics::single_image_frc (src/deconv.cpp:255-276,
+    src/metrics.cpp:241-264)."""
+    v = np.asarray(img, np.float32)
+    v = v[tuple(slice(0, s - s % 2) for s in v.shape)]
+    even = v[tuple(slice(0, None, 2) for _ in v.shape)]
+    odd = v[tuple(slice(1, None, 2) for _ in v.shape)]
+    f, c = frc_curve(even, odd)
+    return frc_resolution(f, c, spacing * 2.0)
+
+
 def relative_change(prev: float, cur: float) -> float:
     """src/deconv.cpp:296-300."""
     if math.isinf(prev) and math.isinf(cur) and prev == cur:
@@ -175,13 +228,14 @@ def validate(observed, psf, rel_tol, patience, max_iters):
 
 
 def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, patience=3,
-                    max_iters=100, flat_init=False, iterates=None):
-    """src/deconv.cpp:304-431.  Only the si_psnr_vs_input metric is restated
-    here (the other two are checked against the compiled reference).  If
+                    max_iters=100, flat_init=False, iterates=None, spacing=1.0):
+    """src/deconv.cpp:304-431 with the si_psnr_vs_input and frc_resolution
+    metrics (ssim_vs_prev is checked against the compiled reference only; its
+    reference implementation reads freed memory).  If
     `iterates` is a list, the cropped f32 estimate after every iteration is
     appended to it."""
     obs, k = validate(observed, psf, rel_tol, patience, max_iters)
-    if metric != "si_psnr_vs_input":
+    if metric not in ("si_psnr_vs_input", "frc_resolution"):
         raise NotImplementedError(metric)
     pshape, off = padded_domain(obs.shape, k.shape)
     t = RlTransforms(pshape, k)
@@ -200,7 +254,7 @@ def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, pati
         cur = crop_interior(est, off, obs.shape)
         if iterates is not None:
             iterates.append(cur)
-        value = si_psnr(cur, obs)
+        value = si_psnr(cur, obs) if metric == "si_psnr_vs_input" else single_image_frc(cur, spacing)
         trace.metric.append(value)
         if have_prev:
             fails = fails + 1 if relative_change(prev, value) < rel_tol else 0

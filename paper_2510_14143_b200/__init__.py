@@ -78,7 +78,7 @@ _STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: 
 # --- ctypes binding -----------------------------------------------------------
 class _Rule(ctypes.Structure):
     _fields_ = [("metric", ctypes.c_int), ("rel_tol", ctypes.c_double), ("patience", ctypes.c_int),
-                ("max_iters", ctypes.c_int)]
+                ("max_iters", ctypes.c_int), ("spacing", ctypes.c_double)]
 
 
 _dp = ctypes.POINTER(ctypes.c_double)
@@ -178,8 +178,11 @@ class StoppingRule:
     patience: int = 3
     max_iters: int = 100
 
-    def _c(self) -> _Rule:
-        return _Rule(_METRIC_ID[self.metric], float(self.rel_tol), int(self.patience), int(self.max_iters))
+    def _c(self, spacing: Optional[float] = None) -> _Rule:
+        """C struct; `spacing` is observed.spacing()->back() in the reference
+        (used by frc_resolution), None = no spacing (1.0)."""
+        return _Rule(_METRIC_ID[self.metric], float(self.rel_tol), int(self.patience), int(self.max_iters),
+                     float(spacing) if spacing else 0.0)
 
 
 @dataclass
@@ -358,14 +361,17 @@ class RlPlan(_Plan):
 
 
 def richardson_lucy(observed, psf, rule: StoppingRule = StoppingRule(), flat_init: bool = False,
-                    device: int = 0) -> RlResult:
-    """richardson_lucy (reference src/deconv.cpp:304-431) on the GPU."""
+                    device: int = 0, spacing: Optional[Sequence[float]] = None) -> RlResult:
+    """richardson_lucy (reference src/deconv.cpp:304-431) on the GPU.
+    `spacing` mirrors NdImage::spacing() of the observed image (only its last
+    entry is used, by the frc_resolution metric)."""
     obs = _f32(observed)
     k = _f32(psf)
     est = np.empty_like(obs)
     tb = _TraceBuf(max(int(rule.max_iters), 1))
+    sp = float(spacing[-1]) if spacing is not None and len(spacing) else None
     _check(lib().vk_richardson_lucy(device, obs.ndim, _shape(obs.shape), obs.ctypes.data, k.ndim,
-                                    _shape(k.shape), k.ctypes.data_as(_fp), ctypes.byref(rule._c()),
+                                    _shape(k.shape), k.ctypes.data_as(_fp), ctypes.byref(rule._c(sp)),
                                     int(bool(flat_init)), est.ctypes.data, ctypes.byref(tb.c)))
     return RlResult(est, tb.trace(rule.metric, obs.ndim))
 

@@ -23,6 +23,7 @@
 #include "../../include/vk_rl.h"
 #include "fast_table.h"
 #include "rl_passes.cuh"
+#include "rl_metrics.cuh"
 
 using vk::Geom;
 using vk::LinePlan;
@@ -192,6 +193,15 @@ struct vk_rl_plan_s {
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
   int cl_clusters = 0;
+  // frc_resolution stopping metric (rl_metrics.cuh): a sub-plan supplies the
+  // r2c transforms of the two half-size checkerboard images
+  vk_rl_plan_s* frc = nullptr;
+  DevBuf<float> frc_even, frc_odd;
+  DevBuf<double> frc_bins;
+  double* h_frc = nullptr;  // pinned [3][nbins]
+  int frc_nbins = 0;
+  double frc_binf = 0;
+  int frc_h[3]{1, 1, 1}, frc_s[3]{0, 0, 0};
   int xL = 1, yL = 1, zL = 1;
   size_t xs = 0, ys = 0, zs = 0;
 
@@ -219,6 +229,8 @@ struct vk_rl_plan_s {
     for (auto e : prof_pool) cudaEventDestroy(e);
     if (h_acc) cudaFreeHost(h_acc);
     if (stream) cudaStreamDestroy(stream);
+    if (h_frc) cudaFreeHost(h_frc);
+    delete frc;
   }
 };
 
@@ -456,20 +468,27 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, g.cy, p->SB.p, p->SA.p, nullptr);
 }
 
+// Full r2c spectrum [Hx][Wz][Wy] of a real block [rz][ry][rx] corner-embedded
+// in the plan's W grid, times `scale`.
+void spectrum3d(vk_rl_plan p, cudaStream_t s, const float* d_src, int rz, int ry, int rx, float scale,
+                float2* dst) {
+  const Geom& g = p->g;
+  x_pass(p, s, vk::XM_FWD, d_src, rz, ry, rx, scale, nullptr, nullptr, nullptr, nullptr);
+  const int nl = g.Hx * rz;
+  if (g.Wz == 1) {
+    y_pass(p, s, vk::YM_FWD, nl, ry, ry, g.Wy, g.Wy, 0, p->SA.p, dst, nullptr);
+    return;
+  }
+  y_pass(p, s, vk::YM_FWD, nl, ry, ry, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
+  z_pass(p, s, vk::ZM_FWD_OUT, rz, rz, 0, 0, p->SB.p, nullptr, dst);
+}
+
 // OTF of a corner-embedded PSF on the W grid, 1/prod(W) folded in
 // (deconv.cpp:126-130 + fft_plan.cpp:95-96).
 void build_otf(vk_rl_plan p, const float* d_psf, float2* otf_dst) {
   const Geom& g = p->g;
-  cudaStream_t s = p->stream;
   const float scale = (float)(1.0 / ((double)g.Wz * g.Wy * g.Wx));
-  x_pass(p, s, vk::XM_FWD, d_psf, p->Kz, p->Ky, p->Kx, scale, nullptr, nullptr, nullptr, nullptr);
-  const int nl = g.Hx * p->Kz;
-  if (g.Wz == 1) {
-    y_pass(p, s, vk::YM_FWD, nl, p->Ky, p->Ky, g.Wy, g.Wy, 0, p->SA.p, otf_dst, nullptr);
-    return;
-  }
-  y_pass(p, s, vk::YM_FWD, nl, p->Ky, p->Ky, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
-  z_pass(p, s, vk::ZM_FWD_OUT, p->Kz, p->Kz, 0, 0, p->SB.p, nullptr, otf_dst);
+  spectrum3d(p, p->stream, d_psf, p->Kz, p->Ky, p->Kx, scale, otf_dst);
 }
 
 // Task list, ring and counters of the one-launch y/z convolution.  Lag D (in
@@ -763,14 +782,93 @@ double si_psnr_from_sums(const RefStats& r, double sx, double sxx, double sxr) {
   return 10.0 * std::log10(r.range * r.range / err);
 }
 
+// Sub-plan and buffers for single_image_frc of the image crop
+// (metrics.cpp:241-264): even_view trims odd extents, the half extents must be
+// 5-smooth for the device r2c (no Bluestein yet).
+void setup_frc(vk_rl_plan p) {
+  if (p->frc) return;
+  uint64_t half[3] = {1, 1, 1}, ones[3] = {1, 1, 1};
+  for (int a = 0; a < p->rank; ++a) {
+    const uint64_t e = p->ishape[a] - p->ishape[a] % 2;  // even_view (deconv.cpp:255-276)
+    if (e == 0) fail(VK_ERR_UNSUPPORTED, "frc_resolution needs every image extent >= 2");
+    half[a] = e / 2;
+    if (good_size(half[a]) != half[a])
+      fail(VK_ERR_UNSUPPORTED, "frc_resolution on the B200 path needs 5-smooth half extents (got " +
+                                   std::to_string(half[a]) + ")");
+  }
+  const float one = 1.0f;
+  p->frc = create_plan(p->device, p->rank, half, p->rank, ones, &one, 0);
+  uint64_t nmax = 0;
+  for (int a = 0; a < p->rank; ++a) nmax = std::max(nmax, half[a]);
+  p->frc_binf = 1.0 / (double)nmax;  // ring_width / n_max (metrics.cpp:166-169)
+  p->frc_nbins = (int)std::floor(0.5 / p->frc_binf) + 1;
+  for (int a3 = 0; a3 < 3; ++a3) {
+    const int a = a3 - (3 - p->rank);
+    p->frc_h[a3] = a >= 0 ? (int)half[a] : 1;
+    p->frc_s[a3] = a >= 0 ? 1 : 0;
+  }
+  const size_t hn = (size_t)p->frc_h[0] * p->frc_h[1] * p->frc_h[2];
+  p->frc_even.alloc(hn, "frc even");
+  p->frc_odd.alloc(hn, "frc odd");
+  p->frc_bins.alloc((size_t)3 * p->frc_nbins, "frc bins");
+  ck(cudaMallocHost(&p->h_frc, (size_t)3 * p->frc_nbins * sizeof(double)), "frc pinned");
+}
+
+// frc_resolution(frc(even, odd), 2*spacing) of the current estimate crop
+// (metrics.cpp:146-239); the host walks the few hundred ring values.
+double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
+  vk_rl_plan_s* f = p->frc;
+  const int nb = p->frc_nbins;
+  ck(cudaMemsetAsync(p->frc_bins.p, 0, (size_t)3 * nb * sizeof(double), s), "frc bins");
+  vk::frc_split_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, p->g, p->frc_h[0], p->frc_h[1], p->frc_h[2],
+                                                     p->frc_s[0], p->frc_s[1], p->frc_s[2], p->frc_even.p,
+                                                     p->frc_odd.p);
+  launch_check(p, "frc split");
+  const vk::Geom& fg = f->g;
+  spectrum3d(f, s, p->frc_even.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf.p);
+  spectrum3d(f, s, p->frc_odd.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf_flip.p);
+  vk::frc_bins_kernel<<<148 * 2, kThreads, (size_t)3 * nb * sizeof(double), s>>>(
+      f->otf.p, f->otf_flip.p, fg.Wz, fg.Wy, fg.Wx, fg.Hx, p->frc_binf, nb, p->frc_bins.p);
+  launch_check(p, "frc bins");
+  ck(cudaMemcpyAsync(p->h_frc, p->frc_bins.p, (size_t)3 * nb * sizeof(double), cudaMemcpyDeviceToHost, s),
+     "frc D2H");
+  ck(cudaStreamSynchronize(s), "frc");
+  const double* num = p->h_frc;
+  const double* da = p->h_frc + nb;
+  const double* db = p->h_frc + 2 * nb;
+  auto corr = [&](int j) {
+    const double den = std::sqrt(da[j] * db[j]);
+    return den > 0 ? num[j] / den : 0.0;
+  };
+  const double threshold = 1.0 / 7.0, sp = spacing * 2.0;  // single_image_frc doubles the spacing
+  for (int j = 1; j < nb; ++j) {  // DC excluded (metrics.cpp:221-239)
+    if (corr(j) < threshold) {
+      double nu;
+      if (j == 1 || corr(j - 1) < threshold) {
+        nu = j * p->frc_binf;
+      } else {
+        const double c0 = corr(j - 1), c1 = corr(j);
+        const double f0 = (j - 1) * p->frc_binf, f1 = j * p->frc_binf;
+        nu = f0 + (f1 - f0) * (c0 - threshold) / (c0 - c1);
+      }
+      if (nu <= 0) return std::numeric_limits<double>::infinity();
+      return sp / nu;
+    }
+  }
+  return std::numeric_limits<double>::infinity();  // kUnresolved
+}
+
 // The richardson_lucy loop on device buffers (deconv.cpp:333-430).
 void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_rule* rule, int flat_init,
                 vk_trace* trace, cudaStream_t s, bool check_obs) {
   check_rule(rule);
   if (!p->pad) fail(VK_ERR_ARG, "plan was created without padding (rl_step plan)");
-  if (rule->metric != VK_METRIC_SI_PSNR_VS_INPUT)
-    fail(VK_ERR_UNSUPPORTED, std::string(rule->metric == VK_METRIC_SSIM_VS_PREV ? "ssim_vs_prev" : "frc_resolution") +
-                                 " stopping metric is not implemented on the B200 path yet");
+  if (rule->metric == VK_METRIC_SSIM_VS_PREV)
+    fail(VK_ERR_UNSUPPORTED, "ssim_vs_prev stopping metric is not implemented on the B200 path yet");
+  if (rule->metric != VK_METRIC_SI_PSNR_VS_INPUT && rule->metric != VK_METRIC_FRC_RESOLUTION)
+    fail(VK_ERR_ARG, "unknown stopping metric");
+  const bool frc = rule->metric == VK_METRIC_FRC_RESOLUTION;
+  const double spacing = rule->spacing > 0 ? rule->spacing : 1.0;
   const Geom& g = p->g;
   const int iters = rule->max_iters;
   ensure_iter_buffers(p, iters);
@@ -797,7 +895,8 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   const RefStats rs{(double)nI, st.sr, st.srr, (double)fmax - (double)fmin};
   // DegenerateReference surfaces at the first metric evaluation in the
   // reference; no estimate is returned either way.
-  si_psnr_from_sums(rs, 0.0, 0.0, 0.0);
+  if (!frc) si_psnr_from_sums(rs, 0.0, 0.0, 0.0);
+  if (frc) setup_frc(p);
 
   vk::pad_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p);
   launch_check(p, "pad");
@@ -821,18 +920,23 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     conv_yz(p, s, p->otf.p);
     x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc, nullptr);
     conv_yz(p, s, p->otf_flip.p);
-    const bool last = it == iters;
+    // the last iteration writes the cropped output directly unless a metric
+    // still needs the updated estimate
+    const bool last = it == iters && !frc;
     x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc,
            last ? d_out : nullptr);
+    if (frc) values.push_back(frc_eval(p, s, spacing));  // syncs: the value is needed on the host
     ck(cudaEventRecord(p->events[it], s), "event");
     run = it;
-    if (may_stop && it >= rule->patience + 1 && !last) {
-      ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)it * 4 * sizeof(double), cudaMemcpyDeviceToHost, s),
-         "acc D2H");
-      ck(cudaStreamSynchronize(s), "iteration");
-      while ((int)values.size() < it) {
-        const double* a = p->h_acc + values.size() * 4;
-        values.push_back(si_psnr_from_sums(rs, a[1], a[2], a[3]));
+    if (may_stop && it >= rule->patience + 1 && it < iters) {
+      if (!frc) {
+        ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)it * 4 * sizeof(double), cudaMemcpyDeviceToHost, s),
+           "acc D2H");
+        ck(cudaStreamSynchronize(s), "iteration");
+        while ((int)values.size() < it) {
+          const double* a = p->h_acc + values.size() * 4;
+          values.push_back(si_psnr_from_sums(rs, a[1], a[2], a[3]));
+        }
       }
       // replay the stopping rule over the values so far (deconv.cpp:409-423)
       fails = 0;
@@ -855,6 +959,10 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
       }
     }
   }
+  if (frc && !stopped) {  // the last iteration ran in UPDATE mode: crop now
+    vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
+    launch_check(p, "crop");
+  }
   ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
   ck(cudaStreamSynchronize(s), "run");
   prof_collect(p);
@@ -864,7 +972,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     for (int i = 0; i < 3; ++i) trace->fft_shape[i] = i < p->rank ? p->wshape[i] : 0;
     for (int k = 0; k < run && k < trace->capacity; ++k) {
       const double* a = p->h_acc + (size_t)k * 4;
-      if (trace->metric) trace->metric[k] = si_psnr_from_sums(rs, a[1], a[2], a[3]);
+      if (trace->metric) trace->metric[k] = frc ? values[k] : si_psnr_from_sums(rs, a[1], a[2], a[3]);
       if (trace->log_likelihood) trace->log_likelihood[k] = a[0];
       if (trace->wall_s) {
         float ms = 0;

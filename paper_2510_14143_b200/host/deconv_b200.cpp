@@ -147,7 +147,9 @@ RlResult richardson_lucy(const NdImage& observed, const NdImage& psf, const Stop
   tr.metric = metric.data();
   tr.wall_s = wall.data();
   tr.log_likelihood = ll.data();
-  const vk_stop_rule r{static_cast<int>(rule.metric), rule.rel_tol, rule.patience, rule.max_iters};
+  // FRC uses the x spacing of the observed image (deconv.cpp:286-287)
+  const double spacing = obs.spacing() ? obs.spacing()->back() : 0.0;
+  const vk_stop_rule r{static_cast<int>(rule.metric), rule.rel_tol, rule.patience, rule.max_iters, spacing};
   std::vector<float> est(obs.size());
   check(vk_richardson_lucy(device(), static_cast<int>(sh.size()), sh.data(), obs.f32_values().data(),
                            static_cast<int>(ks.size()), ks.data(), k.f32_values().data(), &r, flat_init ? 1 : 0,

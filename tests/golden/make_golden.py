@@ -82,6 +82,18 @@ def main():
     rl_case("tol_inf", obs, ref.gaussian_psf((3, 3, 3), [0.8]), 10, rel_tol=np.inf, patience=3,
             max_iters=10)
 
+    # frc_resolution metric (the reference's default rule), fixed count and the
+    # full default rule {frc, 1e-3, 3, 100} (deconv.hpp:35-40)
+    truth = ref.generate_blobs((20, 48, 48), n_objects=4, radius_min=3, radius_max=5, seed=17,
+                               noise_sigma=0.05)
+    psf = ref.gaussian_psf((5, 7, 7), [1.0, 1.5, 1.5])
+    frc_obs = blur_observed(truth, psf)
+    rl_case("frc3d", frc_obs, psf, 6, metric="frc_resolution")
+    rl_case("frc3d_default", frc_obs, psf, 100, metric="frc_resolution", rel_tol=1e-3, patience=3,
+            max_iters=100)
+    obs2 = (rng.random((64, 81)) * 2 + 0.2).astype(np.float32)  # odd extent: even_view trims it
+    rl_case("frc2d", obs2, ref.gaussian_psf((9, 9), [1.5]), 5, metric="frc_resolution")
+
     # delta PSF: estimate == observed after iteration 1
     d = np.zeros((3, 3, 3), np.float32)
     d[1, 1, 1] = 1

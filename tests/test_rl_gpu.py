@@ -242,6 +242,31 @@ def test_fused_yz_conv_matches_three_pass(name, shape, mk):
     assert rel_l2(r1.estimate, its[0]) <= TOL_1
 
 
+def test_frc_default_rule_c1():
+    """The reference's DEFAULT rule (frc_resolution, 1e-3, patience 3) on the
+    C1 shape: per-iteration FRC resolution on the device vs the oracle's
+    single_image_frc, same stop iteration and reason."""
+    psf = O.gaussian_psf((15, 15, 15), 1.75)
+    obs = synth.blurred(synth.blobs((64, 256, 256), 120, 6, 10, seed=1), psf)
+    its = []
+    e, t = O.richardson_lucy(obs, psf, "frc_resolution", 1e-3, 3, 12, iterates=its)
+    r = vk.richardson_lucy(obs, psf, vk.StoppingRule(max_iters=12))
+    ref_vals = np.asarray(t.metric)
+    ours = np.asarray([x.value for x in r.trace.records])
+    n = min(len(ours), len(ref_vals))
+    assert np.array_equal(np.isinf(ours[:n]), np.isinf(ref_vals[:n]))
+    fin = ~np.isinf(ref_vals[:n])
+    np.testing.assert_allclose(ours[:n][fin], ref_vals[:n][fin], rtol=TOL_METRIC)
+    rel = [O.relative_change(a, b) for a, b in zip(ref_vals[:-1], ref_vals[1:])]
+    if not any(abs(x - 1e-3) <= 1e-5 for x in rel if math.isfinite(x)):
+        assert len(ours) == len(ref_vals) and r.trace.stop_reason == t.stop_reason
+        assert rel_l2(r.estimate, e) <= TOL_N
+    # a physical spacing scales the resolution (deconv.cpp:286-287)
+    r2 = vk.richardson_lucy(obs, psf, vk.StoppingRule(max_iters=2, patience=2), spacing=(2.0, 0.5, 0.5))
+    v1 = [x.value for x in r.trace.records[:2]]
+    np.testing.assert_allclose([x.value for x in r2.trace.records], np.asarray(v1) * 0.5, rtol=1e-12)
+
+
 def test_c2_full_size_first_iterations():
     """C2 at full size (128x512x512, 31^3 widefield): the benchmark's own grid
     (192 x 576 x 576) through the fast kernels, 2 iterations vs the oracle."""
