@@ -114,6 +114,26 @@ void compare_rl(const std::string& name, const NdImage& obs, const NdImage& psf,
   report(gn.estimate.shape() == obs.shape() && gn.estimate.backend() == obs.backend(), name + " result metadata");
 }
 
+// The reference's DEFAULT rule (frc_resolution) end to end: trace values
+// (resolution, inf = unresolved), iterations and stop reason.
+void compare_default_rule(const std::string& name, const NdImage& obs, const NdImage& psf, int max_iters) {
+  deconv::StoppingRule rule;  // {frc_resolution, 1e-3, 3, 100}
+  rule.max_iters = max_iters;
+  const RefRun rn = ref_rl(obs, psf, rule, false);
+  const deconv::RlResult gn = deconv::richardson_lucy(obs, psf, rule, false);
+  bool ok = rn.rc == 0 && (int)gn.trace.records.size() == rn.iters &&
+            gn.trace.stop_reason == (rn.reason ? "converged" : "max_iters");
+  for (int i = 0; ok && i < rn.iters; ++i) {
+    const double a = gn.trace.records[i].value, b = rn.metric[i];
+    ok = gn.trace.records[i].metric_name == "frc_resolution" &&
+         (std::isinf(b) ? std::isinf(a) : std::abs(a - b) <= 1e-3 * std::abs(b));
+  }
+  char buf[128];
+  std::snprintf(buf, sizeof buf, "%d vs %d iterations, relL2 %.2e", (int)gn.trace.records.size(), rn.iters,
+                rel_l2(gn.estimate.f32_values(), rn.est));
+  report(ok && rel_l2(gn.estimate.f32_values(), rn.est) <= 1e-3, name + " default rule (frc)", buf);
+}
+
 template <class Exc>
 void expect_error(const std::string& name, const NdImage& obs, const NdImage& psf, deconv::StoppingRule rule) {
   const RefRun r = ref_rl(obs, psf, rule, false);
@@ -134,6 +154,7 @@ int main() {
   const NdImage psf3 = synth::gaussian_psf({7, 7, 7}, {1.0});
   compare_rl("blobs3d", blurred_blobs({20, 48, 48}, 4, 7, psf3), psf3, 6, false);
   compare_rl("blobs3d_flat", blurred_blobs({20, 48, 48}, 4, 9, psf3), psf3, 4, true);
+  compare_default_rule("blobs3d", blurred_blobs({20, 48, 48}, 4, 17, psf3), psf3, 12);
   // fast-kernel grid (W = 96 x 288 x 288, the C1 grid) at the C1 size
   const NdImage psf15 = synth::gaussian_psf({15, 15, 15}, {1.75});
   compare_rl("c1", blurred_blobs({64, 256, 256}, 60, 1, psf15), psf15, 3, false);
