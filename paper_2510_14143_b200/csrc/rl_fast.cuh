@@ -153,6 +153,53 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
       const float* ob = a.obs + ob_off;
       float* ea = a.est + ((size_t)z * g.Py + (va ? ya : 0)) * g.Px;
       float* eb = a.est + ((size_t)z * g.Py + (vb ? yb : 0)) * g.Px;
+      if (ina && inb && x0 >= g.ox && x0 + CH <= g.ox + g.Ix) {
+        // interior chunk (the common case): no clamps, no predicates
+        const float* oa2 = oa + (x0 - g.ox) + lane;
+        const float* ob2 = ob + (x0 - g.ox) + lane;
+        float* ea2 = ea + x0 + lane;
+        float* eb2 = eb + x0 + lane;
+        const int s0 = sw<L>(x0 + lane + g.cx, l);
+        float2 m[U];
+        float o_a[U], o_b[U], e_a[U], e_b[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          m[u] = A[s0 + u * 32 * (L + 1)];
+          o_a[u] = __ldg(oa2 + u * 32);
+          o_b[u] = __ldg(ob2 + u * 32);
+          if (!ratio) {
+            e_a[u] = ea2[u * 32];
+            e_b[u] = eb2[u * 32];
+          }
+        }
+        float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          float2 val;
+          if (ratio) {
+            const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
+            val = make_float2(__fdividef(o_a[u], ma), __fdividef(o_b[u], mb));
+            f0 += fmaf(o_a[u], __logf(ma), -ma) + fmaf(o_b[u], __logf(mb), -mb);
+          } else {
+            val = make_float2(fmaxf(e_a[u] * m[u].x, 0.f), fmaxf(e_b[u] * m[u].y, 0.f));
+            if (!last) {
+              ea2[u * 32] = val.x;
+              eb2[u * 32] = val.y;
+            } else {
+              a.out[oa_off + (x0 - g.ox) + lane + u * 32] = val.x;
+              a.out[ob_off + (x0 - g.ox) + lane + u * 32] = val.y;
+            }
+            f0 += val.x + val.y;
+            f1 = fmaf(val.x, val.x, fmaf(val.y, val.y, f1));
+            f2 = fmaf(val.x, o_a[u], fmaf(val.y, o_b[u], f2));
+          }
+          A[s0 + u * 32 * (L + 1)] = val;
+        }
+        acc0 += f0;
+        acc1 += f1;
+        acc2 += f2;
+        continue;
+      }
       float2 m[U];
       float o_a[U], o_b[U], e_a[U], e_b[U];
 #pragma unroll
