@@ -30,7 +30,7 @@
 extern "C" {
 #endif
 
-#define VK_RL_ABI_VERSION 2
+#define VK_RL_ABI_VERSION 3
 #define VK_MAX_RANK 3
 
 /* Status codes; each maps to one reference exception type
@@ -46,7 +46,8 @@ typedef enum vk_status {
   VK_ERR_ODD_EXTENT = 7,       /* voxelkit::OddExtent             */
   VK_ERR_CUDA = 8,             /* CUDA runtime failure            */
   VK_ERR_OOM = 9,              /* device allocation failure       */
-  VK_ERR_UNSUPPORTED = 10      /* not implemented on this path    */
+  VK_ERR_UNSUPPORTED = 10,     /* not implemented on this path    */
+  VK_ERR_KERNEL_TOO_LARGE = 11 /* voxelkit::KernelTooLarge        */
 } vk_status;
 
 /* deconv::StopMetric (deconv.hpp:28) */
@@ -142,6 +143,24 @@ vk_status vk_richardson_lucy(int device, int rank, const uint64_t* shape, const 
 vk_status vk_rl_step_psf(int device, int rank, const uint64_t* shape, const float* estimate,
                          const float* observed, int psf_rank, const uint64_t* psf_shape,
                          const float* psf, float* out);
+
+/* filters::fft_convolve(img, kernel, circular) (filters.cpp:174-264) and its
+ * registry op "fft_convolve" (filters.cpp:316-323) on the same transforms.
+ * Linear: zero-padded to good_size(A + K - 1) per axis, the centred same-size
+ * result (crop at (K-1)/2).  Circular: on the image grid itself with the
+ * kernel centre wrapped to index 0 (KernelTooLarge if a kernel extent exceeds
+ * the image's; extents must be 5-smooth on this path, else
+ * VK_ERR_UNSUPPORTED).  The kernel is used as given (no sign or sum checks,
+ * as in the reference).  Rank mismatch -> ShapeMismatch.  A conv plan is only
+ * valid with the vk_conv_* calls. */
+vk_status vk_conv_plan_create(int device, int rank, const uint64_t* shape, int kernel_rank,
+                              const uint64_t* kernel_shape, const float* kernel, int circular,
+                              vk_rl_plan* out);
+vk_status vk_conv_run(vk_rl_plan plan, const float* image, float* out);
+vk_status vk_conv_run_device(vk_rl_plan plan, const float* d_image, float* d_out, void* stream);
+vk_status vk_fft_convolve(int device, int rank, const uint64_t* shape, const float* image,
+                          int kernel_rank, const uint64_t* kernel_shape, const float* kernel,
+                          int circular, float* out);
 
 /* fftx::good_size (fft_plan.cpp:41-49). */
 uint64_t vk_good_size(uint64_t n);

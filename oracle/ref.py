@@ -22,7 +22,8 @@ _i32p = ctypes.POINTER(ctypes.c_int)
 
 # Status codes shared with include/vk_rl.h.
 CODE_NAMES = {1: "Error", 2: "ShapeMismatch", 3: "NegativeInput", 4: "UnnormalizedPsf",
-              5: "DegenerateReference", 6: "TooSmall", 7: "OddExtent", 99: "Other"}
+              5: "DegenerateReference", 6: "TooSmall", 7: "OddExtent", 11: "KernelTooLarge",
+              99: "Other"}
 
 METRICS = {"si_psnr_vs_input": 0, "ssim_vs_prev": 1, "frc_resolution": 2}
 
@@ -73,6 +74,12 @@ def lib():
         L.vkref_single_image_frc.restype = ctypes.c_int
         L.vkref_single_image_frc.argtypes = [ctypes.c_int, _u64p, _f32p, ctypes.c_double, _f64p,
                                              ctypes.c_char_p, ctypes.c_int]
+        L.vkref_ssim.restype = ctypes.c_int
+        L.vkref_ssim.argtypes = [ctypes.c_int, _u64p, _f32p, _f32p, _f64p, ctypes.c_char_p,
+                                 ctypes.c_int]
+        L.vkref_gaussian.restype = ctypes.c_int
+        L.vkref_gaussian.argtypes = [ctypes.c_int, _u64p, _f32p, ctypes.c_double, ctypes.c_double,
+                                     _f32p, ctypes.c_char_p, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -188,3 +195,24 @@ def single_image_frc(x, spacing=1.0) -> float:
                                       ctypes.byref(v), err, 512)
     _check(rc, err)
     return v.value
+
+
+def ssim(x, ref) -> float:
+    """metrics::ssim as shipped (reads freed temporaries; see ref_capi.cpp)."""
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    b = np.ascontiguousarray(ref, dtype=np.float32)
+    v = ctypes.c_double(0)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().vkref_ssim(a.ndim, _shape(a.shape), _fp(a), _fp(b), ctypes.byref(v), err, 512)
+    _check(rc, err)
+    return v.value
+
+
+def gaussian(x, sigma=1.5, truncate=3.5) -> np.ndarray:
+    a = np.ascontiguousarray(x, dtype=np.float32)
+    out = np.empty(a.shape, np.float32)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().vkref_gaussian(a.ndim, _shape(a.shape), _fp(a), float(sigma), float(truncate),
+                              _fp(out), err, 512)
+    _check(rc, err)
+    return out

@@ -12,6 +12,9 @@
 //   vkref_generate_blobs  -> synth::generate_blobs       (proj/src/synth.cpp:199-224)
 //   vkref_si_psnr         -> metrics::si_psnr            (proj/src/metrics.cpp:67-101)
 //   vkref_good_size       -> fftx::good_size             (proj/src/fft_plan.cpp:41-49)
+//   vkref_single_image_frc-> metrics::single_image_frc   (proj/src/metrics.cpp:241-264)
+//   vkref_ssim            -> metrics::ssim (as shipped)  (proj/src/metrics.cpp:103-144)
+//   vkref_gaussian        -> filters::gaussian           (proj/src/filters.cpp:78-140)
 // Exceptions are mapped to the same status codes the product C-ABI uses
 // (include/vk_rl.h) so error-parity tests compare like with like.
 #include <cstdint>
@@ -41,6 +44,7 @@ enum {
   E_DEGENERATE = 5,
   E_TOO_SMALL = 6,
   E_ODD = 7,
+  E_KERNEL_TOO_LARGE = 11,
   E_OTHER = 99,
 };
 
@@ -72,6 +76,7 @@ int fail(const std::exception& e, int code, char* err, int errlen) {
   catch (const DegenerateReference& e) { return fail(e, E_DEGENERATE, err, errlen); } \
   catch (const TooSmall& e) { return fail(e, E_TOO_SMALL, err, errlen); } \
   catch (const OddExtent& e) { return fail(e, E_ODD, err, errlen); }       \
+  catch (const KernelTooLarge& e) { return fail(e, E_KERNEL_TOO_LARGE, err, errlen); } \
   catch (const Error& e) { return fail(e, E_ARG, err, errlen); }           \
   catch (const std::exception& e) { return fail(e, E_OTHER, err, errlen); }
 
@@ -185,6 +190,32 @@ int vkref_single_image_frc(int rank, const std::uint64_t* shape, const float* x,
                            double spacing, double* value, char* err, int errlen) {
   try {
     *value = metrics::single_image_frc(make(rank, shape, x, false), spacing);
+    return OK;
+  }
+  VKREF_CATCH
+}
+
+// metrics::ssim as shipped (proj/src/metrics.cpp:103-144).  It reads the
+// smoothed moments through spans of destroyed temporaries (:128-132), so the
+// value is only trustworthy while the allocator has not reused those blocks;
+// callers cross-check it against vkref_gaussian-based recomputation.
+int vkref_ssim(int rank, const std::uint64_t* shape, const float* x, const float* ref,
+               double* value, char* err, int errlen) {
+  try {
+    *value = metrics::ssim(make(rank, shape, x, false), make(rank, shape, ref, false));
+    return OK;
+  }
+  VKREF_CATCH
+}
+
+// filters::gaussian (proj/src/filters.cpp:78-140), sigma per axis.
+int vkref_gaussian(int rank, const std::uint64_t* shape, const float* x, double sigma,
+                   double truncate, float* out, char* err, int errlen) {
+  try {
+    const NdImage g = filters::gaussian(make(rank, shape, x, false),
+                                        std::vector<double>(rank, sigma), truncate);
+    const auto v = g.f32_values();
+    std::memcpy(out, v.data(), v.size() * sizeof(float));
     return OK;
   }
   VKREF_CATCH

@@ -188,6 +188,69 @@ def single_image_frc(img: np.ndarray, spacing: float = 1.0) -> float:
     return frc_resolution(f, c, spacing * 2.0)
 
 
+def gaussian_kernel_1d(sigma: float, truncate: float) -> np.ndarray:
+    """filters.cpp:78-90: half = ceil(truncate*sigma) taps per side,
+    exp(-0.5 (i/sigma)^2) normalised by their (sequential) sum."""
+    half = int(math.ceil(truncate * sigma))
+    w = [math.exp(-0.5 * (i / sigma) * (i / sigma)) for i in range(-half, half + 1)]
+    tot = 0.0
+    for v in w:
+        tot += v
+    return np.array([v / tot for v in w])
+
+
+def mirror_index(i: np.ndarray, n: int) -> np.ndarray:
+    """nd_utils.hpp:31-38 (reflect about the end samples, period 2(n-1))."""
+    if n == 1:
+        return np.zeros_like(i)
+    period = 2 * (n - 1)
+    m = np.mod(i, period)
+    return np.where(m >= n, period - m, m)
+
+
+def gaussian(img: np.ndarray, sigma: float = 1.5, truncate: float = 3.5) -> np.ndarray:
+    """filters::gaussian (filters.cpp:92-140): one separable pass per axis,
+    mirror boundary, double accumulation in tap order (each product and sum
+    rounded separately, as the reference's scalar loop does), f32 result."""
+    cur = np.asarray(img, np.float32).astype(np.float64)
+    w = gaussian_kernel_1d(sigma, truncate)
+    half = len(w) // 2
+    for axis in range(cur.ndim):
+        n = cur.shape[axis]
+        idx = np.arange(n)
+        acc = np.zeros_like(cur)
+        for k in range(-half, half + 1):
+            acc = acc + w[k + half] * np.take(cur, mirror_index(idx + k, n), axis=axis)
+        cur = acc
+    return cur.astype(np.float32)
+
+
+def ssim(x: np.ndarray, ref: np.ndarray) -> float:
+    """metrics::ssim (src/metrics.cpp:103-144) with the moments held alive
+    (the reference reads them through dangling spans): five
+    Gaussian-smoothed fields (sigma 1.5, truncate 3.5), c1 = (0.01 R)^2,
+    c2 = (0.03 R)^2 with R = range of `ref`, mean of the SSIM map."""
+    a = np.asarray(x, np.float32)
+    b = np.asarray(ref, np.float32)
+    if a.shape != b.shape:
+        raise OracleError("ShapeMismatch", "ssim: shape mismatch")
+    if any(e < 7 for e in a.shape):
+        raise OracleError("TooSmall", "ssim needs every extent >= 7")
+    rng = float(b.max()) - float(b.min())
+    c1 = (0.01 * rng) * (0.01 * rng)
+    c2 = (0.03 * rng) * (0.03 * rng)
+    mx = gaussian(a).astype(np.float64)
+    mr = gaussian(b).astype(np.float64)
+    mxx = gaussian(a * a).astype(np.float64)  # f32 products (metrics.cpp:121-125)
+    mrr = gaussian(b * b).astype(np.float64)
+    mxr = gaussian(a * b).astype(np.float64)
+    var_x = mxx - mx * mx
+    var_r = mrr - mr * mr
+    cov = mxr - mx * mr
+    m = ((2 * mx * mr + c1) * (2 * cov + c2)) / ((mx * mx + mr * mr + c1) * (var_x + var_r + c2))
+    return float(m.sum()) / float(a.size)
+
+
 def relative_change(prev: float, cur: float) -> float:
     """src/deconv.cpp:296-300."""
     if math.isinf(prev) and math.isinf(cur) and prev == cur:
@@ -229,13 +292,13 @@ def validate(observed, psf, rel_tol, patience, max_iters):
 
 def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, patience=3,
                     max_iters=100, flat_init=False, iterates=None, spacing=1.0):
-    """src/deconv.cpp:304-431 with the si_psnr_vs_input and frc_resolution
-    metrics (ssim_vs_prev is checked against the compiled reference only; its
-    reference implementation reads freed memory).  If
+    """src/deconv.cpp:304-431 with all three stopping metrics (ssim_vs_prev
+    compares with the previous iterate, the observed image at iteration 1,
+    deconv.cpp:352,403,423).  If
     `iterates` is a list, the cropped f32 estimate after every iteration is
     appended to it."""
     obs, k = validate(observed, psf, rel_tol, patience, max_iters)
-    if metric not in ("si_psnr_vs_input", "frc_resolution"):
+    if metric not in ("si_psnr_vs_input", "frc_resolution", "ssim_vs_prev"):
         raise NotImplementedError(metric)
     pshape, off = padded_domain(obs.shape, k.shape)
     t = RlTransforms(pshape, k)
@@ -245,6 +308,7 @@ def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, pati
     inner = tuple(slice(o, o + s) for o, s in zip(off, obs.shape))
     ov = obs.astype(np.float64)
     fails, prev, have_prev = 0, 0.0, False
+    previous = obs
     for it in range(1, max_iters + 1):
         model = t.convolve(est, False)
         m = np.maximum(model[inner], K_DIV_EPSILON)
@@ -254,7 +318,13 @@ def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, pati
         cur = crop_interior(est, off, obs.shape)
         if iterates is not None:
             iterates.append(cur)
-        value = si_psnr(cur, obs) if metric == "si_psnr_vs_input" else single_image_frc(cur, spacing)
+        if metric == "si_psnr_vs_input":
+            value = si_psnr(cur, obs)
+        elif metric == "ssim_vs_prev":
+            value = ssim(cur, previous)
+        else:
+            value = single_image_frc(cur, spacing)
+        previous = cur
         trace.metric.append(value)
         if have_prev:
             fails = fails + 1 if relative_change(prev, value) < rel_tol else 0

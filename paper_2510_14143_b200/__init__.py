@@ -68,11 +68,15 @@ class Unsupported(Error):
     pass
 
 
+class KernelTooLarge(Error):
+    pass
+
+
 KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv", "yz_dataflow",
                 "yz_cluster")  # vk_kernel_kind
 
 _STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: DegenerateReference,
-           6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported}
+           6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported, 11: KernelTooLarge}
 
 
 # --- ctypes binding -----------------------------------------------------------
@@ -120,9 +124,14 @@ def lib() -> ctypes.CDLL:
     L.vk_richardson_lucy.argtypes = [i, i, _u64p, _vp, i, _u64p, _fp, ctypes.POINTER(_Rule), i, _vp,
                                      ctypes.POINTER(_Trace)]
     L.vk_rl_step_psf.argtypes = [i, i, _u64p, _vp, _vp, i, _u64p, _fp, _vp]
+    L.vk_conv_plan_create.argtypes = [i, i, _u64p, i, _u64p, _fp, i, ctypes.POINTER(_vp)]
+    L.vk_conv_run.argtypes = [_vp, _vp, _vp]
+    L.vk_conv_run_device.argtypes = [_vp, _vp, _vp, _vp]
+    L.vk_fft_convolve.argtypes = [i, i, _u64p, _vp, i, _u64p, _fp, i, _vp]
     for name in ("vk_rl_plan_create", "vk_rl_plan_shapes", "vk_rl_plan_device_bytes", "vk_rl_plan_launches",
                  "vk_rl_plan_destroy", "vk_rl_run", "vk_rl_run_device", "vk_rl_run_batch", "vk_rl_step",
-                 "vk_rl_step_device", "vk_richardson_lucy", "vk_rl_step_psf"):
+                 "vk_rl_step_device", "vk_richardson_lucy", "vk_rl_step_psf", "vk_conv_plan_create",
+                 "vk_conv_run", "vk_conv_run_device", "vk_fft_convolve"):
         getattr(L, name).restype = st
     L.vk_rl_plan_describe.argtypes = [_vp, ctypes.c_char_p, i]
     L.vk_rl_plan_describe.restype = st
@@ -235,13 +244,17 @@ class _TraceBuf:
 
 
 class _Plan:
-    def __init__(self, shape, psf, pad: bool, device: int = 0):
+    def __init__(self, shape, psf, pad: bool, device: int = 0, conv: int = 0):
         self._h = None
         k = _f32(psf)
         shape = tuple(int(s) for s in shape)
         h = _vp()
-        _check(lib().vk_rl_plan_create(device, len(shape), _shape(shape), k.ndim, _shape(k.shape),
-                                       k.ctypes.data_as(_fp), int(pad), ctypes.byref(h)))
+        if conv:
+            _check(lib().vk_conv_plan_create(device, len(shape), _shape(shape), k.ndim, _shape(k.shape),
+                                             k.ctypes.data_as(_fp), int(conv == 2), ctypes.byref(h)))
+        else:
+            _check(lib().vk_rl_plan_create(device, len(shape), _shape(shape), k.ndim, _shape(k.shape),
+                                           k.ctypes.data_as(_fp), int(pad), ctypes.byref(h)))
         self._h = h
         self.device = device
         r = ctypes.c_int(0)
@@ -400,6 +413,40 @@ def rl_step(estimate, observed, transforms, device: int = 0) -> np.ndarray:
     return out
 
 
+class ConvPlan(_Plan):
+    """filters::fft_convolve(img, kernel, circular) transforms for one image
+    shape (reference src/filters.cpp:174-264): the kernel spectrum stays on the
+    GPU; run() / run_device() convolve any image of that shape."""
+
+    def __init__(self, image_shape, kernel, circular: bool = False, device: int = 0):
+        super().__init__(image_shape, kernel, pad=False, device=device, conv=2 if circular else 1)
+        self.circular = bool(circular)
+
+    def run(self, image, out: Optional[np.ndarray] = None) -> np.ndarray:
+        a = _f32(image)
+        if a.shape != self.image_shape_:
+            raise ShapeMismatch(f"ShapeMismatch: image {list(a.shape)} vs plan {list(self.image_shape_)}")
+        o = np.empty_like(a) if out is None else out
+        _check(lib().vk_conv_run(self._h, a.ctypes.data, o.ctypes.data))
+        return o
+
+    def run_device(self, img_ptr: int, out_ptr: int, stream: int = 0) -> None:
+        _check(lib().vk_conv_run_device(self._h, img_ptr, out_ptr, stream))
+
+
+def fft_convolve(image, kernel, circular: bool = False, device: int = 0) -> np.ndarray:
+    """filters::fft_convolve (reference src/filters.cpp:174-264, registry op
+    "fft_convolve" :316-323) on the GPU: linear mode returns the centred
+    same-size result of the zero-padded convolution, circular mode the
+    periodic convolution with the kernel centre at index 0."""
+    a = _f32(image)
+    k = _f32(kernel)
+    out = np.empty_like(a)
+    _check(lib().vk_fft_convolve(device, a.ndim, _shape(a.shape), a.ctypes.data, k.ndim, _shape(k.shape),
+                                 k.ctypes.data_as(_fp), int(bool(circular)), out.ctypes.data))
+    return out
+
+
 def exported_symbols() -> List[str]:
     """Function names declared in include/vk_rl.h (for the ABI tests)."""
     import re
@@ -410,7 +457,7 @@ def exported_symbols() -> List[str]:
 
 __all__ = [
     "Error", "ShapeMismatch", "NegativeInput", "UnnormalizedPsf", "DegenerateReference", "TooSmall",
-    "OddExtent", "CudaError", "Unsupported", "StopMetric", "StoppingRule", "IterationRecord",
+    "OddExtent", "CudaError", "Unsupported", "KernelTooLarge", "ConvPlan", "fft_convolve", "StopMetric", "StoppingRule", "IterationRecord",
     "IterationTrace", "RlResult", "RlTransforms", "RlPlan", "richardson_lucy", "rl_step", "good_size",
     "to_string", "lib", "exported_symbols",
 ]

@@ -68,4 +68,117 @@ __global__ void frc_bins_kernel(const float2* __restrict__ A, const float2* __re
     if (hist[i] != 0.0) atomicAdd(&bins[i], hist[i]);
 }
 
+// ---------------------------------------------------------------------------
+// ssim_vs_prev: metrics::ssim(current, previous) (src/metrics.cpp:103-144)
+// with filters::gaussian(sigma 1.5, truncate 3.5) (src/filters.cpp:78-140).
+// Five moments (x, r, x^2, r^2, x r; the squares and product in f32 as
+// metrics.cpp:121-125 forms them) are smoothed by one separable 13-tap pass
+// per image axis with mirror boundary (nd_utils.hpp:31-38).  Like the
+// reference the passes accumulate in double, in tap order, with every product
+// and sum rounded separately (no FMA contraction), and keep double between
+// passes; the last pass rounds the five moments to f32 (filters.cpp:135-138)
+// and folds the SSIM map and its sum into the same kernel.  The moments stay
+// in HBM between passes: 40 B per voxel and field pair per pass.
+// ---------------------------------------------------------------------------
+
+constexpr int kSsimHalf = 6;  // ceil(3.5 * 1.5)
+struct SsimTaps {
+  double w[2 * kSsimHalf + 1];
+};
+
+// Crop the P-domain estimate into `cur` and record its [min, max] as f32 bits
+// (values are >= 0; -0 is ordered as +0) for the next iteration's range.
+__global__ void crop_range_kernel(const float* __restrict__ est, float* __restrict__ out, Geom g,
+                                  unsigned int* __restrict__ range) {
+  const size_t n = (size_t)g.Iz * g.Iy * g.Ix;
+  unsigned int mn = 0x7f800000u, mx = 0u;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % g.Ix);
+    const size_t t = i / g.Ix;
+    const int y = (int)(t % g.Iy), z = (int)(t / g.Iy);
+    const float v = est[((size_t)(z + g.oz) * g.Py + (y + g.oy)) * g.Px + (x + g.ox)];
+    out[i] = v;
+    const unsigned int b = v == 0.f ? 0u : __float_as_uint(v);
+    mn = min(mn, b);
+    mx = max(mx, b);
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+    mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMin(&range[0], mn);
+    atomicMax(&range[1], mx);
+  }
+}
+
+__device__ __forceinline__ int ssim_mirror(int i, int n) {  // |offset| <= 6 < n
+  if (i < 0) return -i;
+  if (i >= n) return 2 * (n - 1) - i;
+  return i;
+}
+
+// One smoothing pass along an axis of extent `ext` and element stride
+// `stride`.  FIRST: the moments come from (xc, rp); otherwise from `in`
+// (5 fields of n doubles).  LAST: no store; the SSIM map is summed into *sum
+// with c1, c2 from the previous image's range (range[0..1] = f32 bits).
+template <bool FIRST, bool LAST>
+__global__ void __launch_bounds__(256) ssim_axis_kernel(const float* __restrict__ xc, const float* __restrict__ rp,
+                                                        const double* __restrict__ in, double* __restrict__ out,
+                                                        size_t n, int ext, size_t stride, SsimTaps t,
+                                                        const unsigned int* __restrict__ range,
+                                                        double* __restrict__ sum) {
+  double c1 = 0, c2 = 0;
+  if (LAST) {
+    const double r = (double)__uint_as_float(range[1]) - (double)__uint_as_float(range[0]);
+    c1 = __dmul_rn(__dmul_rn(0.01, r), __dmul_rn(0.01, r));
+    c2 = __dmul_rn(__dmul_rn(0.03, r), __dmul_rn(0.03, r));
+  }
+  double part = 0.0;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)((i / stride) % (size_t)ext);
+    const size_t base = i - (size_t)c * stride;
+    double acc[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+    for (int k = -kSsimHalf; k <= kSsimHalf; ++k) {
+      const size_t j = base + (size_t)ssim_mirror(c + k, ext) * stride;
+      const double w = t.w[k + kSsimHalf];
+      double v[5];
+      if (FIRST) {
+        const float a = xc[j], b = rp[j];
+        v[0] = a;
+        v[1] = b;
+        v[2] = __fmul_rn(a, a);
+        v[3] = __fmul_rn(b, b);
+        v[4] = __fmul_rn(a, b);
+      } else {
+#pragma unroll
+        for (int f = 0; f < 5; ++f) v[f] = in[f * n + j];
+      }
+#pragma unroll
+      for (int f = 0; f < 5; ++f) acc[f] = __dadd_rn(acc[f], __dmul_rn(w, v[f]));
+    }
+    if (!LAST) {
+#pragma unroll
+      for (int f = 0; f < 5; ++f) out[f * n + i] = acc[f];
+    } else {
+      // metrics.cpp:133-142 on the f32-rounded moments
+      const double mx = (float)acc[0], mr = (float)acc[1];
+      const double mxx = (float)acc[2], mrr = (float)acc[3], mxr = (float)acc[4];
+      const double var_x = __dsub_rn(mxx, __dmul_rn(mx, mx));
+      const double var_r = __dsub_rn(mrr, __dmul_rn(mr, mr));
+      const double cov = __dsub_rn(mxr, __dmul_rn(mx, mr));
+      const double num = __dmul_rn(__dadd_rn(__dmul_rn(__dmul_rn(2.0, mx), mr), c1),
+                                   __dadd_rn(__dmul_rn(2.0, cov), c2));
+      const double den = __dmul_rn(__dadd_rn(__dadd_rn(__dmul_rn(mx, mx), __dmul_rn(mr, mr)), c1),
+                                   __dadd_rn(__dadd_rn(var_x, var_r), c2));
+      part += __ddiv_rn(num, den);
+    }
+  }
+  if (LAST) {
+    double v1[1] = {part};
+    block_accumulate<1>(v1, sum);
+  }
+}
+
 }  // namespace vk

@@ -34,7 +34,9 @@ namespace vk {
 
 constexpr float kEps = 1e-12f;  // kDivEpsilon, include/voxelkit/core_ops.hpp:26
 
-enum XMode : int { XM_FWD = 0, XM_RATIO = 1, XM_UPDATE = 2, XM_UPDATE_LAST = 3 };
+// XM_CONV_OUT (generic kernel only): C2R and store of the cropped result,
+// for filters::fft_convolve plans.
+enum XMode : int { XM_FWD = 0, XM_RATIO = 1, XM_UPDATE = 2, XM_UPDATE_LAST = 3, XM_CONV_OUT = 4 };
 enum YMode : int { YM_FWD = 0, YM_INV = 1, YM_CONV = 2 };
 enum ZMode : int { ZM_CONV = 0, ZM_FWD_OUT = 1 };
 
@@ -187,6 +189,18 @@ __global__ void __launch_bounds__(256) xpass_kernel(const XArgs a) {
   float2* R = fft_lines<true>(A, B, L, LP, a.plan);
   float2* O = (R == A) ? B : A;
 
+  if (a.mode == XM_CONV_OUT) {  // P == I: every row is inside
+    for (int idx = threadIdx.x; idx < g.Px * 2 * L; idx += blockDim.x) {
+      const int x = idx / (2 * L), r = idx - x * 2 * L;
+      const int y = y0 + r;
+      if (y < g.Py) {
+        const float2 c = R[(x + g.cx) * LP + r % L];
+        a.out[((size_t)z * g.Py + y) * g.Px + x] = r / L ? c.y : c.x;
+      }
+    }
+    return;
+  }
+
   // 3. pointwise epilogue over the P-domain rows of this CTA
   double accv[3] = {0.0, 0.0, 0.0};
   const bool last = a.mode == XM_UPDATE_LAST;
@@ -334,7 +348,7 @@ __global__ void obs_stats_kernel(const float* __restrict__ obs, size_t n, ObsSta
     neg |= (o < 0.f) ? 1u : 0u;
     v[0] += o;
     v[1] += (double)o * o;
-    const unsigned int b = __float_as_uint(o);
+    const unsigned int b = o == 0.f ? 0u : __float_as_uint(o);  // -0 orders as +0
     if (!(o < 0.f)) {
       mn = min(mn, b);
       mx = max(mx, b);
@@ -376,6 +390,22 @@ __global__ void fill_mean_kernel(float* __restrict__ est, size_t n, const ObsSta
   const float mean = (float)(st->sump / (double)n);
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
     est[i] = mean;
+}
+
+// Circular-mode kernel of filters::fft_convolve (filters.cpp:215-233): the
+// kernel centre (K-1)/2 wrapped to index 0 of the W grid (dst pre-zeroed).
+__global__ void wrap_kernel_kernel(const float* __restrict__ k, int Kz, int Ky, int Kx, int Wz, int Wy, int Wx,
+                                   float* __restrict__ dst) {
+  const size_t n = (size_t)Kz * Ky * Kx;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % Kx);
+    const size_t t = i / Kx;
+    const int y = (int)(t % Ky), z = (int)(t / Ky);
+    const int wz = ((z - (Kz - 1) / 2) % Wz + Wz) % Wz;
+    const int wy = ((y - (Ky - 1) / 2) % Wy + Wy) % Wy;
+    const int wx = ((x - (Kx - 1) / 2) % Wx + Wx) % Wx;
+    dst[((size_t)wz * Wy + wy) * Wx + wx] = k[i];
+  }
 }
 
 // P -> I crop (deconv.cpp:239-252) for runs that stop early.

@@ -170,6 +170,7 @@ struct vk_rl_plan_s {
   int device = 0;
   int rank = 3;
   bool pad = true;
+  int conv = 0;  // 0: RL plan; 1 / 2: filters::fft_convolve plan, linear / circular
   uint64_t ishape[3]{}, dshape[3]{}, wshape[3]{}, kshape[3]{};
   Geom g{};
   int Kz = 1, Ky = 1, Kx = 1;
@@ -202,6 +203,15 @@ struct vk_rl_plan_s {
   int frc_nbins = 0;
   double frc_binf = 0;
   int frc_h[3]{1, 1, 1}, frc_s[3]{0, 0, 0};
+  // ssim_vs_prev stopping metric (rl_metrics.cuh): current / previous crops
+  // (ping-pong), two sets of five double moment fields, per-iteration crop
+  // ranges ([iters+1][2] f32 bits, row 0 = observed) and SSIM-map sums
+  DevBuf<float> ss_img[2];
+  DevBuf<double> ss_f[2];
+  DevBuf<unsigned> ss_range;
+  DevBuf<double> ss_sum;
+  int ss_cap = 0;
+  bool ss_ready = false;
   int xL = 1, yL = 1, zL = 1;
   size_t xs = 0, ys = 0, zs = 0;
 
@@ -555,9 +565,15 @@ void to3(int rank, const uint64_t* in, uint64_t* out3) {
 }
 
 vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank, const uint64_t* psf_shape,
-                       const float* psf, int pad) {
+                       const float* psf, int pad, int conv = 0) {
   if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
-  if (psf_rank != rank) fail(VK_ERR_SHAPE, "ShapeMismatch: psf rank must match the image rank");
+  if (psf_rank != rank)
+    fail(VK_ERR_SHAPE, conv ? "ShapeMismatch: fft_convolve: rank mismatch"
+                            : "ShapeMismatch: psf rank must match the image rank");
+  if (conv == 2)  // filters.cpp:184-190
+    for (int i = 0; i < rank; ++i)
+      if (psf_shape[i] > shape[i])
+        fail(VK_ERR_KERNEL_TOO_LARGE, "KernelTooLarge: circular convolution needs kernel <= image");
   for (int i = 0; i < rank; ++i) {
     if (shape[i] == 0) fail(VK_ERR_ARG, "empty image");
     if (psf_shape[i] == 0) fail(VK_ERR_ARG, "empty psf");
@@ -568,6 +584,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->device = device;
     p->rank = rank;
     p->pad = pad != 0;
+    p->conv = conv;
     uint64_t I3[3], K3[3];
     to3(rank, shape, I3);
     to3(rank, psf_shape, K3);
@@ -580,13 +597,17 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     for (int a = 0; a < 3; ++a) {
       const uint64_t off = p->pad ? K3[a] / 2 : 0;  // deconv.cpp:215-216
       const uint64_t P = I3[a] + 2 * off;
-      const uint64_t W = good_size(P + K3[a] - 1);  // deconv.cpp:116
+      // deconv.cpp:116 / filters.cpp:191-192; circular: the image grid itself
+      const uint64_t W = conv == 2 ? P : good_size(P + K3[a] - 1);
       if (P > (1u << 30) || W > (1u << 30)) fail(VK_ERR_ARG, "extent too large");
+      if (good_size(W) != W)
+        fail(VK_ERR_UNSUPPORTED, "circular fft_convolve on the B200 path needs 5-smooth extents (got " +
+                                     std::to_string(W) + ")");
       *Ip[a] = (int)I3[a];
       *Pp[a] = (int)P;
       *Op[a] = (int)off;
       *Wp[a] = (int)W;
-      *Cp[a] = (int)((K3[a] - 1) / 2);  // kernel_center, deconv.cpp:40
+      *Cp[a] = conv == 2 ? 0 : (int)((K3[a] - 1) / 2);  // kernel_center, deconv.cpp:40
     }
     g.Hx = g.Wx / 2 + 1;
     p->Kz = (int)K3[0];
@@ -682,6 +703,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       const char* nodf = std::getenv("VK_RL_NO_DATAFLOW");
       if (p->fy && p->fz && df_env && df_env[0] == '1' && !(nodf && nodf[0] == '1'))
         p->df = vk::df_lookup(g.Wy, g.Wz);
+      if (conv) p->fx = nullptr;  // XM_CONV_OUT lives in the generic x kernel
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
@@ -705,7 +727,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->SA.alloc(sa, "spectrum A");
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
     p->otf.alloc(so, "otf");
-    p->otf_flip.alloc(so, "otf_flip");
+    if (!conv) p->otf_flip.alloc(so, "otf_flip");
     p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
     if (p->df) setup_dataflow(p);
     p->stats.alloc(1, "stats");
@@ -716,7 +738,26 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     DevBuf<float> dpsf;
     dpsf.alloc(kn, "psf");
     ck(cudaMemcpyAsync(dpsf.p, psf, kn * sizeof(float), cudaMemcpyHostToDevice, p->stream), "psf H2D");
+    if (conv == 2) {  // circular: centre-wrapped kernel on the full grid
+      DevBuf<float> wrapped;
+      const size_t wn = (size_t)g.Wz * g.Wy * g.Wx;
+      wrapped.alloc(wn, "wrapped kernel");
+      ck(cudaMemsetAsync(wrapped.p, 0, wn * sizeof(float), p->stream), "wrap");
+      vk::wrap_kernel_kernel<<<148, kThreads, 0, p->stream>>>(dpsf.p, p->Kz, p->Ky, p->Kx, g.Wz, g.Wy, g.Wx,
+                                                               wrapped.p);
+      launch_check(p, "wrap kernel");
+      spectrum3d(p, p->stream, wrapped.p, g.Wz, g.Wy, g.Wx,
+                 (float)(1.0 / ((double)g.Wz * g.Wy * g.Wx)), p->otf.p);
+      ck(cudaStreamSynchronize(p->stream), "otf");
+      p->launches = 0;
+      return p;
+    }
     build_otf(p, dpsf.p, p->otf.p);
+    if (conv) {
+      ck(cudaStreamSynchronize(p->stream), "otf");
+      p->launches = 0;
+      return p;
+    }
     ck(cudaStreamSynchronize(p->stream), "otf");
     ck(cudaMemcpyAsync(dpsf.p, flipped.data(), kn * sizeof(float), cudaMemcpyHostToDevice, p->stream),
        "psf H2D");
@@ -858,16 +899,89 @@ double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
   return std::numeric_limits<double>::infinity();  // kUnresolved
 }
 
+// Buffers for ssim_vs_prev (metrics.cpp:103-144): TooSmall below 7 voxels
+// per axis (raised at the first metric evaluation in the reference, before
+// any estimate is returned either way).
+void setup_ssim(vk_rl_plan p, int iters) {
+  for (int a = 0; a < p->rank; ++a)
+    if (p->ishape[a] < 7) fail(VK_ERR_TOO_SMALL, "ssim needs every extent >= 7");
+  const Geom& g = p->g;
+  const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
+  if (!p->ss_ready) {
+    for (auto& b : p->ss_img) b.alloc(nI, "ssim images");
+    for (int k = 0; k < std::min(p->rank - 1, 2); ++k) p->ss_f[k].alloc(5 * nI, "ssim moments");
+    p->ss_ready = true;
+  }
+  if (iters > p->ss_cap) {
+    p->ss_range.alloc((size_t)(iters + 1) * 2, "ssim ranges");
+    p->ss_sum.alloc((size_t)iters, "ssim sums");
+    p->ss_cap = iters;
+  }
+}
+
+// ssim(crop(est), previous) for iteration `it` (1-based); previous is the
+// observed image at it = 1 and the crop of iteration it-1 afterwards
+// (deconv.cpp:352, 403, 423).  The sum lands in ss_sum[it-1]; no sync.
+void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
+  const Geom& g = p->g;
+  const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
+  float* cur = p->ss_img[it % 2].p;
+  const float* prev = it == 1 ? d_obs : p->ss_img[(it - 1) % 2].p;
+  vk::crop_range_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, cur, g, p->ss_range.p + 2 * it);
+  launch_check(p, "ssim crop");
+  static const vk::SsimTaps taps = [] {  // filters.cpp:78-90
+    vk::SsimTaps t{};
+    const double sigma = 1.5;
+    double sum = 0;
+    for (int i = -vk::kSsimHalf; i <= vk::kSsimHalf; ++i) {
+      const double v = std::exp(-0.5 * (i / sigma) * (i / sigma));
+      t.w[i + vk::kSsimHalf] = v;
+      sum += v;
+    }
+    for (double& v : t.w) v /= sum;
+    return t;
+  }();
+  const unsigned* range = p->ss_range.p + 2 * (it - 1);
+  double* sum = p->ss_sum.p + (it - 1);
+  const int grid = 148 * 8;
+  size_t stride = 1;
+  size_t strides[3];
+  for (int a = p->rank - 1; a >= 0; --a) {
+    strides[a] = stride;
+    stride *= p->ishape[a];
+  }
+  for (int k = 0; k < p->rank; ++k) {
+    const int ext = (int)p->ishape[k];
+    const double* in = k == 0 ? nullptr : p->ss_f[(k - 1) % 2].p;
+    double* out = k == p->rank - 1 ? nullptr : p->ss_f[k % 2].p;
+    const bool first = k == 0, last = k == p->rank - 1;
+    if (first && last)
+      vk::ssim_axis_kernel<true, true><<<grid, kThreads, 0, s>>>(cur, prev, in, out, nI, ext, strides[k], taps,
+                                                                   range, sum);
+    else if (first)
+      vk::ssim_axis_kernel<true, false><<<grid, kThreads, 0, s>>>(cur, prev, in, out, nI, ext, strides[k], taps,
+                                                                    range, sum);
+    else if (last)
+      vk::ssim_axis_kernel<false, true><<<grid, kThreads, 0, s>>>(cur, prev, in, out, nI, ext, strides[k], taps,
+                                                                    range, sum);
+    else
+      vk::ssim_axis_kernel<false, false><<<grid, kThreads, 0, s>>>(cur, prev, in, out, nI, ext, strides[k],
+                                                                     taps, range, sum);
+    launch_check(p, "ssim pass");
+  }
+}
+
 // The richardson_lucy loop on device buffers (deconv.cpp:333-430).
 void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_rule* rule, int flat_init,
                 vk_trace* trace, cudaStream_t s, bool check_obs) {
   check_rule(rule);
+  if (p->conv) fail(VK_ERR_ARG, "plan was created for fft_convolve");
   if (!p->pad) fail(VK_ERR_ARG, "plan was created without padding (rl_step plan)");
-  if (rule->metric == VK_METRIC_SSIM_VS_PREV)
-    fail(VK_ERR_UNSUPPORTED, "ssim_vs_prev stopping metric is not implemented on the B200 path yet");
-  if (rule->metric != VK_METRIC_SI_PSNR_VS_INPUT && rule->metric != VK_METRIC_FRC_RESOLUTION)
+  if (rule->metric != VK_METRIC_SI_PSNR_VS_INPUT && rule->metric != VK_METRIC_FRC_RESOLUTION &&
+      rule->metric != VK_METRIC_SSIM_VS_PREV)
     fail(VK_ERR_ARG, "unknown stopping metric");
   const bool frc = rule->metric == VK_METRIC_FRC_RESOLUTION;
+  const bool ssim = rule->metric == VK_METRIC_SSIM_VS_PREV;
   const double spacing = rule->spacing > 0 ? rule->spacing : 1.0;
   const Geom& g = p->g;
   const int iters = rule->max_iters;
@@ -895,8 +1009,22 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   const RefStats rs{(double)nI, st.sr, st.srr, (double)fmax - (double)fmin};
   // DegenerateReference surfaces at the first metric evaluation in the
   // reference; no estimate is returned either way.
-  if (!frc) si_psnr_from_sums(rs, 0.0, 0.0, 0.0);
+  if (!frc && !ssim) si_psnr_from_sums(rs, 0.0, 0.0, 0.0);
   if (frc) setup_frc(p);
+  if (ssim) {
+    setup_ssim(p, iters);
+    std::vector<unsigned> r0((size_t)(iters + 1) * 2);
+    for (size_t i = 0; i < r0.size(); i += 2) {
+      r0[i] = 0x7f800000u;
+      r0[i + 1] = 0u;
+    }
+    r0[0] = st.minbits;  // row 0: the observed image (the first `previous`)
+    r0[1] = st.maxbits;
+    ck(cudaMemcpyAsync(p->ss_range.p, r0.data(), r0.size() * sizeof(unsigned), cudaMemcpyHostToDevice, s),
+       "ssim ranges");
+    ck(cudaMemsetAsync(p->ss_sum.p, 0, (size_t)iters * sizeof(double), s), "ssim sums");
+    ck(cudaStreamSynchronize(s), "ssim init");  // r0 is pageable
+  }
 
   vk::pad_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p);
   launch_check(p, "pad");
@@ -922,14 +1050,21 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     conv_yz(p, s, p->otf_flip.p);
     // the last iteration writes the cropped output directly unless a metric
     // still needs the updated estimate
-    const bool last = it == iters && !frc;
+    const bool last = it == iters && !frc && !ssim;
     x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc,
            last ? d_out : nullptr);
     if (frc) values.push_back(frc_eval(p, s, spacing));  // syncs: the value is needed on the host
+    if (ssim) ssim_eval(p, s, it, d_obs);
     ck(cudaEventRecord(p->events[it], s), "event");
     run = it;
     if (may_stop && it >= rule->patience + 1 && it < iters) {
-      if (!frc) {
+      if (ssim) {
+        std::vector<double> sums(it);
+        ck(cudaMemcpyAsync(sums.data(), p->ss_sum.p, (size_t)it * sizeof(double), cudaMemcpyDeviceToHost, s),
+           "ssim D2H");
+        ck(cudaStreamSynchronize(s), "iteration");
+        while ((int)values.size() < it) values.push_back(sums[values.size()] / (double)nI);
+      } else if (!frc) {
         ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)it * 4 * sizeof(double), cudaMemcpyDeviceToHost, s),
            "acc D2H");
         ck(cudaStreamSynchronize(s), "iteration");
@@ -959,12 +1094,18 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
       }
     }
   }
-  if (frc && !stopped) {  // the last iteration ran in UPDATE mode: crop now
+  if ((frc || ssim) && !stopped) {  // the last iteration ran in UPDATE mode: crop now
     vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
     launch_check(p, "crop");
   }
   ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
   ck(cudaStreamSynchronize(s), "run");
+  if (ssim) {
+    std::vector<double> sums(run);
+    ck(cudaMemcpy(sums.data(), p->ss_sum.p, (size_t)run * sizeof(double), cudaMemcpyDeviceToHost), "ssim D2H");
+    values.resize(run);
+    for (int k = 0; k < run; ++k) values[k] = sums[k] / (double)nI;
+  }
   prof_collect(p);
   if (trace) {
     trace->iters_run = run;
@@ -972,7 +1113,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     for (int i = 0; i < 3; ++i) trace->fft_shape[i] = i < p->rank ? p->wshape[i] : 0;
     for (int k = 0; k < run && k < trace->capacity; ++k) {
       const double* a = p->h_acc + (size_t)k * 4;
-      if (trace->metric) trace->metric[k] = frc ? values[k] : si_psnr_from_sums(rs, a[1], a[2], a[3]);
+      if (trace->metric) trace->metric[k] = (frc || ssim) ? values[k] : si_psnr_from_sums(rs, a[1], a[2], a[3]);
       if (trace->log_likelihood) trace->log_likelihood[k] = a[0];
       if (trace->wall_s) {
         float ms = 0;
@@ -983,7 +1124,20 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
 }
 
+// filters::fft_convolve on a conv plan (filters.cpp:174-264): R2C of the
+// image, times the kernel spectrum (1/prod(W) folded in), C2R and the crop at
+// the kernel centre (linear) or at 0 (circular).
+void conv_device(vk_rl_plan p, const float* d_img, float* d_out, cudaStream_t s) {
+  if (!p->conv) fail(VK_ERR_ARG, "plan was not created by vk_conv_plan_create");
+  const Geom& g = p->g;
+  p->launches = 0;
+  x_pass(p, s, vk::XM_FWD, d_img, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr, 0);
+  conv_yz(p, s, p->otf.p);
+  x_pass(p, s, vk::XM_CONV_OUT, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, nullptr, nullptr, d_out);
+}
+
 void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_out, cudaStream_t s) {
+  if (p->conv) fail(VK_ERR_ARG, "plan was created for fft_convolve");
   if (p->pad) fail(VK_ERR_ARG, "rl_step needs a plan created with pad_replicate = 0");
   const Geom& g = p->g;
   ensure_iter_buffers(p, 1);
@@ -1054,7 +1208,11 @@ vk_status vk_rl_plan_device_bytes(vk_rl_plan p, uint64_t* bytes) {
   return guarded([&] {
     if (!p || !bytes) fail(VK_ERR_ARG, "NULL argument");
     *bytes = (p->SA.n + p->SB.n + p->otf.n + p->otf_flip.n) * sizeof(float2) +
-             (p->est.n + p->obs.n + p->out.n) * sizeof(float) + p->acc.n * sizeof(double);
+             (p->est.n + p->obs.n + p->out.n) * sizeof(float) + p->acc.n * sizeof(double) +
+             p->ring.n * sizeof(float2) + (p->ss_img[0].n + p->ss_img[1].n) * sizeof(float) +
+             (p->ss_f[0].n + p->ss_f[1].n + p->ss_sum.n) * sizeof(double) +
+             (p->frc_even.n + p->frc_odd.n) * sizeof(float);
+    if (p->frc) *bytes += (p->frc->SA.n + p->frc->SB.n + p->frc->otf.n + p->frc->otf_flip.n) * sizeof(float2);
   });
 }
 
@@ -1214,6 +1372,49 @@ vk_status vk_rl_step_psf(int device, int rank, const uint64_t* shape, const floa
   });
   if (st != VK_OK) return st;
   st = vk_rl_step(p, e, o, out);
+  std::string keep = g_last_error;
+  vk_rl_plan_destroy(p);
+  g_last_error = keep;
+  return st;
+}
+
+vk_status vk_conv_plan_create(int device, int rank, const uint64_t* shape, int kernel_rank,
+                              const uint64_t* kernel_shape, const float* kernel, int circular, vk_rl_plan* out) {
+  return guarded([&] {
+    if (!shape || !kernel_shape || !kernel || !out) fail(VK_ERR_ARG, "NULL argument");
+    *out = create_plan(device, rank, shape, kernel_rank, kernel_shape, kernel, 0, circular ? 2 : 1);
+  });
+}
+
+vk_status vk_conv_run_device(vk_rl_plan p, const float* d_img, float* d_out, void* stream) {
+  return guarded([&] {
+    if (!p || !d_img || !d_out) fail(VK_ERR_ARG, "NULL argument");
+    DeviceGuard dg(p->device);
+    conv_device(p, d_img, d_out, (cudaStream_t)stream);
+  });
+}
+
+vk_status vk_conv_run(vk_rl_plan p, const float* img, float* out) {
+  return guarded([&] {
+    if (!p || !img || !out) fail(VK_ERR_ARG, "NULL argument");
+    DeviceGuard dg(p->device);
+    const size_t n = image_count(p);
+    DevBuf<float> di, dout;
+    di.alloc(n, "image");
+    dout.alloc(n, "output");
+    ck(cudaMemcpyAsync(di.p, img, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
+    conv_device(p, di.p, dout.p, p->stream);
+    ck(cudaMemcpyAsync(out, dout.p, n * sizeof(float), cudaMemcpyDeviceToHost, p->stream), "D2H");
+    ck(cudaStreamSynchronize(p->stream), "fft_convolve");
+  });
+}
+
+vk_status vk_fft_convolve(int device, int rank, const uint64_t* shape, const float* img, int kernel_rank,
+                          const uint64_t* kernel_shape, const float* kernel, int circular, float* out) {
+  vk_rl_plan p = nullptr;
+  vk_status st = vk_conv_plan_create(device, rank, shape, kernel_rank, kernel_shape, kernel, circular, &p);
+  if (st != VK_OK) return st;
+  st = vk_conv_run(p, img, out);
   std::string keep = g_last_error;
   vk_rl_plan_destroy(p);
   g_last_error = keep;

@@ -146,5 +146,25 @@ def main():
         print("err", name, errs[name])
 
 
+def gaussian_fixtures():
+    """filters::gaussian (sigma 1.5, truncate 3.5: the ssim window) on 1D/2D/3D
+    inputs.  The reference's metrics::ssim itself reads freed temporaries
+    (it returns NaN or values > 1 here), so ssim parity is
+    pinned on this filter plus the restated formula."""
+    rng = np.random.default_rng(1505)
+    out = {}
+    for i, shp in enumerate([(64,), (40, 52), (9, 12, 15)]):
+        a = (rng.random(shp) * 3).astype(np.float32)
+        out[f"in{i}"] = a
+        out[f"out{i}"] = ref.gaussian(a, 1.5, 3.5)
+        out[f"sq{i}"] = ref.gaussian(a * a, 1.5, 3.5)
+    np.savez_compressed(os.path.join(OUT, "gaussian_ssim.npz"), **out)
+    print("gaussian_ssim", [v.shape for k, v in out.items() if k.startswith("in")])
+
+
 if __name__ == "__main__":
-    main()
+    if sys.argv[1:] == ["gaussian"]:
+        gaussian_fixtures()
+    else:
+        main()
+        gaussian_fixtures()

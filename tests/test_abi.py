@@ -15,7 +15,7 @@ def test_header_symbols_exported():
     L = vk.lib()
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
-    assert L.vk_abi_version() == 2
+    assert L.vk_abi_version() == 3
 
 
 def test_good_size_matches_oracle():

@@ -51,6 +51,26 @@ def test_fft_convolve_golden():
     assert rel_l2(O.fft_convolve(g["img"], g["kernel"], True), g["circular"]) <= 1e-7
 
 
+def test_ssim_gaussian_bit_exact_vs_reference():
+    """The ssim window (filters::gaussian, sigma 1.5, truncate 3.5) reproduces
+    the reference bit for bit, so ssim parity rests on the formula alone."""
+    g = load_golden(golden_files("gaussian_ssim")[0])
+    for i in range(3):
+        a = g[f"in{i}"]
+        assert np.array_equal(O.gaussian(a), g[f"out{i}"])
+        assert np.array_equal(O.gaussian(a * a), g[f"sq{i}"])
+
+
+def test_ssim_oracle_properties():
+    rng = np.random.default_rng(2)
+    a = (rng.random((9, 10, 11)) * 2).astype(np.float32)
+    assert abs(O.ssim(a, a) - 1.0) < 1e-12
+    b = (a + 0.3 * rng.random(a.shape)).astype(np.float32)
+    assert 0 < O.ssim(b, a) < 1
+    with pytest.raises(O.OracleError, match="ssim needs every extent >= 7"):
+        O.ssim(a[:6], a[:6])
+
+
 @pytest.mark.parametrize("path", golden_files("err_"), ids=os.path.basename)
 def test_validation_order_and_messages(path):
     g = load_golden(path)

@@ -351,8 +351,44 @@ def test_plan_reuse_batch_and_device_api():
     assert rel_l2(batch[2].estimate, its[-1]) <= TOL_N
 
 
-def test_unsupported_metric_is_loud():
+def test_ssim_too_small_is_loud():
     psf = O.gaussian_psf((3, 3, 3), 1.0)
     obs = np.ones((6, 8, 8), np.float32) + np.arange(384, dtype=np.float32).reshape(6, 8, 8) / 384
-    with pytest.raises(vk.Error):
+    with pytest.raises(vk.TooSmall, match="ssim needs every extent >= 7"):
         vk.richardson_lucy(obs, psf, vk.StoppingRule("ssim_vs_prev", 1e-3, 3, 5))
+
+
+SSIM_CASES = [((12, 20, 24), (5, 5, 5), 4), ((40, 52), (9, 9), 4), ((64,), (7,), 3), ((7, 9, 11), (3, 3, 3), 3)]
+
+
+@pytest.mark.parametrize("shape,kshape,iters", SSIM_CASES, ids=lambda v: "x".join(map(str, v)) if
+                         isinstance(v, tuple) else str(v))
+def test_ssim_metric_on_device_iterates(shape, kshape, iters):
+    """The device ssim_vs_prev values against the oracle's ssim evaluated on
+    the device's own iterates (out_0 = observed): isolates the metric, which
+    the device computes in the reference's rounding order."""
+    rng = np.random.default_rng(5)
+    obs = (rng.random(shape) * 3 + 0.2).astype(np.float32)
+    k = rng.random(kshape) + 0.5
+    psf = (k / k.sum()).astype(np.float32)
+    outs = [obs] + [vk.richardson_lucy(obs, psf, fixed_rule(i, "ssim_vs_prev")).estimate
+                    for i in range(1, iters + 1)]
+    rn = vk.richardson_lucy(obs, psf, fixed_rule(iters, "ssim_vs_prev"))
+    assert np.array_equal(rn.estimate, outs[-1])
+    want = [O.ssim(outs[i], outs[i - 1]) for i in range(1, iters + 1)]
+    got = [r.value for r in rn.trace.records]
+    np.testing.assert_allclose(got, want, rtol=1e-12)
+
+
+def test_ssim_rule_matches_oracle_run():
+    """Full RL with the ssim_vs_prev rule (early stop) against the oracle."""
+    psf = O.gaussian_psf((5, 5, 5), 1.0)
+    obs = synth.blurred(synth.blobs((16, 32, 32), 3, 2.0, 4.0, seed=3), psf) + np.float32(0.05)
+    e, t = O.richardson_lucy(obs, psf, "ssim_vs_prev", 1e-4, 2, 40)
+    r = vk.richardson_lucy(obs, psf, vk.StoppingRule("ssim_vs_prev", 1e-4, 2, 40))
+    assert r.trace.stop_reason == t.stop_reason
+    assert len(r.trace.records) == len(t.metric)
+    np.testing.assert_allclose([x.value for x in r.trace.records], t.metric, rtol=1e-6)
+    assert rel_l2(r.estimate, e) <= TOL_N
+
+
