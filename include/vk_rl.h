@@ -47,7 +47,12 @@ typedef enum vk_status {
   VK_ERR_CUDA = 8,             /* CUDA runtime failure            */
   VK_ERR_OOM = 9,              /* device allocation failure       */
   VK_ERR_UNSUPPORTED = 10,     /* not implemented on this path    */
-  VK_ERR_KERNEL_TOO_LARGE = 11 /* voxelkit::KernelTooLarge        */
+  VK_ERR_KERNEL_TOO_LARGE = 11, /* voxelkit::KernelTooLarge       */
+  VK_ERR_BAD_MAGIC = 12,        /* voxelkit::BadMagic             */
+  VK_ERR_HEADER_MISMATCH = 13,  /* voxelkit::HeaderMismatch       */
+  VK_ERR_TRUNCATED = 14,        /* voxelkit::TruncatedPayload     */
+  VK_ERR_PLACEMENT = 15,        /* voxelkit::PlacementFailure     */
+  VK_ERR_EVEN_EXTENT = 16       /* voxelkit::EvenExtent           */
 } vk_status;
 
 /* deconv::StopMetric (deconv.hpp:28) */

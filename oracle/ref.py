@@ -23,7 +23,8 @@ _i32p = ctypes.POINTER(ctypes.c_int)
 # Status codes shared with include/vk_rl.h.
 CODE_NAMES = {1: "Error", 2: "ShapeMismatch", 3: "NegativeInput", 4: "UnnormalizedPsf",
               5: "DegenerateReference", 6: "TooSmall", 7: "OddExtent", 11: "KernelTooLarge",
-              99: "Other"}
+              12: "BadMagic", 13: "HeaderMismatch", 14: "TruncatedPayload", 15: "PlacementFailure",
+              16: "EvenExtent", 99: "Other"}
 
 METRICS = {"si_psnr_vs_input": 0, "ssim_vs_prev": 1, "frc_resolution": 2}
 
@@ -80,6 +81,15 @@ def lib():
         L.vkref_gaussian.restype = ctypes.c_int
         L.vkref_gaussian.argtypes = [ctypes.c_int, _u64p, _f32p, ctypes.c_double, ctypes.c_double,
                                      _f32p, ctypes.c_char_p, ctypes.c_int]
+        if hasattr(L, "vkref_write_volume"):
+            L.vkref_write_volume.restype = ctypes.c_int
+            L.vkref_write_volume.argtypes = [ctypes.c_char_p, ctypes.c_int, ctypes.c_int, _u64p,
+                                             ctypes.c_void_p, _f64p, ctypes.c_char_p, ctypes.c_int]
+            L.vkref_read_volume.restype = ctypes.c_int
+            L.vkref_read_volume.argtypes = [ctypes.c_char_p, ctypes.POINTER(ctypes.c_int),
+                                            ctypes.POINTER(ctypes.c_int), _u64p,
+                                            ctypes.POINTER(ctypes.c_int), _f64p, _f32p,
+                                            ctypes.c_uint64, ctypes.c_char_p, ctypes.c_int]
         _lib = L
     return _lib
 
@@ -216,3 +226,38 @@ def gaussian(x, sigma=1.5, truncate=3.5) -> np.ndarray:
                               _fp(out), err, 512)
     _check(rc, err)
     return out
+
+
+_ELEM = {np.dtype(np.float32): 0, np.dtype(np.uint16): 1, np.dtype(np.uint32): 2, np.dtype(np.bool_): 3}
+
+
+def write_volume(path, arr, spacing=None) -> None:
+    """io::write_volume (reads the reference's own bytes; needs io.cpp built)."""
+    a = np.ascontiguousarray(arr)
+    if a.dtype == np.bool_:
+        a = a.astype(np.uint8)
+        elem = 3
+    else:
+        elem = _ELEM[a.dtype]
+    sp = None if spacing is None else np.ascontiguousarray(spacing, np.float64)
+    err = ctypes.create_string_buffer(512)
+    rc = lib().vkref_write_volume(str(path).encode(), elem, a.ndim, _shape(a.shape), a.ctypes.data,
+                                  None if sp is None else sp.ctypes.data_as(_f64p), err, 512)
+    _check(rc, err)
+
+
+def read_volume(path):
+    """io::read_volume -> (f32 values, elem id, spacing or None)."""
+    elem, rank, has = ctypes.c_int(0), ctypes.c_int(0), ctypes.c_int(0)
+    shape = (ctypes.c_uint64 * 4)()
+    sp = (ctypes.c_double * 4)()
+    err = ctypes.create_string_buffer(512)
+    rc = lib().vkref_read_volume(str(path).encode(), ctypes.byref(elem), ctypes.byref(rank), shape,
+                                 ctypes.byref(has), sp, None, 0, err, 512)
+    _check(rc, err)
+    shp = tuple(int(shape[i]) for i in range(rank.value))
+    out = np.empty(shp, np.float32)
+    rc = lib().vkref_read_volume(str(path).encode(), ctypes.byref(elem), ctypes.byref(rank), shape,
+                                 ctypes.byref(has), sp, _fp(out), out.size, err, 512)
+    _check(rc, err)
+    return out, elem.value, (tuple(sp[i] for i in range(rank.value)) if has.value else None)

@@ -15,6 +15,8 @@
 //   vkref_single_image_frc-> metrics::single_image_frc   (proj/src/metrics.cpp:241-264)
 //   vkref_ssim            -> metrics::ssim (as shipped)  (proj/src/metrics.cpp:103-144)
 //   vkref_gaussian        -> filters::gaussian           (proj/src/filters.cpp:78-140)
+//   vkref_write_volume    -> io::write_volume (f32 / u16)  (proj/src/io.cpp:53-81)
+//   vkref_read_volume     -> io::read_volume              (proj/src/io.cpp:83-158)
 // Exceptions are mapped to the same status codes the product C-ABI uses
 // (include/vk_rl.h) so error-parity tests compare like with like.
 #include <cstdint>
@@ -27,6 +29,7 @@
 #include "voxelkit/errors.hpp"
 #include "voxelkit/filters.hpp"
 #include "voxelkit/image.hpp"
+#include "voxelkit/io.hpp"
 #include "voxelkit/metrics.hpp"
 #include "voxelkit/synth.hpp"
 #include "fft_plan.hpp"
@@ -45,6 +48,11 @@ enum {
   E_TOO_SMALL = 6,
   E_ODD = 7,
   E_KERNEL_TOO_LARGE = 11,
+  E_BAD_MAGIC = 12,
+  E_HEADER_MISMATCH = 13,
+  E_TRUNCATED = 14,
+  E_PLACEMENT = 15,
+  E_EVEN_EXTENT = 16,
   E_OTHER = 99,
 };
 
@@ -77,6 +85,11 @@ int fail(const std::exception& e, int code, char* err, int errlen) {
   catch (const TooSmall& e) { return fail(e, E_TOO_SMALL, err, errlen); } \
   catch (const OddExtent& e) { return fail(e, E_ODD, err, errlen); }       \
   catch (const KernelTooLarge& e) { return fail(e, E_KERNEL_TOO_LARGE, err, errlen); } \
+  catch (const BadMagic& e) { return fail(e, E_BAD_MAGIC, err, errlen); } \
+  catch (const HeaderMismatch& e) { return fail(e, E_HEADER_MISMATCH, err, errlen); } \
+  catch (const TruncatedPayload& e) { return fail(e, E_TRUNCATED, err, errlen); } \
+  catch (const PlacementFailure& e) { return fail(e, E_PLACEMENT, err, errlen); } \
+  catch (const EvenExtent& e) { return fail(e, E_EVEN_EXTENT, err, errlen); } \
   catch (const Error& e) { return fail(e, E_ARG, err, errlen); }           \
   catch (const std::exception& e) { return fail(e, E_OTHER, err, errlen); }
 
@@ -220,5 +233,54 @@ int vkref_gaussian(int rank, const std::uint64_t* shape, const float* x, double 
   }
   VKREF_CATCH
 }
+
+#ifdef VKREF_HAVE_IO
+// elem 0 = f32, 1 = u16, 2 = u32, 3 = bool; spacing may be NULL.
+int vkref_write_volume(const char* path, int elem, int rank, const std::uint64_t* shape,
+                       const void* data, const double* spacing, char* err, int errlen) {
+  try {
+    const Shape sh = to_shape(rank, shape);
+    const std::size_t n = shape_volume(sh);
+    NdImage img;
+    if (elem == 0) {
+      const float* p = static_cast<const float*>(data);
+      img = NdImage::f32(sh, std::vector<float>(p, p + n));
+    } else if (elem == 1) {
+      const std::uint16_t* p = static_cast<const std::uint16_t*>(data);
+      img = NdImage::u16(sh, std::vector<std::uint16_t>(p, p + n));
+    } else if (elem == 2) {
+      const std::uint32_t* p = static_cast<const std::uint32_t*>(data);
+      img = NdImage::labels(sh, std::vector<std::uint32_t>(p, p + n));
+    } else {
+      const std::uint8_t* p = static_cast<const std::uint8_t*>(data);
+      img = NdImage::boolean(sh, std::vector<std::uint8_t>(p, p + n));
+    }
+    if (spacing) img = img.with_spacing(std::vector<double>(spacing, spacing + rank));
+    io::write_volume(path, img);
+    return OK;
+  }
+  VKREF_CATCH
+}
+
+// Reads into f32 (as_f32); shape/rank/elem/spacing reported.
+int vkref_read_volume(const char* path, int* elem, int* rank, std::uint64_t* shape, int* has_spacing,
+                      double* spacing, float* out, std::uint64_t out_cap, char* err, int errlen) {
+  try {
+    const NdImage img = io::read_volume(path);
+    *elem = img.elem() == Elem::f32 ? 0 : img.elem() == Elem::u16 ? 1 : img.elem() == Elem::u32_label ? 2 : 3;
+    *rank = static_cast<int>(img.rank());
+    for (std::size_t a = 0; a < img.rank() && a < 4; ++a) shape[a] = img.shape()[a];
+    *has_spacing = img.spacing() ? 1 : 0;
+    if (img.spacing())
+      for (std::size_t a = 0; a < img.rank() && a < 4; ++a) spacing[a] = (*img.spacing())[a];
+    if (out) {
+      const auto v = img.as_f32().f32_values();
+      std::memcpy(out, v.data(), std::min<std::uint64_t>(out_cap, v.size()) * sizeof(float));
+    }
+    return OK;
+  }
+  VKREF_CATCH
+}
+#endif
 
 }  // extern "C"

@@ -29,6 +29,7 @@ import numpy as np
 _HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.environ.get("VK_RL_LIB") or os.path.join(_HERE, "lib", "libvkrl.so")
 HEADER_PATH = os.path.join(os.path.dirname(_HERE), "include", "vk_rl.h")
+HEADER_PATHS = [HEADER_PATH, os.path.join(os.path.dirname(_HERE), "include", "vk_io.h")]
 
 
 # --- errors (reference: proj/include/voxelkit/errors.hpp:25-70) -------------
@@ -72,11 +73,32 @@ class KernelTooLarge(Error):
     pass
 
 
+class BadMagic(Error):
+    pass
+
+
+class HeaderMismatch(Error):
+    pass
+
+
+class TruncatedPayload(Error):
+    pass
+
+
+class PlacementFailure(Error):
+    pass
+
+
+class EvenExtent(Error):
+    pass
+
+
 KERNEL_KINDS = ("x_fwd", "x_ratio", "x_update", "y_fwd", "z_conv", "y_inv", "y_conv", "yz_dataflow",
                 "yz_cluster")  # vk_kernel_kind
 
 _STATUS = {1: Error, 2: ShapeMismatch, 3: NegativeInput, 4: UnnormalizedPsf, 5: DegenerateReference,
-           6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported, 11: KernelTooLarge}
+           6: TooSmall, 7: OddExtent, 8: CudaError, 9: CudaError, 10: Unsupported, 11: KernelTooLarge,
+           12: BadMagic, 13: HeaderMismatch, 14: TruncatedPayload, 15: PlacementFailure, 16: EvenExtent}
 
 
 # --- ctypes binding -----------------------------------------------------------
@@ -92,6 +114,18 @@ class _Trace(ctypes.Structure):
     _fields_ = [("capacity", ctypes.c_int), ("metric", _dp), ("wall_s", _dp), ("log_likelihood", _dp),
                 ("iters_run", ctypes.c_int), ("stop_reason", ctypes.c_int),
                 ("fft_shape", ctypes.c_uint64 * 3)]
+
+
+class _VolumeInfo(ctypes.Structure):
+    _fields_ = [("elem", ctypes.c_int), ("rank", ctypes.c_int), ("shape", ctypes.c_uint64 * 4),
+                ("has_spacing", ctypes.c_int), ("spacing", ctypes.c_double * 4),
+                ("payload_offset", ctypes.c_uint64), ("payload_bytes", ctypes.c_uint64)]
+
+
+class _SynthSpec(ctypes.Structure):
+    _fields_ = [("shape", ctypes.c_uint64 * 3), ("n_objects", ctypes.c_uint64), ("radius_min", ctypes.c_double),
+                ("radius_max", ctypes.c_double), ("seed", ctypes.c_uint64), ("noise_sigma", ctypes.c_double),
+                ("anisotropy", ctypes.c_double), ("inplane_margin", ctypes.c_double)]
 
 
 _u64p = ctypes.POINTER(ctypes.c_uint64)
@@ -139,6 +173,16 @@ def lib() -> ctypes.CDLL:
     L.vk_rl_plan_profile_read.argtypes = [_vp, i, _dp, _u64p, _u64p, i]
     L.vk_rl_plan_profile.restype = st
     L.vk_rl_plan_profile_read.restype = st
+    L.vk_volume_info_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(_VolumeInfo)]
+    L.vk_volume_read.argtypes = [ctypes.c_char_p, ctypes.POINTER(_VolumeInfo), _vp, ctypes.c_uint64]
+    L.vk_volume_read_device.argtypes = [ctypes.c_char_p, ctypes.POINTER(_VolumeInfo), _vp, ctypes.c_uint64, _vp]
+    L.vk_volume_write.argtypes = [ctypes.c_char_p, ctypes.POINTER(_VolumeInfo), _vp]
+    L.vk_volume_write_device.argtypes = [ctypes.c_char_p, ctypes.POINTER(_VolumeInfo), _vp, _vp]
+    L.vk_generate_blobs.argtypes = [i, ctypes.POINTER(_SynthSpec), _vp, _dp, _vp]
+    L.vk_gaussian_psf.argtypes = [i, _u64p, _dp, i, _fp]
+    for name in ("vk_volume_info_read", "vk_volume_read", "vk_volume_read_device", "vk_volume_write",
+                 "vk_volume_write_device", "vk_generate_blobs", "vk_gaussian_psf"):
+        getattr(L, name).restype = st
     L.vk_good_size.argtypes = [ctypes.c_uint64]
     L.vk_good_size.restype = ctypes.c_uint64
     L.vk_last_error.restype = ctypes.c_char_p
@@ -447,11 +491,136 @@ def fft_convolve(image, kernel, circular: bool = False, device: int = 0) -> np.n
     return out
 
 
+# --- NDIV volumes and synthetic inputs (include/vk_io.h) ----------------------
+_ELEM_DTYPE = {0: np.float32, 1: np.uint16, 2: np.uint32, 3: np.bool_}
+_DTYPE_ELEM = {np.dtype(np.float32): 0, np.dtype(np.uint16): 1, np.dtype(np.uint32): 2, np.dtype(np.bool_): 3}
+
+
+@dataclass
+class Volume:
+    """An NDIV volume: values (numpy, the file's element type) + spacing."""
+    values: np.ndarray
+    spacing: Optional[tuple] = None
+
+
+def read_volume(path) -> Volume:
+    """io::read_volume (reference src/io.cpp:83-158)."""
+    info = _VolumeInfo()
+    p = os.fsencode(path)
+    _check(lib().vk_volume_info_read(p, ctypes.byref(info)))
+    shape = tuple(int(info.shape[i]) for i in range(info.rank))
+    out = np.empty(shape, _ELEM_DTYPE[info.elem])
+    _check(lib().vk_volume_read(p, ctypes.byref(info), out.ctypes.data, out.nbytes))
+    sp = tuple(float(info.spacing[i]) for i in range(info.rank)) if info.has_spacing else None
+    return Volume(out, sp)
+
+
+def _info_for(values: np.ndarray, spacing) -> _VolumeInfo:
+    info = _VolumeInfo()
+    if values.dtype not in _DTYPE_ELEM:
+        raise Error(f"unsupported element type {values.dtype}")
+    info.elem = _DTYPE_ELEM[values.dtype]
+    info.rank = values.ndim
+    if values.ndim > 4:
+        raise HeaderMismatch(f"HeaderMismatch: unsupported rank {values.ndim}")
+    for i, e in enumerate(values.shape):
+        info.shape[i] = int(e)
+    if spacing is not None:
+        if len(spacing) != values.ndim:
+            raise ShapeMismatch("ShapeMismatch: spacing needs one entry per axis")
+        info.has_spacing = 1
+        for i, v in enumerate(spacing):
+            info.spacing[i] = float(v)
+    return info
+
+
+def write_volume(path, values, spacing=None) -> None:
+    """io::write_volume (reference src/io.cpp:53-81); bytewise identical files."""
+    a = np.ascontiguousarray(values)
+    info = _info_for(a, spacing)
+    _check(lib().vk_volume_write(os.fsencode(path), ctypes.byref(info), a.ctypes.data))
+
+
+@dataclass
+class VolumeInfo:
+    shape: tuple
+    dtype: type
+    spacing: Optional[tuple] = None
+
+
+def _py_info(info: _VolumeInfo) -> VolumeInfo:
+    return VolumeInfo(tuple(int(info.shape[i]) for i in range(info.rank)), _ELEM_DTYPE[info.elem],
+                      tuple(float(info.spacing[i]) for i in range(info.rank)) if info.has_spacing else None)
+
+
+def volume_info(path) -> VolumeInfo:
+    """Header of an NDIV file, fully validated (magic, JSON, payload length)."""
+    info = _VolumeInfo()
+    _check(lib().vk_volume_info_read(os.fsencode(path), ctypes.byref(info)))
+    return _py_info(info)
+
+
+def read_volume_device(path, dst_ptr: int, dst_bytes: int, stream: int = 0) -> VolumeInfo:
+    """Stream the payload straight into device memory (pinned double
+    buffering: the file read of one chunk overlaps the H2D of the other)."""
+    info = _VolumeInfo()
+    _check(lib().vk_volume_read_device(os.fsencode(path), ctypes.byref(info), dst_ptr, dst_bytes, stream))
+    return _py_info(info)
+
+
+def write_volume_device(path, src_ptr: int, shape, dtype=np.float32, spacing=None, stream: int = 0) -> None:
+    """write_volume from device memory (D2H chunks overlap the file writes)."""
+    info = _info_for(np.empty((0,) * len(tuple(shape)), dtype), spacing)
+    for i, e in enumerate(shape):
+        info.shape[i] = int(e)
+    _check(lib().vk_volume_write_device(os.fsencode(path), ctypes.byref(info), src_ptr, stream))
+
+
+@dataclass
+class SynthSpec:
+    """synth::SynthSpec (reference include/voxelkit/synth.hpp:27-39)."""
+    shape: tuple = (32, 128, 128)
+    n_objects: int = 20
+    radius_min: float = 6.0
+    radius_max: float = 10.0
+    seed: int = 0
+    noise_sigma: float = 0.05
+    anisotropy: float = 1.0
+    inplane_margin: float = 0.0
+
+    def _c(self) -> _SynthSpec:
+        if len(self.shape) != 3:
+            raise Error("generate_blobs expects a 3D ZYX shape")
+        return _SynthSpec((ctypes.c_uint64 * 3)(*[int(v) for v in self.shape]), int(self.n_objects),
+                          float(self.radius_min), float(self.radius_max), int(self.seed),
+                          float(self.noise_sigma), float(self.anisotropy), float(self.inplane_margin))
+
+
+def generate_blobs_device(spec: SynthSpec, out_ptr: int, device: int = 0, stream: int = 0) -> tuple:
+    """generate_blobs(spec).intensity into a device buffer; returns the spacing."""
+    sp = (ctypes.c_double * 3)()
+    c = spec._c()
+    _check(lib().vk_generate_blobs(device, ctypes.byref(c), out_ptr, sp, stream))
+    return tuple(sp)
+
+
+def gaussian_psf(shape, sigmas) -> np.ndarray:
+    """synth::gaussian_psf (reference src/synth.cpp:226-258)."""
+    shape = tuple(int(s) for s in shape)
+    sig = np.ascontiguousarray(np.atleast_1d(np.asarray(sigmas, np.float64)))
+    out = np.empty(shape, np.float32)
+    _check(lib().vk_gaussian_psf(len(shape), _shape(shape), sig.ctypes.data_as(_dp), sig.size,
+                                 out.ctypes.data_as(_fp)))
+    return out
+
+
 def exported_symbols() -> List[str]:
     """Function names declared in include/vk_rl.h (for the ABI tests)."""
     import re
-    with open(HEADER_PATH) as f:
-        txt = f.read()
+    txt = ""
+    for h in HEADER_PATHS:
+        with open(h) as f:
+            txt += f.read()
     return sorted(set(re.findall(r"^\s*(?:vk_status|uint64_t|const char\*|int)\s+(vk_\w+)\s*\(", txt, re.M)))
 
 
@@ -459,5 +628,7 @@ __all__ = [
     "Error", "ShapeMismatch", "NegativeInput", "UnnormalizedPsf", "DegenerateReference", "TooSmall",
     "OddExtent", "CudaError", "Unsupported", "KernelTooLarge", "ConvPlan", "fft_convolve", "StopMetric", "StoppingRule", "IterationRecord",
     "IterationTrace", "RlResult", "RlTransforms", "RlPlan", "richardson_lucy", "rl_step", "good_size",
-    "to_string", "lib", "exported_symbols",
+    "to_string", "lib", "exported_symbols", "Volume", "VolumeInfo", "volume_info", "read_volume", "write_volume", "read_volume_device",
+    "write_volume_device", "SynthSpec", "generate_blobs_device", "gaussian_psf", "BadMagic", "HeaderMismatch",
+    "TruncatedPayload", "PlacementFailure", "EvenExtent",
 ]

@@ -35,19 +35,39 @@ def _nvcc() -> str:
     raise RuntimeError("nvcc not found")
 
 
+CLI_SRC = os.path.join(PKG, "host", "vk_cli.cu")
+CLI = os.path.join(LIBDIR, "voxelkit_b200")
+
+
 def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith(".cu"))
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
 
 
 def deps():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)) + [os.path.join(ROOT, "include", "vk_rl.h")]
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)) + [
+        os.path.join(ROOT, "include", h) for h in ("vk_rl.h", "vk_io.h")]
 
 
 def up_to_date() -> bool:
-    if not os.path.exists(LIB):
+    if not (os.path.exists(LIB) and os.path.exists(CLI)):
         return False
-    t = os.path.getmtime(LIB)
-    return all(os.path.getmtime(d) <= t for d in deps())
+    t = min(os.path.getmtime(LIB), os.path.getmtime(CLI))
+    return all(os.path.getmtime(d) <= t for d in deps() + [CLI_SRC])
+
+
+def build_cli(verbose: bool = False) -> str:
+    """voxelkit_b200 (the CLI `deconvolve` on the B200 path), linked against
+    lib/libvkrl.so with an $ORIGIN rpath."""
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-std=c++17",
+           "-I" + os.path.join(ROOT, "include"), "-o", CLI + ".tmp", CLI_SRC,
+           "-L" + LIBDIR, "-lvkrl", "-Xlinker", "-rpath,$ORIGIN"]
+    if verbose:
+        print(" ".join(cmd))
+    r = subprocess.run(cmd, capture_output=True, text=True)
+    if r.returncode != 0:
+        raise RuntimeError(f"nvcc (cli) failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+    os.replace(CLI + ".tmp", CLI)
+    return CLI
 
 
 def build(force: bool = False, verbose: bool = False) -> str:
@@ -64,6 +84,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if verbose and r.stderr:
         print(r.stderr)
     os.replace(tmp, LIB)
+    build_cli(verbose)
     return LIB
 
 

@@ -63,6 +63,15 @@ vk_status guarded(F&& f) {
   }
 }
 
+}  // namespace
+
+// Shared with the other C-ABI translation units (vk_io.cpp, vk_synth.cu).
+namespace vk {
+void set_last_error(const std::string& msg) { g_last_error = msg; }
+}  // namespace vk
+
+namespace {
+
 uint64_t good_size(uint64_t n) {
   if (n <= 1) return 1;
   for (uint64_t c = n;; ++c) {

@@ -162,9 +162,65 @@ def gaussian_fixtures():
     print("gaussian_ssim", [v.shape for k, v in out.items() if k.startswith("in")])
 
 
+def io_fixtures():
+    """NDIV files written by the reference's io::write_volume, synth goldens
+    (generate_blobs, gaussian_psf) and the CLI `deconvolve` pipeline run
+    through the reference library (generate_blobs -> fft_convolve -> vmax 0
+    -> richardson_lucy), for SURVEY.md §8(f) row f2."""
+    d = os.path.join(OUT, "ndiv")
+    os.makedirs(d, exist_ok=True)
+    rng = np.random.default_rng(77)
+    vols = {
+        "f32_zyx_spacing": (np.arange(8, dtype=np.float32).reshape(2, 2, 2), [0.29, 0.065, 0.065]),
+        "f32_yx": (rng.standard_normal((5, 7)).astype(np.float32), None),
+        "f32_czyx": (rng.random((3, 2, 4, 5)).astype(np.float32), [1.0, 2.5, 0.1, 0.1]),
+        "u16_x": (np.array([0, 7, 65535], np.uint16), None),
+        "u32_yx": (np.arange(4, dtype=np.uint32).reshape(2, 2), [1e-05, 123456789.0]),
+        "bool_yx": (np.array([[1, 0], [0, 1]], np.bool_), None),
+        "f32_odd_spacing": (rng.random((2, 3, 4)).astype(np.float32), [1 / 3, 2e-07, 1e16]),
+    }
+    man = {}
+    for name, (v, sp) in vols.items():
+        ref.write_volume(os.path.join(d, name + ".ndiv"), v, sp)
+        man[name] = v
+        man[name + "__spacing"] = np.array(sp if sp is not None else [], np.float64)
+    np.savez_compressed(os.path.join(d, "manifest.npz"), **man)
+
+    # synth goldens
+    blobs = ref.generate_blobs((20, 48, 48), n_objects=6, radius_min=3.0, radius_max=4.5, seed=11,
+                               noise_sigma=0.05)
+    quiet = ref.generate_blobs((16, 40, 40), n_objects=3, radius_min=2.5, radius_max=4.0, seed=5,
+                               noise_sigma=0.0)
+    empty = ref.generate_blobs((8, 16, 16), n_objects=0, radius_min=2.0, radius_max=3.0, seed=1,
+                               noise_sigma=0.05)
+    psfs = {"psf_a": ref.gaussian_psf((9, 17, 17), [1.0, 2.0, 2.0]),
+            "psf_b": ref.gaussian_psf((5, 5), [1.5]),
+            "psf_c": ref.gaussian_psf((7,), [0.0]),
+            "psf_d": ref.gaussian_psf((3, 9, 5), [0.7, 2.2, 1.1])}
+    np.savez_compressed(os.path.join(OUT, "synth.npz"), blobs=blobs, quiet=quiet, empty=empty, **psfs)
+
+    # CLI deconvolve, synthetic mode: --shape 20 48 48 --objects 4 --radius 3 4.5
+    # --seed 7 --gaussian 1.0 1.5 1.5 --metric si_psnr --max-iters 6 (rel_tol 1e-3, patience 3)
+    truth = ref.generate_blobs((20, 48, 48), n_objects=4, radius_min=3.0, radius_max=4.5, seed=7,
+                               noise_sigma=0.05)
+    ks = [2 * int(np.ceil(4.0 * s)) + 1 for s in (1.0, 1.5, 1.5)]
+    psf = ref.gaussian_psf(ks, [1.0, 1.5, 1.5])
+    observed = np.maximum(ref.fft_convolve(truth, psf), 0).astype(np.float32)
+    r = ref.richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, patience=3,
+                            max_iters=6)
+    np.savez_compressed(os.path.join(OUT, "cli_synthetic.npz"), truth=truth, psf=psf, observed=observed,
+                        estimate=r.estimate, metric=r.metric, iters_run=r.iters_run,
+                        stop_reason=r.stop_reason, fft_shape=np.array(r.fft_shape),
+                        si_blurred=ref.si_psnr(observed, truth), si_estimate=ref.si_psnr(r.estimate, truth))
+    print("io fixtures", sorted(vols), blobs.shape, r.iters_run, r.stop_reason)
+
+
 if __name__ == "__main__":
     if sys.argv[1:] == ["gaussian"]:
         gaussian_fixtures()
+    elif sys.argv[1:] == ["io"]:
+        io_fixtures()
     else:
         main()
         gaussian_fixtures()
+        io_fixtures()
