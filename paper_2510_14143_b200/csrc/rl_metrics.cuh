@@ -68,6 +68,48 @@ __global__ void frc_bins_kernel(const float2* __restrict__ A, const float2* __re
     if (hist[i] != 0.0) atomicAdd(&bins[i], hist[i]);
 }
 
+// Direct DFT along one axis, for FRC half extents that are not 5-smooth (the
+// reference's FFTW plans any length; the line FFTs here are radix 2/3/5).
+// Logical output coordinates (c0, c1, c2) over extents (e0, e1, e2); axis
+// `ax` sums n input samples with the exact twiddle tw[(j k) mod n] =
+// exp(-2 pi i (j k mod n) / n).  Strides in elements; REAL_IN reads floats.
+// Cost n per output: a fallback, used only where the FFT path cannot run.
+template <bool REAL_IN>
+__global__ void dft_axis_kernel(const void* __restrict__ in, float2* __restrict__ out, int e0, int e1, int e2,
+                                int ax, int n, long long is0, long long is1, long long is2, long long os0,
+                                long long os1, long long os2, const float2* __restrict__ tw) {
+  const size_t total = (size_t)e0 * e1 * e2;
+  const long long isa = ax == 0 ? is0 : ax == 1 ? is1 : is2;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < total; i += (size_t)gridDim.x * blockDim.x) {
+    int c[3];
+    c[2] = (int)(i % e2);
+    const size_t t = i / e2;
+    c[1] = (int)(t % e1);
+    c[0] = (int)(t / e1);
+    const int k = c[ax];
+    c[ax] = 0;
+    const long long base = c[0] * is0 + c[1] * is1 + c[2] * is2;
+    c[ax] = k;
+    float re = 0.f, im = 0.f;
+    int m = 0;
+    for (int j = 0; j < n; ++j) {
+      const float2 w = tw[m];
+      if (REAL_IN) {
+        const float v = static_cast<const float*>(in)[base + j * isa];
+        re = fmaf(v, w.x, re);
+        im = fmaf(v, w.y, im);
+      } else {
+        const float2 v = static_cast<const float2*>(in)[base + j * isa];
+        re = fmaf(v.x, w.x, fmaf(-v.y, w.y, re));
+        im = fmaf(v.x, w.y, fmaf(v.y, w.x, im));
+      }
+      m += k;
+      if (m >= n) m -= n;
+    }
+    out[c[0] * os0 + c[1] * os1 + c[2] * os2] = make_float2(re, im);
+  }
+}
+
 // ---------------------------------------------------------------------------
 // ssim_vs_prev: metrics::ssim(current, previous) (src/metrics.cpp:103-144)
 // with filters::gaussian(sigma 1.5, truncate 3.5) (src/filters.cpp:78-140).

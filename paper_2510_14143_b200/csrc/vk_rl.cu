@@ -212,6 +212,9 @@ struct vk_rl_plan_s {
   int frc_nbins = 0;
   double frc_binf = 0;
   int frc_h[3]{1, 1, 1}, frc_s[3]{0, 0, 0};
+  // non-5-smooth half extents: direct per-axis DFTs instead of the sub-plan
+  bool frc_dft = false;
+  DevBuf<float2> frc_tw[3], frc_t1, frc_A, frc_B;
   // ssim_vs_prev stopping metric (rl_metrics.cuh): current / previous crops
   // (ping-pong), two sets of five double moment fields, per-iteration crop
   // ranges ([iters+1][2] f32 bits, row 0 = observed) and SSIM-map sums
@@ -836,18 +839,18 @@ double si_psnr_from_sums(const RefStats& r, double sx, double sxx, double sxr) {
 // (metrics.cpp:241-264): even_view trims odd extents, the half extents must be
 // 5-smooth for the device r2c (no Bluestein yet).
 void setup_frc(vk_rl_plan p) {
-  if (p->frc) return;
+  if (p->frc || p->frc_dft) return;
   uint64_t half[3] = {1, 1, 1}, ones[3] = {1, 1, 1};
+  bool smooth = true;
   for (int a = 0; a < p->rank; ++a) {
     const uint64_t e = p->ishape[a] - p->ishape[a] % 2;  // even_view (deconv.cpp:255-276)
     if (e == 0) fail(VK_ERR_UNSUPPORTED, "frc_resolution needs every image extent >= 2");
     half[a] = e / 2;
-    if (good_size(half[a]) != half[a])
-      fail(VK_ERR_UNSUPPORTED, "frc_resolution on the B200 path needs 5-smooth half extents (got " +
-                                   std::to_string(half[a]) + ")");
+    smooth = smooth && good_size(half[a]) == half[a];
   }
   const float one = 1.0f;
-  p->frc = create_plan(p->device, p->rank, half, p->rank, ones, &one, 0);
+  if (smooth) p->frc = create_plan(p->device, p->rank, half, p->rank, ones, &one, 0);
+  p->frc_dft = !smooth;
   uint64_t nmax = 0;
   for (int a = 0; a < p->rank; ++a) nmax = std::max(nmax, half[a]);
   p->frc_binf = 1.0 / (double)nmax;  // ring_width / n_max (metrics.cpp:166-169)
@@ -860,6 +863,22 @@ void setup_frc(vk_rl_plan p) {
   const size_t hn = (size_t)p->frc_h[0] * p->frc_h[1] * p->frc_h[2];
   p->frc_even.alloc(hn, "frc even");
   p->frc_odd.alloc(hn, "frc odd");
+  if (p->frc_dft) {
+    const size_t cn = (size_t)p->frc_h[0] * p->frc_h[1] * (p->frc_h[2] / 2 + 1);
+    p->frc_t1.alloc(2 * cn, "frc dft scratch");
+    p->frc_A.alloc(cn, "frc spectrum A");
+    p->frc_B.alloc(cn, "frc spectrum B");
+    for (int a = 0; a < 3; ++a) {  // exp(-2 pi i m / n), m < n, from the exact angle
+      const int n = p->frc_h[a];
+      std::vector<float2> tw(n);
+      for (int m = 0; m < n; ++m) {
+        const double ang = -2.0 * M_PI * (double)m / (double)n;
+        tw[m] = make_float2((float)std::cos(ang), (float)std::sin(ang));
+      }
+      p->frc_tw[a].alloc(n, "frc twiddles");
+      ck(cudaMemcpy(p->frc_tw[a].p, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice), "frc twiddles");
+    }
+  }
   p->frc_bins.alloc((size_t)3 * p->frc_nbins, "frc bins");
   ck(cudaMallocHost(&p->h_frc, (size_t)3 * p->frc_nbins * sizeof(double)), "frc pinned");
 }
@@ -874,12 +893,35 @@ double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
                                                      p->frc_s[0], p->frc_s[1], p->frc_s[2], p->frc_even.p,
                                                      p->frc_odd.p);
   launch_check(p, "frc split");
-  const vk::Geom& fg = f->g;
-  spectrum3d(f, s, p->frc_even.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf.p);
-  spectrum3d(f, s, p->frc_odd.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf_flip.p);
-  vk::frc_bins_kernel<<<148 * 2, kThreads, (size_t)3 * nb * sizeof(double), s>>>(
-      f->otf.p, f->otf_flip.p, fg.Wz, fg.Wy, fg.Wx, fg.Hx, p->frc_binf, nb, p->frc_bins.p);
-  launch_check(p, "frc bins");
+  if (p->frc_dft) {
+    // r2c along x, then y, then z (written in the [Hx][hz][hy] bins layout)
+    const int hz = p->frc_h[0], hy = p->frc_h[1], hx = p->frc_h[2], Hx = hx / 2 + 1;
+    const long long cy = Hx, cz = (long long)hy * Hx;
+    float2* t1 = p->frc_t1.p;
+    float2* t2 = p->frc_t1.p + (size_t)hz * hy * Hx;
+    const int grid = 148 * 8;
+    for (int img = 0; img < 2; ++img) {
+      const float* src = img ? p->frc_odd.p : p->frc_even.p;
+      float2* dst = img ? p->frc_B.p : p->frc_A.p;
+      vk::dft_axis_kernel<true><<<grid, kThreads, 0, s>>>(src, t1, hz, hy, Hx, 2, hx, (long long)hy * hx, hx, 1,
+                                                          cz, cy, 1, p->frc_tw[2].p);
+      vk::dft_axis_kernel<false><<<grid, kThreads, 0, s>>>(t1, t2, hz, hy, Hx, 1, hy, cz, cy, 1, cz, cy, 1,
+                                                           p->frc_tw[1].p);
+      vk::dft_axis_kernel<false><<<grid, kThreads, 0, s>>>(t2, dst, hz, hy, Hx, 0, hz, cz, cy, 1, hy, 1,
+                                                           (long long)hz * hy, p->frc_tw[0].p);
+      launch_check(p, "frc dft");
+    }
+    vk::frc_bins_kernel<<<148 * 2, kThreads, (size_t)3 * nb * sizeof(double), s>>>(
+        p->frc_A.p, p->frc_B.p, hz, hy, hx, Hx, p->frc_binf, nb, p->frc_bins.p);
+    launch_check(p, "frc bins");
+  } else {
+    const vk::Geom& fg = f->g;
+    spectrum3d(f, s, p->frc_even.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf.p);
+    spectrum3d(f, s, p->frc_odd.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf_flip.p);
+    vk::frc_bins_kernel<<<148 * 2, kThreads, (size_t)3 * nb * sizeof(double), s>>>(
+        f->otf.p, f->otf_flip.p, fg.Wz, fg.Wy, fg.Wx, fg.Hx, p->frc_binf, nb, p->frc_bins.p);
+    launch_check(p, "frc bins");
+  }
   ck(cudaMemcpyAsync(p->h_frc, p->frc_bins.p, (size_t)3 * nb * sizeof(double), cudaMemcpyDeviceToHost, s),
      "frc D2H");
   ck(cudaStreamSynchronize(s), "frc");

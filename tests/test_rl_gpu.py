@@ -267,6 +267,27 @@ def test_frc_default_rule_c1():
     np.testing.assert_allclose([x.value for x in r2.trace.records], np.asarray(v1) * 0.5, rtol=1e-12)
 
 
+FRC_ODD_CASES = [((12, 30, 34), (5, 7, 7)), ((50, 70), (9, 9)), ((46,), (7,)), ((15, 43, 29), (3, 5, 5))]
+
+
+@pytest.mark.parametrize("shape,kshape", FRC_ODD_CASES, ids=lambda v: "x".join(map(str, v)))
+def test_frc_non_smooth_half_extents(shape, kshape):
+    """FRC on images whose even_view half extents are not 5-smooth (17, 35,
+    23, 21 ...): the direct-DFT spectra path, fixed iteration count."""
+    rng = np.random.default_rng(sum(shape))
+    k = rng.random(kshape) + 0.2
+    psf = (k / k.sum()).astype(np.float32)
+    obs = np.maximum(O.fft_convolve((rng.random(shape) * 3).astype(np.float32), psf), 0).astype(np.float32)
+    e, t = O.richardson_lucy(obs, psf, "frc_resolution", 1e-300, 4, 4)
+    r = vk.richardson_lucy(obs, psf, fixed_rule(4, "frc_resolution"))
+    ours = np.asarray([x.value for x in r.trace.records])
+    ref_vals = np.asarray(t.metric)
+    assert np.array_equal(np.isinf(ours), np.isinf(ref_vals))
+    fin = ~np.isinf(ref_vals)
+    np.testing.assert_allclose(ours[fin], ref_vals[fin], rtol=TOL_METRIC)
+    assert rel_l2(r.estimate, e) <= TOL_N
+
+
 def test_c2_full_size_first_iterations():
     """C2 at full size (128x512x512, 31^3 widefield): the benchmark's own grid
     (192 x 576 x 576) through the fast kernels, 2 iterations vs the oracle."""
