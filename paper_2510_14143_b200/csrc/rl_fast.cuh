@@ -124,9 +124,15 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
     const bool last = a.mode == XM_UPDATE_LAST;
     const bool ratio = a.mode == XM_RATIO;
     double acc0 = 0.0, acc1 = 0.0, acc2 = 0.0;
-    // work item = (line l, chunk of CH samples); one warp per item, U samples
-    // of both rows of the line per lane
-    const int nch = (g.Px + CH - 1) / CH;
+    // Work items (line l, chunk c), one warp each.  Chunks c < nci cover the
+    // interior columns [ox, ox+Ix) in CH-sample pieces aligned at ox (U
+    // samples of both rows of the line per lane, no x clamp); the remaining
+    // chunks cover the 2*ox pad columns, one sample per lane, whose observed
+    // value is the replicated edge (deconv.cpp:221-237) and which never enter
+    // the sums.
+    const int nci = (g.Ix + CH - 1) / CH;
+    const int npad = g.Px - g.Ix;
+    const int nch = nci + (npad + 31) / 32;
     // items (l, ch) walked with incremental carries instead of div/mod
     int l = 0, ch = warp;
     while (ch >= nch) {
@@ -142,24 +148,47 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
         ++l;
       }
       if (l >= L) break;
-      const int x0 = ch * CH;
       const int ya = y0 + l, yb = y0 + L + l;
       const bool va = ya < g.Py, vb = yb < g.Py;
       const int iya = ya - g.oy, iyb = yb - g.oy;
       const bool ina = va && zin && iya >= 0 && iya < g.Iy, inb = vb && zin && iyb >= 0 && iyb < g.Iy;
       const size_t oa_off = (zoff + clampi(iya, 0, g.Iy - 1)) * g.Ix;
       const size_t ob_off = (zoff + clampi(iyb, 0, g.Iy - 1)) * g.Ix;
-      const float* oa = a.obs + oa_off;
-      const float* ob = a.obs + ob_off;
       float* ea = a.est + ((size_t)z * g.Py + (va ? ya : 0)) * g.Px;
       float* eb = a.est + ((size_t)z * g.Py + (vb ? yb : 0)) * g.Px;
-      if (ina && inb && x0 >= g.ox && x0 + CH <= g.ox + g.Ix) {
-        // interior chunk (the common case): no clamps, no predicates
-        const float* oa2 = oa + (x0 - g.ox) + lane;
-        const float* ob2 = ob + (x0 - g.ox) + lane;
-        float* ea2 = ea + x0 + lane;
-        float* eb2 = eb + x0 + lane;
-        const int s0 = sw<L>(x0 + lane + g.cx, l);
+      if (ch >= nci) {
+        // pad columns: x in [0, ox) and [ox+Ix, Px)
+        const int p = (ch - nci) * 32 + lane;
+        if (p < npad) {
+          const bool left = p < g.ox;
+          const int x = left ? p : p + g.Ix;
+          const int xo = left ? 0 : g.Ix - 1;
+          const int sidx = sw<L>(x + g.cx, l);
+          const float2 m = A[sidx];
+          float2 val;
+          if (ratio) {
+            val = make_float2(va ? __fdividef(__ldg(a.obs + oa_off + xo), fmaxf(m.x, kEps)) : 0.f,
+                              vb ? __fdividef(__ldg(a.obs + ob_off + xo), fmaxf(m.y, kEps)) : 0.f);
+          } else {
+            val = make_float2(va ? fmaxf(ea[x] * m.x, 0.f) : 0.f, vb ? fmaxf(eb[x] * m.y, 0.f) : 0.f);
+            if (!last) {
+              if (va) ea[x] = val.x;
+              if (vb) eb[x] = val.y;
+            }
+          }
+          A[sidx] = val;
+        }
+        continue;
+      }
+      const int c0 = ch * CH;  // interior column of this chunk's first sample
+      const int x0 = g.ox + c0;
+      const int s0 = sw<L>(x0 + lane + g.cx, l);
+      const float* oa2 = a.obs + oa_off + c0 + lane;
+      const float* ob2 = a.obs + ob_off + c0 + lane;
+      float* ea2 = ea + x0 + lane;
+      float* eb2 = eb + x0 + lane;
+      if (va && vb && c0 + CH <= g.Ix) {
+        // full chunk of two existing rows (the common case): no predicates
         float2 m[U];
         float o_a[U], o_b[U], e_a[U], e_b[U];
 #pragma unroll
@@ -172,86 +201,82 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
             e_b[u] = eb2[u * 32];
           }
         }
-        float f0 = 0.f, f1 = 0.f, f2 = 0.f;
+        float fa0 = 0.f, fa1 = 0.f, fa2 = 0.f, fb0 = 0.f, fb1 = 0.f, fb2 = 0.f;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           float2 val;
           if (ratio) {
+            // fast reciprocal/log (<= 2 ulp / 2^-21 abs): the f32 path's own
+            // rounding (~1e-7 rel) dominates either way
             const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
             val = make_float2(__fdividef(o_a[u], ma), __fdividef(o_b[u], mb));
-            f0 += fmaf(o_a[u], __logf(ma), -ma) + fmaf(o_b[u], __logf(mb), -mb);
+            fa0 += fmaf(o_a[u], __logf(ma), -ma);
+            fb0 += fmaf(o_b[u], __logf(mb), -mb);
           } else {
             val = make_float2(fmaxf(e_a[u] * m[u].x, 0.f), fmaxf(e_b[u] * m[u].y, 0.f));
             if (!last) {
               ea2[u * 32] = val.x;
               eb2[u * 32] = val.y;
             } else {
-              a.out[oa_off + (x0 - g.ox) + lane + u * 32] = val.x;
-              a.out[ob_off + (x0 - g.ox) + lane + u * 32] = val.y;
+              if (ina) a.out[oa_off + c0 + lane + u * 32] = val.x;
+              if (inb) a.out[ob_off + c0 + lane + u * 32] = val.y;
             }
-            f0 += val.x + val.y;
-            f1 = fmaf(val.x, val.x, fmaf(val.y, val.y, f1));
-            f2 = fmaf(val.x, o_a[u], fmaf(val.y, o_b[u], f2));
+            fa0 += val.x;
+            fa1 = fmaf(val.x, val.x, fa1);
+            fa2 = fmaf(val.x, o_a[u], fa2);
+            fb0 += val.y;
+            fb1 = fmaf(val.y, val.y, fb1);
+            fb2 = fmaf(val.y, o_b[u], fb2);
           }
           A[s0 + u * 32 * (L + 1)] = val;
         }
-        acc0 += f0;
-        acc1 += f1;
-        acc2 += f2;
+        if (ina) {
+          acc0 += fa0;
+          acc1 += fa1;
+          acc2 += fa2;
+        }
+        if (inb) {
+          acc0 += fb0;
+          acc1 += fb1;
+          acc2 += fb2;
+        }
         continue;
       }
-      float2 m[U];
-      float o_a[U], o_b[U], e_a[U], e_b[U];
+      // partial chunk (last interior piece or a missing second row)
 #pragma unroll
       for (int u = 0; u < U; ++u) {
-        const int x = x0 + u * 32 + lane;
-        const bool ok = x < g.Px;
-        const int xo = clampi(x - g.ox, 0, g.Ix - 1);
-        m[u] = ok ? A[sw<L>(x + g.cx, l)] : make_float2(0.f, 0.f);
-        o_a[u] = (ok && va) ? __ldg(&oa[xo]) : 0.f;
-        o_b[u] = (ok && vb) ? __ldg(&ob[xo]) : 0.f;
-        e_a[u] = (!ratio && ok && va) ? ea[x] : 0.f;
-        e_b[u] = (!ratio && ok && vb) ? eb[x] : 0.f;
-      }
-      float f0 = 0.f, f1 = 0.f, f2 = 0.f;
-#pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int x = x0 + u * 32 + lane;
-        if (x >= g.Px) break;
-        const int ix = x - g.ox;
-        const bool xin = ix >= 0 && ix < g.Ix;
+        const int c = c0 + u * 32 + lane;
+        if (c >= g.Ix) break;
+        const int sidx = s0 + u * 32 * (L + 1);
+        const float2 m = A[sidx];
+        const float o_a = __ldg(oa2 + u * 32), o_b = __ldg(ob2 + u * 32);
         float2 val;
         if (ratio) {
-          // fast reciprocal/log (<= 2 ulp / 2^-21 abs): the f32 path's own
-          // rounding (~1e-7 rel) dominates either way
-          const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
-          val = make_float2(va ? __fdividef(o_a[u], ma) : 0.f, vb ? __fdividef(o_b[u], mb) : 0.f);
-          if (xin && ina) f0 += fmaf(o_a[u], __logf(ma), -ma);
-          if (xin && inb) f0 += fmaf(o_b[u], __logf(mb), -mb);
+          const float ma = fmaxf(m.x, kEps), mb = fmaxf(m.y, kEps);
+          val = make_float2(va ? __fdividef(o_a, ma) : 0.f, vb ? __fdividef(o_b, mb) : 0.f);
+          if (ina) acc0 += fmaf(o_a, __logf(ma), -ma);
+          if (inb) acc0 += fmaf(o_b, __logf(mb), -mb);
         } else {
-          val = make_float2(va ? fmaxf(e_a[u] * m[u].x, 0.f) : 0.f, vb ? fmaxf(e_b[u] * m[u].y, 0.f) : 0.f);
+          val = make_float2(va ? fmaxf(ea2[u * 32] * m.x, 0.f) : 0.f, vb ? fmaxf(eb2[u * 32] * m.y, 0.f) : 0.f);
           if (!last) {
-            if (va) ea[x] = val.x;
-            if (vb) eb[x] = val.y;
+            if (va) ea2[u * 32] = val.x;
+            if (vb) eb2[u * 32] = val.y;
           }
-          if (xin && ina) {
-            f0 += val.x;
-            f1 = fmaf(val.x, val.x, f1);
-            f2 = fmaf(val.x, o_a[u], f2);
-            if (last) a.out[oa_off + ix] = val.x;
+          if (ina) {
+            acc0 += val.x;
+            acc1 += (double)val.x * val.x;
+            acc2 += (double)val.x * o_a;
+            if (last) a.out[oa_off + c] = val.x;
           }
-          if (xin && inb) {
-            f0 += val.y;
-            f1 = fmaf(val.y, val.y, f1);
-            f2 = fmaf(val.y, o_b[u], f2);
-            if (last) a.out[ob_off + ix] = val.y;
+          if (inb) {
+            acc0 += val.y;
+            acc1 += (double)val.y * val.y;
+            acc2 += (double)val.y * o_b;
+            if (last) a.out[ob_off + c] = val.y;
           }
         }
-        A[sw<L>(x + g.cx, l)] = val;
+        A[sidx] = val;
       }
-      acc0 += f0;
-      acc1 += f1;
-      acc2 += f2;
     }
     if (ratio) {
       double v1[1] = {acc0};
