@@ -8,7 +8,9 @@
 namespace vk {
 
 struct FastEntry {
-  int N;
+  int N, R1;            // N = R1 * R2 (pass-1 / pass-2 radices)
+  size_t smem_xp;       // x-pass
+  size_t smem_yp;       // y-pass FWD/INV
   int Lx, NTx;          // x-pass and y-pass: lines per CTA, threads
   size_t smem_x;        // x-pass, and y-pass FWD/INV
   size_t smem_yconv;    // y-pass CONV (adds the prefetched OTF tile)

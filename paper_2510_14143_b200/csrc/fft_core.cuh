@@ -35,6 +35,7 @@ struct LinePlan {
   int rad[kMaxStages];
   int ns[kMaxStages];
   const float2* tw;
+  const float2* tw2;  // fast path: pass-2 twiddles, butterfly-major (reg::load_twiddles2 layout), global
 };
 
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }

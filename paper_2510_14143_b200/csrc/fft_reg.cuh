@@ -186,7 +186,9 @@ __device__ __forceinline__ int sw(int i, int l) {
 // must cover every pass-1 butterfly with one thread (NT >= L*R2) so pass 1 can
 // stage its inputs in registers, sync, and overwrite in place; pass 2 reads
 // and writes the same index set per thread.  Caller syncs before.
-template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1>
+// TWG: `tw` is the butterfly-major table in global memory (read through L1)
+// instead of shared memory.
+template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1, bool TWG = false>
 __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
   static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
 #ifdef VK_DEBUG_NOFFT  // experiment builds only: isolate the memory cost of a pass
@@ -213,7 +215,7 @@ __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
     v[0] = buf[j * LP + l];
     static_for<1, R2>([&](auto r) {
       constexpr int rr = decltype(r)::value;
-      const float2 w = tw[j * R2 + rr];  // load_twiddles2 layout
+      const float2 w = TWG ? __ldg(tw + j * R2 + rr) : tw[j * R2 + rr];  // load_twiddles2 layout
       const float2 x = buf[(j + rr * R1) * LP + l];
       v[rr] = INV ? cmulc(x, w) : cmul(x, w);
     });

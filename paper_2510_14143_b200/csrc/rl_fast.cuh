@@ -40,9 +40,12 @@ struct FastCfg {
   static constexpr int NT = ((L * (R1 > R2 ? R1 : R2)) + 31) / 32 * 32;
   static constexpr int DATA = N * (L + 1);  // padded line block, see reg::sw
   static constexpr size_t smem = (size_t)(DATA + N + (OTF_PREFETCH ? N * L : 0)) * sizeof(float2);
+  static constexpr size_t smem_x = (size_t)DATA * sizeof(float2);  // x pass: twiddles from global
 };
 
-template <int R1, int R2, int L>
+// TWG: pass-2 twiddles read from global memory (L1) instead of a shared
+// table, when dropping the table buys one more resident CTA per SM.
+template <int R1, int R2, int L, bool TWG>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
     xpass_fast(const XArgs a) {
   using C = FastCfg<R1, R2, L>;
@@ -52,9 +55,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   constexpr int U = 4;
   constexpr int CH = 32 * U;  // samples per work item
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* A = smem + N;
-  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  const float2* tw = TWG ? a.plan.tw2 : smem;
+  float2* A = TWG ? smem : smem + N;
+  if (!TWG) reg::load_twiddles2<R1, R2>(smem, a.plan.tw);
   const int z = blockIdx.y;
   const int y0 = blockIdx.x * 2 * L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -119,7 +122,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
       }
     }
     __syncthreads();
-    reg::fft2<R1, R2, L, NT, true>(A, tw);
+    reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, tw);
 
     const bool last = a.mode == XM_UPDATE_LAST;
     const bool ratio = a.mode == XM_RATIO;
@@ -294,7 +297,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
     }
   }
   __syncthreads();
-  reg::fft2<R1, R2, L, NT, false>(A, tw);
+  reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, tw);
   {
     constexpr int KS = NT / L;
     const int l = threadIdx.x & (L - 1);
@@ -313,14 +316,14 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   }
 }
 
-template <int R1, int R2, int L>
+template <int R1, int R2, int L, bool TWG>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     ypass_fast(const YArgs a) {
   using C = FastCfg<R1, R2, L, true>;
   constexpr int N = C::N, NT = C::NT;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* A = smem + N;
+  float2* tw = TWG ? nullptr : smem;  // TWG: pass-2 twiddles from global (a.plan.tw2)
+  float2* A = TWG ? smem : smem + N;
   float2* O = A + C::DATA;  // OTF tile [l][k] (CONV only)
   const int line0 = blockIdx.x * L;
   // async copies: the L input rows (zero padding written directly)
@@ -345,16 +348,17 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     }
     cp_async_commit();
   }
-  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  const float2* twp = TWG ? a.plan.tw2 : tw;
   if (a.mode == YM_CONV)
     cp_async_wait_1();  // input rows landed, OTF may still fly
   else
     cp_async_wait_all();
   __syncthreads();
   if (a.mode == YM_INV) {
-    reg::fft2<R1, R2, L, NT, true>(A, tw);
+    reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, twp);
   } else {
-    reg::fft2<R1, R2, L, NT, false>(A, tw);
+    reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, twp);
     if (a.mode == YM_CONV) {
       cp_async_wait_all();
       __syncthreads();
@@ -363,7 +367,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
         A[sw<L>(k, l)] = cmul(A[sw<L>(k, l)], O[l * N + k]);
       }
       __syncthreads();
-      reg::fft2<R1, R2, L, NT, true>(A, tw);
+      reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, twp);
     }
   }
   for (int l = 0; l < L; ++l) {

@@ -11,16 +11,20 @@ namespace vk {
 
 namespace {
 
-template <int R1, int R2, int LX, int LZ>
+template <int R1, int R2, int LX, int LZ, bool TWG = false>
 FastEntry make_entry() {
   FastEntry e{};
   e.N = R1 * R2;
+  e.R1 = R1;
+  e.smem_xp = TWG ? FastCfg<R1, R2, LX>::smem_x : FastCfg<R1, R2, LX>::smem;
   e.Lx = LX;
   e.NTx = FastCfg<R1, R2, LX>::NT;
   e.smem_x = FastCfg<R1, R2, LX>::smem;
-  e.smem_yconv = FastCfg<R1, R2, LX, true>::smem;
-  e.xk = (const void*)xpass_fast<R1, R2, LX>;
-  e.yk = (const void*)ypass_fast<R1, R2, LX>;
+  e.smem_yp = e.smem_xp;
+  e.smem_yconv = TWG ? (size_t)(FastCfg<R1, R2, LX, true>::DATA + R1 * R2 * LX) * sizeof(float2)
+                     : FastCfg<R1, R2, LX, true>::smem;
+  e.xk = (const void*)xpass_fast<R1, R2, LX, TWG>;
+  e.yk = (const void*)ypass_fast<R1, R2, LX, TWG>;
   e.Lz = LZ;
   e.NTz = FastCfg<R1, R2, LZ, true>::NT;
   e.smem_z = FastCfg<R1, R2, LZ, true>::smem;
@@ -36,7 +40,7 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16>(),  // 192
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 8, 8>(),    // 576
+    make_entry<24, 24, 8, 8, true>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM
     make_entry<30, 36, 8, 4>(),    // 1080
     make_entry<45, 48, 4, 2>(),    // 2160
 };
@@ -97,7 +101,7 @@ cudaError_t fast_init_attributes() {
   }
   for (const auto& e : kTable) {
     cudaError_t r;
-    if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_x))) return r;
+    if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_xp))) return r;
     if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yconv))) return r;
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
     if ((r = cudaFuncSetAttribute(e.zpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zp))) return r;

@@ -186,7 +186,7 @@ struct vk_rl_plan_s {
   int psf_status = 0;  // 0 ok, VK_ERR_NEGATIVE, VK_ERR_UNNORMALIZED_PSF
   std::string psf_msg;
 
-  DevBuf<float2> twx, twy, twz;
+  DevBuf<float2> twx, twy, twz, twx2, twy2;
   LinePlan lpx{}, lpy{}, lpz{};
   // compile-time-length kernels per axis (nullptr -> generic Stockham)
   const vk::FastEntry* fx = nullptr;
@@ -334,7 +334,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
   if (p->fx)
-    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_x, s, &a);
+    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_xp, s, &a);
   else
     vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
   launch_check(p, "xpass");
@@ -360,7 +360,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
   if (p->fy)
-    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_x, s, &a);
+    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a);
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
@@ -716,6 +716,24 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       if (p->fy && p->fz && df_env && df_env[0] == '1' && !(nodf && nodf[0] == '1'))
         p->df = vk::df_lookup(g.Wy, g.Wz);
       if (conv) p->fx = nullptr;  // XM_CONV_OUT lives in the generic x kernel
+      if (p->fx) {  // butterfly-major pass-2 twiddles of the fast x pass (reg::load_twiddles2 layout)
+        const int R1 = p->fx->R1, R2 = g.Wx / R1;
+        std::vector<float2> t2((size_t)R1 * R2);
+        for (int j = 0; j < R1; ++j)
+          for (int r = 0; r < R2; ++r) t2[(size_t)j * R2 + r] = tx[(size_t)r * j];
+        p->twx2.alloc(t2.size(), "twiddles");
+        ck(cudaMemcpy(p->twx2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
+        p->lpx.tw2 = p->twx2.p;
+      }
+      if (p->fy) {  // same for the fast y pass
+        const int R1 = p->fy->R1, R2 = g.Wy / R1;
+        std::vector<float2> t2((size_t)R1 * R2);
+        for (int j = 0; j < R1; ++j)
+          for (int r = 0; r < R2; ++r) t2[(size_t)j * R2 + r] = ty[(size_t)r * j];
+        p->twy2.alloc(t2.size(), "twiddles");
+        ck(cudaMemcpy(p->twy2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
+        p->lpy.tw2 = p->twy2.p;
+      }
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
