@@ -258,11 +258,14 @@ def main():
     stream = torch.cuda.current_stream()
     sh = stream.cuda_stream
 
+    outs = [torch.empty_like(v) for v in vols] if n_batch else [out]
+    in_ptrs, out_ptrs = [v.data_ptr() for v in vols], [o.data_ptr() for o in outs]
+
     def step(trace=False):
-        tr = None
-        for v in vols:
-            tr = plan.run_device(v.data_ptr(), out.data_ptr(), rule, stream=sh, trace=trace)
-        return tr
+        if n_batch:  # independent volumes on the plan's concurrent batch lanes
+            trs = plan.run_batch_device(in_ptrs, out_ptrs, rule, stream=sh, trace=trace)
+            return trs[-1] if trs else None
+        return plan.run_device(in_ptrs[0], out_ptrs[0], rule, stream=sh, trace=trace)
 
     for _ in range(max(args.warmup, 0)):
         step()
@@ -307,7 +310,7 @@ def main():
     e2e_value = None
     if e2e_steps > 0:
         obs_h = torch.empty(shape, dtype=torch.float32, pin_memory=True)
-        obs_h.copy_(vols[-1].cpu())  # `out` holds the device result of the block's last volume
+        obs_h.copy_(vols[-1].cpu())  # `outs[-1]` holds the device result of the block's last volume
         est_h = torch.empty(shape, dtype=torch.float32, pin_memory=True)
         plan.run_ptr(obs_h.data_ptr(), est_h.data_ptr(), rule)  # warm
         if dist:
@@ -320,7 +323,7 @@ def main():
         if dist:
             dist.all_reduce(te, op=dist.ReduceOp.MAX)
         e2e_value = ws * e2e_steps * iters * n_img / float(te.item())  # one volume per rank per e2e step
-        assert torch.equal(est_h, out.cpu()), "host-API and device-API results differ"
+        assert torch.equal(est_h, outs[-1].cpu()), "host-API and device-API results differ"
 
     # ---- roofline of the dominant kernel ------------------------------------
     peak, peak_src = load_peaks()

@@ -129,6 +129,17 @@ vk_status vk_rl_run_batch(vk_rl_plan plan, int n, const float* const* observed,
                           float* const* estimate, const vk_stop_rule* rule, int flat_init,
                           vk_trace* traces);
 
+/* The same on device buffers.  The volumes run concurrently on the plan's
+ * batch lanes (clones with their own work buffers and stream, one host thread
+ * each; VK_RL_LANES overrides the count), so short per-volume grids overlap
+ * and fill the GPU.  Inputs must be ready on `stream`; the call returns when
+ * every estimate is written. */
+vk_status vk_rl_run_batch_device(vk_rl_plan plan, int n, const float* const* d_observed,
+                                 float* const* d_estimate, const vk_stop_rule* rule, int flat_init,
+                                 vk_trace* traces, void* stream);
+/* Lanes currently allocated (1 + clones). */
+vk_status vk_rl_plan_lanes(vk_rl_plan plan, int* lanes);
+
 /* rl_step(estimate, observed, transforms) (deconv.cpp:178-194) on a
  * pad_replicate = 0 plan: one multiplicative update on the plan's domain. */
 vk_status vk_rl_step(vk_rl_plan plan, const float* estimate, const float* observed, float* out);

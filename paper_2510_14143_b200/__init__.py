@@ -153,6 +153,11 @@ def lib() -> ctypes.CDLL:
     L.vk_rl_run_device.argtypes = [_vp, _vp, _vp, ctypes.POINTER(_Rule), i, ctypes.POINTER(_Trace), _vp]
     L.vk_rl_run_batch.argtypes = [_vp, i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_Rule), i,
                                   ctypes.POINTER(_Trace)]
+    L.vk_rl_run_batch_device.argtypes = [_vp, i, ctypes.POINTER(_vp), ctypes.POINTER(_vp), ctypes.POINTER(_Rule),
+                                         i, ctypes.POINTER(_Trace), _vp]
+    L.vk_rl_run_batch_device.restype = st
+    L.vk_rl_plan_lanes.argtypes = [_vp, ctypes.POINTER(i)]
+    L.vk_rl_plan_lanes.restype = st
     L.vk_rl_step.argtypes = [_vp, _vp, _vp, _vp]
     L.vk_rl_step_device.argtypes = [_vp, _vp, _vp, _vp, _vp]
     L.vk_richardson_lucy.argtypes = [i, i, _u64p, _vp, i, _u64p, _fp, ctypes.POINTER(_Rule), i, _vp,
@@ -399,6 +404,30 @@ class RlPlan(_Plan):
         _check(lib().vk_rl_run_device(self._h, obs_ptr, est_ptr, ctypes.byref(rule._c()), int(bool(flat_init)),
                                       ctypes.byref(tb.c) if tb else None, stream))
         return tb.trace(rule.metric, self.rank) if tb else None
+
+    def run_batch_device(self, obs_ptrs: Sequence[int], est_ptrs: Sequence[int], rule: StoppingRule,
+                         flat_init: bool = False, stream: int = 0, trace: bool = True):
+        """Independent device-resident volumes, run concurrently on the plan's
+        batch lanes (vk_rl_run_batch_device)."""
+        n = len(obs_ptrs)
+        tbs = [_TraceBuf(max(int(rule.max_iters), 1)) for _ in range(n)] if trace else None
+        traces = (_Trace * max(n, 1))(*[t.c for t in tbs]) if trace else None
+        ip = (_vp * max(n, 1))(*obs_ptrs)
+        op = (_vp * max(n, 1))(*est_ptrs)
+        _check(lib().vk_rl_run_batch_device(self._h, n, ip, op, ctypes.byref(rule._c()), int(bool(flat_init)),
+                                            traces, stream))
+        if not trace:
+            return None
+        out = []
+        for i in range(n):
+            tbs[i].c = traces[i]
+            out.append(tbs[i].trace(rule.metric, self.rank))
+        return out
+
+    def lanes(self) -> int:
+        v = ctypes.c_int(0)
+        _check(lib().vk_rl_plan_lanes(self._h, ctypes.byref(v)))
+        return int(v.value)
 
     def run_batch(self, observed: Sequence[np.ndarray], rule: StoppingRule = StoppingRule(),
                   flat_init: bool = False) -> List[RlResult]:

@@ -316,7 +316,10 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   }
 }
 
-template <int R1, int R2, int L, bool TWG>
+// PREF: the CONV mode stages the OTF tile in shared memory with cp.async
+// while the forward transform runs; without it (long lines, where the tile
+// would cost a resident CTA) the multiply reads the OTF from global directly.
+template <int R1, int R2, int L, bool TWG, bool PREF>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     ypass_fast(const YArgs a) {
   using C = FastCfg<R1, R2, L, true>;
@@ -339,7 +342,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     }
   }
   cp_async_commit();
-  if (a.mode == YM_CONV) {
+  if (PREF && a.mode == YM_CONV) {
     for (int l = 0; l < L; ++l) {
       const int line = line0 + l;
       if (line >= a.nlines) break;
@@ -350,7 +353,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   }
   if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
   const float2* twp = TWG ? a.plan.tw2 : tw;
-  if (a.mode == YM_CONV)
+  if (PREF && a.mode == YM_CONV)
     cp_async_wait_1();  // input rows landed, OTF may still fly
   else
     cp_async_wait_all();
@@ -360,11 +363,21 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   } else {
     reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, twp);
     if (a.mode == YM_CONV) {
-      cp_async_wait_all();
-      __syncthreads();
-      for (int idx = threadIdx.x; idx < N * L; idx += NT) {
-        const int k = idx / L, l = idx % L;
-        A[sw<L>(k, l)] = cmul(A[sw<L>(k, l)], O[l * N + k]);
+      if (PREF) {
+        cp_async_wait_all();
+        __syncthreads();
+        for (int idx = threadIdx.x; idx < N * L; idx += NT) {
+          const int k = idx / L, l = idx % L;
+          A[sw<L>(k, l)] = cmul(A[sw<L>(k, l)], O[l * N + k]);
+        }
+      } else {
+        // line-major walk: coalesced OTF reads, stride L+1 (odd) in smem
+        for (int l = 0; l < L; ++l) {
+          const int line = line0 + l;
+          if (line >= a.nlines) break;
+          const float2* o = a.otf + (size_t)line * N;
+          for (int k = threadIdx.x; k < N; k += NT) A[sw<L>(k, l)] = cmul(A[sw<L>(k, l)], __ldg(o + k));
+        }
       }
       __syncthreads();
       reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, twp);

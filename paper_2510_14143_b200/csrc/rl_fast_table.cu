@@ -11,7 +11,7 @@ namespace vk {
 
 namespace {
 
-template <int R1, int R2, int LX, int LZ, bool TWG = false>
+template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true>
 FastEntry make_entry() {
   FastEntry e{};
   e.N = R1 * R2;
@@ -21,10 +21,10 @@ FastEntry make_entry() {
   e.NTx = FastCfg<R1, R2, LX>::NT;
   e.smem_x = FastCfg<R1, R2, LX>::smem;
   e.smem_yp = e.smem_xp;
-  e.smem_yconv = TWG ? (size_t)(FastCfg<R1, R2, LX, true>::DATA + R1 * R2 * LX) * sizeof(float2)
-                     : FastCfg<R1, R2, LX, true>::smem;
+  e.smem_yconv = (size_t)(FastCfg<R1, R2, LX, true>::DATA + (TWG ? 0 : R1 * R2) + (YPREF ? R1 * R2 * LX : 0)) *
+                 sizeof(float2);
   e.xk = (const void*)xpass_fast<R1, R2, LX, TWG>;
-  e.yk = (const void*)ypass_fast<R1, R2, LX, TWG>;
+  e.yk = (const void*)ypass_fast<R1, R2, LX, TWG, YPREF>;
   e.Lz = LZ;
   e.NTz = FastCfg<R1, R2, LZ, true>::NT;
   e.smem_z = FastCfg<R1, R2, LZ, true>::smem;
@@ -42,7 +42,7 @@ const FastEntry kTable[] = {
     make_entry<16, 18, 16, 16>(),  // 288
     make_entry<24, 24, 8, 8, true>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM
     make_entry<30, 36, 8, 4>(),    // 1080
-    make_entry<45, 48, 4, 2>(),    // 2160
+    make_entry<45, 48, 4, 2, true, false>(),  // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM
 };
 
 }  // namespace

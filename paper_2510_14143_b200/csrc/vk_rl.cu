@@ -18,6 +18,7 @@
 #include <limits>
 #include <new>
 #include <string>
+#include <thread>
 #include <vector>
 
 #include "../../include/vk_rl.h"
@@ -246,7 +247,13 @@ struct vk_rl_plan_s {
   double prof_ms[VK_KIND_COUNT]{};
   uint64_t prof_n[VK_KIND_COUNT]{};
 
+  // Batch lanes: clones of this plan (own buffers and stream) that run
+  // independent volumes concurrently, one host thread each (lane 0 = this).
+  std::vector<float> psf_host;
+  std::vector<vk_rl_plan_s*> lanes;
+
   ~vk_rl_plan_s() {
+    for (auto* l : lanes) delete l;
     for (auto e : events) cudaEventDestroy(e);
     for (auto e : prof_pool) cudaEventDestroy(e);
     if (h_acc) cudaFreeHost(h_acc);
@@ -629,6 +636,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->ishape[i] = shape[i];
       p->kshape[i] = psf_shape[i];
     }
+    p->psf_host.assign(psf, psf + (size_t)K3[0] * K3[1] * K3[2]);
     const uint64_t P3[3] = {(uint64_t)g.Pz, (uint64_t)g.Py, (uint64_t)g.Px};
     const uint64_t W3[3] = {(uint64_t)g.Wz, (uint64_t)g.Wy, (uint64_t)g.Wx};
     for (int i = 0; i < rank; ++i) {
@@ -1193,6 +1201,66 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
 }
 
+// Lanes for a batch of n independent volumes: VK_RL_LANES, else enough to
+// fill the GPU when one volume's x-pass grid is short of a few waves.
+int lane_count(vk_rl_plan p, int n) {
+  const char* env = std::getenv("VK_RL_LANES");
+  int want;
+  if (env && std::atoi(env) > 0) {
+    want = std::atoi(env);
+  } else {
+    // measured on B200 (profiles/r01/lanes.log): C3 (64^3-class volumes)
+    // 1/2/3/4 lanes = 2.08/2.78/2.83/2.81e10, C5 (2048^2 fields) 1/2/4/6 =
+    // 2.69/3.06/2.84/2.81e10 voxel-iters/s
+    const Geom& g = p->g;
+    const int L = p->fx ? p->fx->Lx : p->xL;
+    const long long ctas = (long long)((g.Py + 2 * L - 1) / (2 * L)) * g.Pz;
+    want = (p->rank == 3 && ctas < 148 * 16) ? 3 : 2;
+  }
+  return std::max(1, std::min(want, n));
+}
+
+// Runs fn(lane_plan, volume) for volumes 0..n-1, volume i on lane i % lanes,
+// each lane on its own host thread and stream; rethrows the first failure.
+template <class F>
+void run_lanes(vk_rl_plan p, int n, F&& fn) {
+  if (n <= 0) return;
+  const int nl = lane_count(p, n);
+  while ((int)p->lanes.size() < nl - 1) {
+    vk_rl_plan q = create_plan(p->device, p->rank, p->ishape, p->rank, p->kshape, p->psf_host.data(), p->pad ? 1 : 0);
+    q->prof = p->prof;
+    p->lanes.push_back(q);
+  }
+  std::vector<Fail> errs(nl);
+  std::vector<int> bad(nl, 0);
+  std::vector<uint64_t> cnt(nl, 0);
+  auto work = [&](int li) {
+    vk_rl_plan q = li == 0 ? p : p->lanes[li - 1];
+    try {
+      DeviceGuard dg(p->device);
+      for (int i = li; i < n; i += nl) {
+        fn(q, i);
+        cnt[li] += q->launches;
+      }
+    } catch (const Fail& e) {
+      errs[li] = e;
+      bad[li] = 1;
+    } catch (const std::exception& e) {
+      errs[li] = Fail{VK_ERR_ARG, e.what()};
+      bad[li] = 1;
+    }
+  };
+  std::vector<std::thread> th;
+  for (int li = 1; li < nl; ++li) th.emplace_back(work, li);
+  work(0);
+  for (auto& t : th) t.join();
+  uint64_t launches = 0;
+  for (int li = 0; li < nl; ++li) launches += cnt[li];
+  p->launches = launches;  // every launch of the batch
+  for (int li = 0; li < nl; ++li)
+    if (bad[li]) throw errs[li];
+}
+
 // filters::fft_convolve on a conv plan (filters.cpp:174-264): R2C of the
 // image, times the kernel spectrum (1/prod(W) folded in), C2R and the crop at
 // the kernel centre (linear) or at 0 (circular).
@@ -1323,6 +1391,10 @@ vk_status vk_rl_plan_profile(vk_rl_plan p, int enable) {
     DeviceGuard dg(p->device);
     prof_collect(p);
     p->prof = enable != 0;
+    for (auto* l : p->lanes) {
+      prof_collect(l);
+      l->prof = p->prof;
+    }
   });
 }
 
@@ -1332,15 +1404,26 @@ vk_status vk_rl_plan_profile_read(vk_rl_plan p, int n_kinds, double* ms_total, u
     if (!p) fail(VK_ERR_ARG, "NULL plan");
     DeviceGuard dg(p->device);
     prof_collect(p);
-    for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k) {
-      if (ms_total) ms_total[k] = p->prof_ms[k];
-      if (launches) launches[k] = p->prof_n[k];
+    for (auto* l : p->lanes) prof_collect(l);
+    for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k) {  // summed over the batch lanes
+      double ms = p->prof_ms[k];
+      uint64_t cnt = p->prof_n[k];
+      for (auto* l : p->lanes) {
+        ms += l->prof_ms[k];
+        cnt += l->prof_n[k];
+      }
+      if (ms_total) ms_total[k] = ms;
+      if (launches) launches[k] = cnt;
       if (alg_bytes_per_launch) alg_bytes_per_launch[k] = alg_bytes(p, k);
     }
     if (reset)
       for (int k = 0; k < VK_KIND_COUNT; ++k) {
         p->prof_ms[k] = 0;
         p->prof_n[k] = 0;
+        for (auto* l : p->lanes) {
+          l->prof_ms[k] = 0;
+          l->prof_n[k] = 0;
+        }
       }
   });
 }
@@ -1382,10 +1465,31 @@ vk_status vk_rl_run_batch(vk_rl_plan p, int n, const float* const* obs, float* c
                           int flat_init, vk_trace* traces) {
   return guarded([&] {
     if (!p || n < 0 || (n > 0 && (!obs || !est))) fail(VK_ERR_ARG, "NULL argument");
-    for (int i = 0; i < n; ++i) {
-      const vk_status st = vk_rl_run(p, obs[i], est[i], rule, flat_init, traces ? &traces[i] : nullptr);
+    check_rule(rule);
+    run_lanes(p, n, [&](vk_rl_plan q, int i) {
+      const vk_status st = vk_rl_run(q, obs[i], est[i], rule, flat_init, traces ? &traces[i] : nullptr);
       if (st != VK_OK) fail(st, "volume " + std::to_string(i) + ": " + g_last_error);
-    }
+    });
+  });
+}
+
+vk_status vk_rl_run_batch_device(vk_rl_plan p, int n, const float* const* d_obs, float* const* d_est,
+                                 const vk_stop_rule* rule, int flat_init, vk_trace* traces, void* stream) {
+  return guarded([&] {
+    if (!p || n < 0 || (n > 0 && (!d_obs || !d_est))) fail(VK_ERR_ARG, "NULL argument");
+    check_rule(rule);
+    DeviceGuard dg(p->device);
+    ck(cudaStreamSynchronize((cudaStream_t)stream), "batch inputs");  // the lanes read them
+    run_lanes(p, n, [&](vk_rl_plan q, int i) {
+      run_device(q, d_obs[i], d_est[i], rule, flat_init, traces ? &traces[i] : nullptr, q->stream, true);
+    });
+  });
+}
+
+vk_status vk_rl_plan_lanes(vk_rl_plan p, int* lanes) {
+  return guarded([&] {
+    if (!p || !lanes) fail(VK_ERR_ARG, "NULL argument");
+    *lanes = 1 + (int)p->lanes.size();
   });
 }
 

@@ -351,6 +351,48 @@ def test_stopping_semantics_tol_inf():
     assert rel_l2(r.estimate, its[-1]) <= TOL_N
 
 
+@pytest.mark.parametrize("lanes", ["", "1", "3"])
+def test_batch_device_lanes_match_single_runs(lanes):
+    """vk_rl_run_batch_device: volumes on concurrent lanes (own buffers,
+    streams, host threads) give bitwise the single-run results and traces."""
+    import torch
+
+    old = os.environ.pop("VK_RL_LANES", None)
+    if lanes:
+        os.environ["VK_RL_LANES"] = lanes
+    try:
+        psf = O.gaussian_psf((7, 7), 1.5)
+        rng = np.random.default_rng(8)
+        vols = [(rng.random((130, 150)) * 2 + 0.1).astype(np.float32) for _ in range(7)]
+        plan = vk.RlPlan((130, 150), psf)
+        rule = fixed_rule(5)
+        single = [plan.run(v, rule) for v in vols]
+        d_in = [torch.from_numpy(v).cuda() for v in vols]
+        d_out = [torch.empty_like(d) for d in d_in]
+        trs = plan.run_batch_device([d.data_ptr() for d in d_in], [d.data_ptr() for d in d_out], rule,
+                                    stream=torch.cuda.current_stream().cuda_stream)
+        torch.cuda.synchronize()
+        for sgl, o, tr in zip(single, d_out, trs):
+            assert np.array_equal(o.cpu().numpy(), sgl.estimate)
+            # the metric sums use FP64 atomics: order-dependent in the last bits
+            np.testing.assert_allclose([r.value for r in tr.records], [r.value for r in sgl.trace.records],
+                                       rtol=1e-12)
+        assert plan.lanes() == (int(lanes) if lanes else 2)  # 2D default
+        assert plan.launches() > 7 * 5 * 4  # every lane's launches are counted
+        host = plan.run_batch(vols, rule)  # the host batch uses the lanes too
+        for sgl, h in zip(single, host):
+            assert np.array_equal(h.estimate, sgl.estimate)
+        # errors propagate from a worker lane (volume 2 negative)
+        bad = [d.clone() for d in d_in]
+        bad[2][0, 0] = -1
+        with pytest.raises(vk.NegativeInput):
+            plan.run_batch_device([d.data_ptr() for d in bad], [d.data_ptr() for d in d_out], rule)
+    finally:
+        os.environ.pop("VK_RL_LANES", None)
+        if old is not None:
+            os.environ["VK_RL_LANES"] = old
+
+
 def test_plan_reuse_batch_and_device_api():
     import torch
 
