@@ -33,6 +33,14 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// Programmatic dependent launch: the host launches the fast pass kernels
+// with cudaLaunchAttributeProgrammaticStreamSerialization.  Each grid lets
+// the next one launch as soon as all of its CTAs are resident (the next
+// grid's CTAs then fill the SMs our tail wave frees), and waits for the
+// previous grid to complete and flush before touching its results.
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+
 template <int R1, int R2, int L, bool OTF_PREFETCH = false>
 struct FastCfg {
   static_assert((L & (L - 1)) == 0, "L must be a power of two (cheap line/index split)");
@@ -57,7 +65,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
   extern __shared__ float2 smem[];
   const float2* tw = TWG ? a.plan.tw2 : smem;
   float2* A = TWG ? smem : smem + N;
-  if (!TWG) reg::load_twiddles2<R1, R2>(smem, a.plan.tw);
+  pdl_trigger();
+  if (!TWG) reg::load_twiddles2<R1, R2>(smem, a.plan.tw);  // constant table: before the wait
+  pdl_wait();
   const int z = blockIdx.y;
   const int y0 = blockIdx.x * 2 * L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -329,6 +339,8 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   float2* A = TWG ? smem : smem + N;
   float2* O = A + C::DATA;  // OTF tile [l][k] (CONV only)
   const int line0 = blockIdx.x * L;
+  pdl_trigger();
+  pdl_wait();
   // async copies: the L input rows (zero padding written directly)
   for (int l = 0; l < L; ++l) {
     const int line = line0 + l;
@@ -411,6 +423,8 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   float2* col = a.S + ((unsigned)kx * a.zrows * a.Wy + (kok ? ky : 0));
   const unsigned oplane = (unsigned)kx * N * a.Wy + (kok ? ky : 0);
   const unsigned Wy = a.Wy;
+  pdl_trigger();
+  pdl_wait();
 #pragma unroll
   for (int k = 0; k < IT; ++k) {
     const int z = z0 + k * ZS;

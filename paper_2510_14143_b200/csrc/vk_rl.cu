@@ -314,9 +314,29 @@ void prof_collect(vk_rl_plan p) {
 
 // ---- pass launchers -------------------------------------------------------
 
-void launch(const void* k, dim3 grid, int nt, size_t smem, cudaStream_t s, void* arg) {
+// pdl: programmatic dependent launch (the kernel calls pdl_trigger/pdl_wait,
+// rl_fast.cuh); VK_RL_NO_PDL=1 turns it off.
+void launch(const void* k, dim3 grid, int nt, size_t smem, cudaStream_t s, void* arg, bool pdl = false) {
   void* args[] = {arg};
-  ck(cudaLaunchKernel(k, grid, dim3(nt), args, smem, s), "launch");
+  static const bool no_pdl = [] {
+    const char* e = std::getenv("VK_RL_NO_PDL");
+    return e && e[0] == '1';
+  }();
+  if (!pdl || no_pdl) {
+    ck(cudaLaunchKernel(k, grid, dim3(nt), args, smem, s), "launch");
+    return;
+  }
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = dim3(nt);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  ck(cudaLaunchKernelExC(&cfg, k, args), "launch");
 }
 
 void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z, int rows_y, int len,
@@ -341,7 +361,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
   if (p->fx)
-    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_xp, s, &a);
+    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_xp, s, &a, true);
   else
     vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
   launch_check(p, "xpass");
@@ -367,7 +387,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
   if (p->fy)
-    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a);
+    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a, true);
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
@@ -399,7 +419,7 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
   const size_t t = prof_begin(p, s);
   if (p->fz)
-    launch(p->fz->zk, grid, p->fz->NTz, p->fz->smem_z, s, &a);
+    launch(p->fz->zk, grid, p->fz->NTz, p->fz->smem_z, s, &a, true);
   else
     vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
   launch_check(p, "zpass");
