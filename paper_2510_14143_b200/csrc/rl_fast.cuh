@@ -53,8 +53,11 @@ struct FastCfg {
 
 // TWG: pass-2 twiddles read from global memory (L1) instead of a shared
 // table, when dropping the table buys one more resident CTA per SM.
-template <int R1, int R2, int L, bool TWG>
-__global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
+// MINB: resident CTAs per SM the register allocation must allow.  PB: the
+// partial-chunk epilogue batches its loads like the full one (worth its
+// registers only where partial chunks are common, e.g. Ix = 1000).
+template <int R1, int R2, int L, bool TWG, int MINB, bool PB>
+__global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB)  // 1: leave the heuristic alone
     xpass_fast(const XArgs a) {
   using C = FastCfg<R1, R2, L>;
   constexpr int N = C::N, NT = C::NT;
@@ -255,40 +258,96 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT)
         }
         continue;
       }
-      // partial chunk (last interior piece or a missing second row)
+      // partial chunk (last interior piece or a missing second row): the
+      // same batched loads, predicated per lane
+      if (PB) {
+        float fa0 = 0.f, fa1 = 0.f, fa2 = 0.f, fb0 = 0.f, fb1 = 0.f, fb2 = 0.f;
+        float2 m[U];
+        float o_a[U], o_b[U], e_a[U], e_b[U];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int c = c0 + u * 32 + lane;
-        if (c >= g.Ix) break;
-        const int sidx = s0 + u * 32 * (L + 1);
-        const float2 m = A[sidx];
-        const float o_a = __ldg(oa2 + u * 32), o_b = __ldg(ob2 + u * 32);
-        float2 val;
-        if (ratio) {
-          const float ma = fmaxf(m.x, kEps), mb = fmaxf(m.y, kEps);
-          val = make_float2(va ? __fdividef(o_a, ma) : 0.f, vb ? __fdividef(o_b, mb) : 0.f);
-          if (ina) acc0 += fmaf(o_a, __logf(ma), -ma);
-          if (inb) acc0 += fmaf(o_b, __logf(mb), -mb);
-        } else {
-          val = make_float2(va ? fmaxf(ea2[u * 32] * m.x, 0.f) : 0.f, vb ? fmaxf(eb2[u * 32] * m.y, 0.f) : 0.f);
-          if (!last) {
-            if (va) ea2[u * 32] = val.x;
-            if (vb) eb2[u * 32] = val.y;
-          }
-          if (ina) {
-            acc0 += val.x;
-            acc1 += (double)val.x * val.x;
-            acc2 += (double)val.x * o_a;
-            if (last) a.out[oa_off + c] = val.x;
-          }
-          if (inb) {
-            acc0 += val.y;
-            acc1 += (double)val.y * val.y;
-            acc2 += (double)val.y * o_b;
-            if (last) a.out[ob_off + c] = val.y;
+        for (int u = 0; u < U; ++u) {
+          const bool ok = c0 + u * 32 + lane < g.Ix;
+          m[u] = ok ? A[s0 + u * 32 * (L + 1)] : make_float2(0.f, 0.f);
+          o_a[u] = ok ? __ldg(oa2 + u * 32) : 0.f;
+          o_b[u] = ok ? __ldg(ob2 + u * 32) : 0.f;
+          if (!ratio) {
+            e_a[u] = (ok && va) ? ea2[u * 32] : 0.f;
+            e_b[u] = (ok && vb) ? eb2[u * 32] : 0.f;
           }
         }
-        A[sidx] = val;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c >= g.Ix) break;
+          float2 val;
+          if (ratio) {
+            const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
+            val = make_float2(va ? __fdividef(o_a[u], ma) : 0.f, vb ? __fdividef(o_b[u], mb) : 0.f);
+            fa0 += fmaf(o_a[u], __logf(ma), -ma);
+            fb0 += fmaf(o_b[u], __logf(mb), -mb);
+          } else {
+            val = make_float2(fmaxf(e_a[u] * m[u].x, 0.f), fmaxf(e_b[u] * m[u].y, 0.f));
+            if (!last) {
+              if (va) ea2[u * 32] = val.x;
+              if (vb) eb2[u * 32] = val.y;
+            } else {
+              if (ina) a.out[oa_off + c] = val.x;
+              if (inb) a.out[ob_off + c] = val.y;
+            }
+            fa0 += val.x;
+            fa1 = fmaf(val.x, val.x, fa1);
+            fa2 = fmaf(val.x, o_a[u], fa2);
+            fb0 += val.y;
+            fb1 = fmaf(val.y, val.y, fb1);
+            fb2 = fmaf(val.y, o_b[u], fb2);
+          }
+          A[s0 + u * 32 * (L + 1)] = val;
+        }
+        if (ina) {
+          acc0 += fa0;
+          acc1 += fa1;
+          acc2 += fa2;
+        }
+        if (inb) {
+          acc0 += fb0;
+          acc1 += fb1;
+          acc2 += fb2;
+        }
+      } else {  // sample by sample (fewest registers)
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int c = c0 + u * 32 + lane;
+          if (c >= g.Ix) break;
+          const int sidx = s0 + u * 32 * (L + 1);
+          const float2 m = A[sidx];
+          const float o_a = __ldg(oa2 + u * 32), o_b = __ldg(ob2 + u * 32);
+          float2 val;
+          if (ratio) {
+            const float ma = fmaxf(m.x, kEps), mb = fmaxf(m.y, kEps);
+            val = make_float2(va ? __fdividef(o_a, ma) : 0.f, vb ? __fdividef(o_b, mb) : 0.f);
+            if (ina) acc0 += fmaf(o_a, __logf(ma), -ma);
+            if (inb) acc0 += fmaf(o_b, __logf(mb), -mb);
+          } else {
+            val = make_float2(va ? fmaxf(ea2[u * 32] * m.x, 0.f) : 0.f, vb ? fmaxf(eb2[u * 32] * m.y, 0.f) : 0.f);
+            if (!last) {
+              if (va) ea2[u * 32] = val.x;
+              if (vb) eb2[u * 32] = val.y;
+            }
+            if (ina) {
+              acc0 += val.x;
+              acc1 += (double)val.x * val.x;
+              acc2 += (double)val.x * o_a;
+              if (last) a.out[oa_off + c] = val.x;
+            }
+            if (inb) {
+              acc0 += val.y;
+              acc1 += (double)val.y * val.y;
+              acc2 += (double)val.y * o_b;
+              if (last) a.out[ob_off + c] = val.y;
+            }
+          }
+          A[sidx] = val;
+        }
       }
     }
     if (ratio) {

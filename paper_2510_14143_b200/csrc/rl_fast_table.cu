@@ -11,7 +11,7 @@ namespace vk {
 
 namespace {
 
-template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true>
+template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false>
 FastEntry make_entry() {
   FastEntry e{};
   e.N = R1 * R2;
@@ -23,7 +23,7 @@ FastEntry make_entry() {
   e.smem_yp = e.smem_xp;
   e.smem_yconv = (size_t)(FastCfg<R1, R2, LX, true>::DATA + (TWG ? 0 : R1 * R2) + (YPREF ? R1 * R2 * LX : 0)) *
                  sizeof(float2);
-  e.xk = (const void*)xpass_fast<R1, R2, LX, TWG>;
+  e.xk = (const void*)xpass_fast<R1, R2, LX, TWG, XMINB, XPB>;
   e.yk = (const void*)ypass_fast<R1, R2, LX, TWG, YPREF>;
   e.Lz = LZ;
   e.NTz = FastCfg<R1, R2, LZ, true>::NT;
@@ -40,8 +40,8 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16>(),  // 192
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 8, 8, true>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM
-    make_entry<30, 36, 8, 4>(),    // 1080
+    make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM
+    make_entry<30, 36, 8, 4, false, true, 1, true>(),  // 1080 (Ix = 1000: partial chunks are common)
     make_entry<45, 48, 4, 2, true, false>(),  // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM
 };
 
