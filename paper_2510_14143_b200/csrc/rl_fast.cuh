@@ -462,14 +462,17 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   }
 }
 
-template <int R1, int R2, int L>
-__global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
+// TWG / PREF / MINB as for the x and y passes: pass-2 twiddles from global,
+// OTF tile staged in shared memory during the forward transform (else read
+// from global in the multiply), and the resident CTAs per SM to allow for.
+template <int R1, int R2, int L, bool TWG, bool PREF, int MINB>
+__global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT, MINB == 1 ? 0 : MINB)
     zpass_fast(const ZArgs a) {
   using C = FastCfg<R1, R2, L, true>;
   constexpr int N = C::N, NT = C::NT;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* A = smem + N;
+  float2* tw = TWG ? nullptr : smem;
+  float2* A = TWG ? smem : smem + N;
   float2* O = A + C::DATA;  // OTF tile, [kz][l] row-major (pitch L)
   // NT is a multiple of L: a thread owns one column l (ky = ky0 + l) and
   // strides z by ZS = NT/L; offsets are 32-bit and compile-time unrolled.
@@ -496,7 +499,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   }
   cp_async_commit();
   const bool conv = a.mode == ZM_CONV;
-  if (conv) {
+  if (PREF && conv) {
     const float2* o = a.otf + oplane;
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
@@ -505,13 +508,14 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     }
     cp_async_commit();
   }
-  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
-  if (conv)
+  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  const float2* twp = TWG ? a.plan.tw2 : tw;
+  if (PREF && conv)
     cp_async_wait_1();
   else
     cp_async_wait_all();
   __syncthreads();
-  reg::fft2<R1, R2, L, NT, false>(A, tw);
+  reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, twp);
   if (!conv) {
     float2* o = a.otf_out + oplane;
 #pragma unroll
@@ -521,15 +525,18 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
     }
     return;
   }
-  cp_async_wait_all();
-  __syncthreads();
+  if (PREF) {
+    cp_async_wait_all();
+    __syncthreads();
+  }
+  const float2* og = a.otf + oplane;
 #pragma unroll
   for (int k = 0; k < IT; ++k) {
     const int z = z0 + k * ZS;
-    if (z < N) A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], O[z * L + l]);
+    if (z < N) A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], PREF ? O[z * L + l] : (kok ? __ldg(&og[(unsigned)z * Wy]) : make_float2(0.f, 0.f)));
   }
   __syncthreads();
-  reg::fft2<R1, R2, L, NT, true>(A, tw);
+  reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, twp);
   if (kok) {
     for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[sw<L>(z + a.out_off, l)];
   }

@@ -187,7 +187,7 @@ struct vk_rl_plan_s {
   int psf_status = 0;  // 0 ok, VK_ERR_NEGATIVE, VK_ERR_UNNORMALIZED_PSF
   std::string psf_msg;
 
-  DevBuf<float2> twx, twy, twz, twx2, twy2;
+  DevBuf<float2> twx, twy, twz, twx2, twy2, twz2;
   LinePlan lpx{}, lpy{}, lpz{};
   // compile-time-length kernels per axis (nullptr -> generic Stockham)
   const vk::FastEntry* fx = nullptr;
@@ -752,6 +752,15 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
         p->twx2.alloc(t2.size(), "twiddles");
         ck(cudaMemcpy(p->twx2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
         p->lpx.tw2 = p->twx2.p;
+      }
+      if (p->fz) {  // and the fast z pass
+        const int R1 = p->fz->R1, R2 = g.Wz / R1;
+        std::vector<float2> t2((size_t)R1 * R2);
+        for (int j = 0; j < R1; ++j)
+          for (int r = 0; r < R2; ++r) t2[(size_t)j * R2 + r] = tz[(size_t)r * j];
+        p->twz2.alloc(t2.size(), "twiddles");
+        ck(cudaMemcpy(p->twz2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
+        p->lpz.tw2 = p->twz2.p;
       }
       if (p->fy) {  // same for the fast y pass
         const int R1 = p->fy->R1, R2 = g.Wy / R1;
