@@ -9,6 +9,7 @@ namespace vk {
 
 struct FastEntry {
   int N, R1;            // N = R1 * R2 (pass-1 / pass-2 radices)
+  bool pdl;             // launch with programmatic dependent launch
   size_t smem_xp;       // x-pass
   size_t smem_yp;       // y-pass FWD/INV
   int Lx, NTx;          // x-pass and y-pass: lines per CTA, threads

@@ -14,10 +14,11 @@ namespace {
 // TWG / YPREF / XMINB / XPB: x and y pass variants (rl_fast.cuh); ZTWG /
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
-          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1>
+          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true>
 FastEntry make_entry() {
   FastEntry e{};
   e.N = R1 * R2;
+  e.pdl = PDL;
   e.R1 = R1;
   e.smem_xp = TWG ? FastCfg<R1, R2, LX>::smem_x : FastCfg<R1, R2, LX>::smem;
   e.Lx = LX;
@@ -46,7 +47,10 @@ const FastEntry kTable[] = {
     make_entry<16, 18, 16, 16>(),  // 288
     make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM
     make_entry<30, 36, 8, 4, false, true, 1, true>(),  // 1080 (Ix = 1000: partial chunks are common)
-    make_entry<45, 48, 4, 2, true, false>(),  // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM
+    // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
+    // in griddepcontrol.wait would hold the scarce slots the batch lanes'
+    // kernels need: C5 3.05e10 without vs 2.66e10 with, profiles/r01/pdl.log)
+    make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false>(),
 };
 
 }  // namespace

@@ -361,7 +361,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
   if (p->fx)
-    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_xp, s, &a, true);
+    launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_xp, s, &a, p->fx->pdl);
   else
     vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
   launch_check(p, "xpass");
@@ -387,7 +387,8 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
   if (p->fy)
-    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a, true);
+    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
+           p->fy->pdl);
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
@@ -419,7 +420,7 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
   const size_t t = prof_begin(p, s);
   if (p->fz)
-    launch(p->fz->zk, grid, p->fz->NTz, p->fz->smem_z, s, &a, true);
+    launch(p->fz->zk, grid, p->fz->NTz, p->fz->smem_z, s, &a, p->fz->pdl);
   else
     vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
   launch_check(p, "zpass");
