@@ -178,6 +178,54 @@ vk_status vk_fft_convolve(int device, int rank, const uint64_t* shape, const flo
                           int kernel_rank, const uint64_t* kernel_shape, const float* kernel,
                           int circular, float* out);
 
+/* ---- Single-volume slab decomposition --------------------
+ * richardson_lucy on a 3D volume split into `nslabs` z slabs of the padded
+ * domain P, one plan per slab (per GPU).  Slab r owns P rows [own_begin,
+ * own_end) and computes on [domain_begin, domain_end) = the owned rows plus
+ * the correlations' reach (Kz-1-cz below, cz above, clipped to P).  After
+ * every x pass the caller overwrites the halo rows of each plan's x-spectrum
+ * S_A with the neighbours' owned rows (ncclSend/Recv, peer copies, ...):
+ * rows are [kx][row][y] complex64 at `spectrum`, `kx_planes` planes of `rows`
+ * rows of `row_elems` elements; halo_below rows start at local row 0, the
+ * halo_above rows at rows - halo_above, and the matching source rows are the
+ * neighbour's first / last owned rows.  Sums (stats, per-iteration LL and
+ * si_psnr sums) are per slab; the caller adds them up (all-reduce).  The
+ * stopping rule runs on the caller's side; si_psnr only.
+ *
+ *   begin(obs_local) -> stats[8]: Σr, Σr², min, max, Σ obs_p over owned rows,
+ *                       negative flag, image voxels, owned P voxels
+ *   start(iters, flat_init, mean)     -> x pass      [exchange]
+ *   per iteration it = 1..:
+ *     forward(obs, it)                -> x pass      [exchange]
+ *     backward(obs, it, out or NULL)  -> x pass      [exchange unless last]
+ *   crop(out) (after a non-final backward), sums(iters) -> acc[iters][4]:
+ *     log-likelihood, Σx, Σx², Σx·r of the owned image rows. */
+typedef struct vk_slab_info {
+  int own_begin, own_end;        /* global P rows owned                    */
+  int domain_begin, domain_end;  /* global P rows of the local domain      */
+  int image_begin, image_end;    /* global image rows owned (obs / output) */
+  int halo_below, halo_above;    /* halo rows of the local domain          */
+  void* spectrum;                /* S_A (device)                           */
+  uint64_t kx_planes, rows, row_elems;
+} vk_slab_info;
+
+vk_status vk_rl_slab_plan_create(int device, const uint64_t* shape, const uint64_t* psf_shape,
+                                 const float* psf, int nslabs, int slab, vk_rl_plan* out,
+                                 vk_slab_info* info);
+vk_status vk_rl_slab_begin(vk_rl_plan plan, const float* d_observed_rows, double* stats, void* stream);
+vk_status vk_rl_slab_start(vk_rl_plan plan, int iters, int flat_init, double mean, void* stream);
+vk_status vk_rl_slab_forward(vk_rl_plan plan, const float* d_observed_rows, int iter, void* stream);
+vk_status vk_rl_slab_backward(vk_rl_plan plan, const float* d_observed_rows, int iter, float* d_out_rows,
+                              void* stream);
+vk_status vk_rl_slab_crop(vk_rl_plan plan, float* d_out_rows, void* stream);
+vk_status vk_rl_slab_sums(vk_rl_plan plan, int iters, double* acc, void* stream);
+/* Halo traffic: S_A rows [row, row+n) of every kx plane to / from a packed
+ * [kx_planes][n][row_elems] complex64 device buffer (for ncclSend/Recv), or
+ * directly between two slab plans (same device or peers). */
+vk_status vk_rl_slab_pack(vk_rl_plan plan, int row, int n, void* d_buf, void* stream);
+vk_status vk_rl_slab_unpack(vk_rl_plan plan, int row, int n, const void* d_buf, void* stream);
+vk_status vk_rl_slab_copy_rows(vk_rl_plan src, int src_row, vk_rl_plan dst, int dst_row, int n, void* stream);
+
 /* fftx::good_size (fft_plan.cpp:41-49). */
 uint64_t vk_good_size(uint64_t n);
 

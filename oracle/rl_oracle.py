@@ -335,6 +335,35 @@ def richardson_lucy(observed, psf, metric="si_psnr_vs_input", rel_tol=1e-3, pati
     return crop_interior(est, off, obs.shape), trace
 
 
+def richardson_lucy_slabs(observed, psf, nslabs: int, iters: int, flat_init=False):
+    """The §8(f4) slab decomposition restated on the CPU (test oracle): the
+    padded domain is cut into `nslabs` z slabs; slab r owns P rows [z0, z1) and
+    convolves over Q = [z0 - hb, z1 + ha) clipped to P with zeros outside,
+    hb = Kz-1-cz, ha = cz, taking its halo rows from the neighbours (here: the
+    global arrays).  Must equal richardson_lucy on the owned rows."""
+    obs, k = validate(observed, psf, 1e-3, 1, iters)
+    pshape, off = padded_domain(obs.shape, k.shape)
+    obs_p = replicate_pad(obs, off)
+    est = np.full(pshape, obs_p.mean()) if flat_init else obs_p.copy()
+    Pz, Kz = pshape[0], k.shape[0]
+    cz = kernel_center(Kz)
+    hb, ha = Kz - 1 - cz, cz
+    bounds = [(Pz * r // nslabs, Pz * (r + 1) // nslabs) for r in range(nslabs)]
+    doms = [(max(0, z0 - hb), min(Pz, z1 + ha)) for z0, z1 in bounds]
+    tfs = [RlTransforms((q1 - q0,) + pshape[1:], k) for q0, q1 in doms]
+    for _ in range(iters):
+        ratio = np.empty(pshape)
+        for (z0, z1), (q0, q1), t in zip(bounds, doms, tfs):
+            m = t.convolve(est[q0:q1], False)[z0 - q0:z1 - q0]
+            ratio[z0:z1] = obs_p[z0:z1] / np.maximum(m, K_DIV_EPSILON)
+        new = np.empty(pshape)
+        for (z0, z1), (q0, q1), t in zip(bounds, doms, tfs):
+            c = t.convolve(ratio[q0:q1], True)[z0 - q0:z1 - q0]
+            new[z0:z1] = np.maximum(est[z0:z1] * c, 0.0)
+        est = new
+    return crop_interior(est, off, obs.shape)
+
+
 def fft_convolve(img, kernel, circular=False) -> np.ndarray:
     """filters::fft_convolve (src/filters.cpp:175-264)."""
     a = np.asarray(img, np.float32).astype(np.float64)

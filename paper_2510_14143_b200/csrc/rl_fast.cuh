@@ -544,31 +544,39 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT, MINB == 1 ? 0 : 
 
 // Persistent, double-buffered z convolution: each CTA walks tiles
 // (kx, ky-chunk) with stride gridDim.x and keeps the NEXT tile's column block
-// and OTF block in flight (cp.async group) while it transforms the current
-// one, so HBM latency hides behind the FFT even at 2 CTAs per SM.
-template <int R1, int R2, int L>
+// (and, with PREF, its OTF block) in flight (cp.async group) while it
+// transforms the current one, so HBM latency hides behind the FFT.  TWG /
+// PREF / MINB as for zpass_fast.
+template <int R1, int R2, int L, bool TWG, bool PREF>
 struct ZPipeCfg {
   static constexpr int N = R1 * R2;
   static constexpr int NT = FastCfg<R1, R2, L, true>::NT;
-  static constexpr int STAGE = N * (L + 1) + N * L;  // padded data block + OTF tile
-  static constexpr size_t smem = (size_t)(N + 2 * STAGE) * sizeof(float2);  // tw + 2 stages
+  static constexpr int STAGE = N * (L + 1) + (PREF ? N * L : 0);  // padded data block (+ OTF tile)
+  static constexpr size_t smem = (size_t)((TWG ? 0 : N) + 2 * STAGE) * sizeof(float2);
 };
 
-template <int R1, int R2, int L>
-__global__ void __launch_bounds__(ZPipeCfg<R1, R2, L>::NT, 2)
+template <int R1, int R2, int L, bool TWG, bool PREF, int MINB>
+__global__ void __launch_bounds__(ZPipeCfg<R1, R2, L, TWG, PREF>::NT, MINB == 1 ? 0 : MINB)
     zpass_pipe(const ZArgs a) {
-  using C = ZPipeCfg<R1, R2, L>;
+  using C = ZPipeCfg<R1, R2, L, TWG, PREF>;
   constexpr int N = C::N, NT = C::NT;
   constexpr int ZS = NT / L;
   constexpr int IT = (N + ZS - 1) / ZS;
   extern __shared__ float2 smem[];
-  float2* tw = smem;
-  float2* buf = smem + N;  // stage s: padded data at buf + s*STAGE, OTF tile right after
-  const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
+  float2* tw = TWG ? nullptr : smem;
+  float2* buf = TWG ? smem : smem + N;  // stage s: padded data at buf + s*STAGE (OTF tile right after)
   const unsigned Wy = a.Wy;
   const int nchunks = (a.Wy + L - 1) / L;
   const int ntiles = nchunks * a.hx;
+  pdl_trigger();
+  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  const float2* twp = TWG ? a.plan.tw2 : tw;
+  pdl_wait();
+  // thread-derived offsets come from reg::fresh_tid() in every use, so the
+  // compiler cannot hoist IT unrolled addresses out of the tile loop
   auto issue = [&](int tile, int stage) {
+    const int t = reg::fresh_tid();
+    const int l = t & (L - 1), z0 = t / L;
     float2* A = buf + stage * C::STAGE;
     float2* O = A + N * (L + 1);
     const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
@@ -583,14 +591,13 @@ __global__ void __launch_bounds__(ZPipeCfg<R1, R2, L>::NT, 2)
           cp_async8(&A[sw<L>(z, l)], &col[(unsigned)z * Wy]);
         else
           A[sw<L>(z, l)] = make_float2(0.f, 0.f);
-        if (kok) cp_async8(&O[z * L + l], &o[(unsigned)z * Wy]);
+        if (PREF && kok) cp_async8(&O[z * L + l], &o[(unsigned)z * Wy]);
       }
     }
   };
   int tile = blockIdx.x;
   if (tile < ntiles) issue(tile, 0);
   cp_async_commit();
-  reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
   for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
     const int stage = it & 1;
     const int next = tile + gridDim.x;
@@ -600,16 +607,22 @@ __global__ void __launch_bounds__(ZPipeCfg<R1, R2, L>::NT, 2)
     __syncthreads();
     float2* A = buf + stage * C::STAGE;
     const float2* O = A + N * (L + 1);
-    reg::fft2<R1, R2, L, NT, false>(A, tw);
+    reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, twp);
+    const int t = reg::fresh_tid();
+    const int l = t & (L - 1), z0 = t / L;
+    const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
+    const bool kok = ky < a.Wy;
+    const float2* og = a.otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
       const int z = z0 + k * ZS;
-      if (z < N) A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], O[z * L + l]);
+      if (z < N)
+        A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], PREF ? O[z * L + l]
+                                                   : (kok ? __ldg(&og[(unsigned)z * Wy]) : make_float2(0.f, 0.f)));
     }
     __syncthreads();
-    reg::fft2<R1, R2, L, NT, true>(A, tw);
-    const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
-    if (ky < a.Wy) {
+    reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, twp);
+    if (kok) {
       float2* col = a.S + ((unsigned)kx * a.zrows * Wy + ky);
       for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[sw<L>(z + a.out_off, l)];
     }

@@ -14,7 +14,7 @@ namespace {
 // TWG / YPREF / XMINB / XPB: x and y pass variants (rl_fast.cuh); ZTWG /
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
-          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true>
+          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2>
 FastEntry make_entry() {
   FastEntry e{};
   e.N = R1 * R2;
@@ -34,15 +34,15 @@ FastEntry make_entry() {
   e.smem_z = (size_t)(FastCfg<R1, R2, LZ, true>::DATA + (ZTWG ? 0 : R1 * R2) + (ZPREF ? R1 * R2 * LZ : 0)) *
              sizeof(float2);
   e.zk = (const void*)zpass_fast<R1, R2, LZ, ZTWG, ZPREF, ZMINB>;
-  e.smem_zp = ZPipeCfg<R1, R2, LZ>::smem;
-  e.zpk = (const void*)zpass_pipe<R1, R2, LZ>;
+  e.smem_zp = ZPipeCfg<R1, R2, LZ, ZTWG, ZPREF>::smem;
+  e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
   return e;
 }
 
 const FastEntry kTable[] = {
     make_entry<8, 12, 16, 16>(),   // 96
     make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8>(),  // 144 (z: 8 CTAs/SM)
-    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5>(),  // 192 (z: 48 regs, 5 CTAs/SM)
+    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2>(),  // 192 (z: 48 regs, 5 CTAs/SM)
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
     make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM

@@ -369,7 +369,9 @@ __global__ void obs_stats_kernel(const float* __restrict__ obs, size_t n, ObsSta
 
 // est = edge-replicate pad of obs (deconv.cpp:221-237, 335-344); also the
 // padded-domain sum for flat_init.
-__global__ void pad_kernel(const float* __restrict__ obs, float* __restrict__ est, Geom g, ObsStats* st) {
+// sum_z0/sum_z1: P rows whose values enter sump (a slab sums its own rows).
+__global__ void pad_kernel(const float* __restrict__ obs, float* __restrict__ est, Geom g, ObsStats* st,
+                           int sum_z0, int sum_z1) {
   const size_t n = (size_t)g.Pz * g.Py * g.Px;
   double v[1] = {0.0};
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
@@ -380,9 +382,15 @@ __global__ void pad_kernel(const float* __restrict__ obs, float* __restrict__ es
                      clampi(x - g.ox, 0, g.Ix - 1);
     const float val = obs[o];
     est[i] = val;
-    v[0] += val;
+    if (z >= sum_z0 && z < sum_z1) v[0] += val;
   }
   block_accumulate<1>(v, &st->sump);
+}
+
+// Constant fill (a slab's flat_init with the mean of the whole volume).
+__global__ void fill_value_kernel(float* __restrict__ est, size_t n, float value) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x)
+    est[i] = value;
 }
 
 // flat_init: est = mean(obs_p) evaluated in double then stored in f32.

@@ -181,6 +181,10 @@ struct vk_rl_plan_s {
   int rank = 3;
   bool pad = true;
   int conv = 0;  // 0: RL plan; 1 / 2: filters::fft_convolve plan, linear / circular
+  // slab plans (vk_rl_slab_*): own P rows [own0, own1) of the local domain;
+  // halo rows below / above are refreshed by the caller between passes
+  bool slab = false;
+  int own0 = 0, own1 = 0;
   uint64_t ishape[3]{}, dshape[3]{}, wshape[3]{}, kshape[3]{};
   Geom g{};
   int Kz = 1, Ky = 1, Kx = 1;
@@ -412,7 +416,7 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   a.hx = p->g.Hx;
   if (p->fz && p->zpipe_blocks && mode == vk::ZM_CONV) {
     const size_t t = prof_begin(p, s);
-    launch(p->fz->zpk, dim3(p->zpipe_blocks), p->fz->NTz, p->fz->smem_zp, s, &a);
+    launch(p->fz->zpk, dim3(p->zpipe_blocks), p->fz->NTz, p->fz->smem_zp, s, &a, p->fz->pdl);
     launch_check(p, "zpass pipe");
     prof_end(p, s, VK_KIND_Z_CONV, t);
     return;
@@ -604,8 +608,10 @@ void to3(int rank, const uint64_t* in, uint64_t* out3) {
   for (int i = 0; i < rank; ++i) out3[3 - rank + i] = in[i];
 }
 
+// zslab (slab plans only): {P rows of the local domain, offset of the local
+// image's first row inside it} for the z axis instead of I + 2 floor(K/2).
 vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank, const uint64_t* psf_shape,
-                       const float* psf, int pad, int conv = 0) {
+                       const float* psf, int pad, int conv = 0, const int* zslab = nullptr) {
   if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
   if (psf_rank != rank)
     fail(VK_ERR_SHAPE, conv ? "ShapeMismatch: fft_convolve: rank mismatch"
@@ -635,10 +641,24 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     int* Wp[3] = {&g.Wz, &g.Wy, &g.Wx};
     int* Cp[3] = {&g.cz, &g.cy, &g.cx};
     for (int a = 0; a < 3; ++a) {
-      const uint64_t off = p->pad ? K3[a] / 2 : 0;  // deconv.cpp:215-216
-      const uint64_t P = I3[a] + 2 * off;
+      uint64_t off = p->pad ? K3[a] / 2 : 0;  // deconv.cpp:215-216
+      uint64_t P = I3[a] + 2 * off;
+      if (zslab && a == 0) {
+        P = (uint64_t)zslab[0];
+        off = (uint64_t)zslab[1];
+      }
       // deconv.cpp:116 / filters.cpp:191-192; circular: the image grid itself
-      const uint64_t W = conv == 2 ? P : good_size(P + K3[a] - 1);
+      uint64_t W = conv == 2 ? P : good_size(P + K3[a] - 1);
+      if (zslab && a == 0) {
+        // a slab's z grid is ours to choose (any W >= P+K-1 gives the same
+        // linear correlation): the smallest compile-time fast length within
+        // 1.5x of good_size, so the z pass keeps the register FFT
+        for (uint64_t c = W; c <= W + W / 2; ++c)
+          if (good_size(c) == c && vk::fast_lookup((int)c)) {
+            W = c;
+            break;
+          }
+      }
       if (P > (1u << 30) || W > (1u << 30)) fail(VK_ERR_ARG, "extent too large");
       if (good_size(W) != W)
         fail(VK_ERR_UNSUPPORTED, "circular fft_convolve on the B200 path needs 5-smooth extents (got " +
@@ -1133,7 +1153,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     ck(cudaStreamSynchronize(s), "ssim init");  // r0 is pageable
   }
 
-  vk::pad_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p);
+  vk::pad_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p, 0, g.Pz);
   launch_check(p, "pad");
   if (flat_init) {
     vk::fill_mean_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, nP, p->stats.p);
@@ -1581,6 +1601,35 @@ vk_status vk_rl_step_psf(int device, int rank, const uint64_t* shape, const floa
   return st;
 }
 
+// ---- single-volume slab decomposition ---------------------
+// The P domain is cut into z slabs; slab r owns P rows [z0, z1) and computes
+// on Q = [z0 - hb, z1 + ha) clipped to [0, Pz), hb = Kz-1-cz, ha = cz (the
+// reach of both correlations, deconv.cpp:40,126-130).  The convolution over Q
+// with zeros outside equals the full one on the owned rows once the halo rows
+// hold the neighbours' values; both exchanges (estimate before the forward
+// correlation, ratio before the backward one) happen in the x-transformed
+// spectrum S_A right after an x pass, because the x transform acts on each
+// (z, y) row alone.  The plan's image is the slab's own image rows.
+
+void slab_geometry(const uint64_t* shape3, const uint64_t* kshape3, int nslabs, int r, int* out) {
+  const int Kz = (int)kshape3[0], Iz = (int)shape3[0];
+  const int ozg = Kz / 2, Pz = Iz + 2 * ozg, cz = (Kz - 1) / 2;
+  const int hb = Kz - 1 - cz, ha = cz;
+  if (nslabs < 1 || r < 0 || r >= nslabs) fail(VK_ERR_ARG, "bad slab index");
+  const int z0 = (int)((long long)Pz * r / nslabs), z1 = (int)((long long)Pz * (r + 1) / nslabs);
+  const int q0 = std::max(0, z0 - hb), q1 = std::min(Pz, z1 + ha);
+  // own image rows (P row z <-> I row z - ozg)
+  const int i0 = std::max(0, z0 - ozg), i1 = std::min(Iz, z1 - ozg);
+  if (z1 - z0 < std::max(hb, ha) || i1 <= i0)
+    fail(VK_ERR_ARG, "too many slabs: each slab needs >= max(halo) P rows and one image row");
+  out[0] = z0;       // own P rows, global
+  out[1] = z1;
+  out[2] = q0;       // local domain, global P rows
+  out[3] = q1;
+  out[4] = i0;       // own image rows
+  out[5] = i1;
+}
+
 vk_status vk_conv_plan_create(int device, int rank, const uint64_t* shape, int kernel_rank,
                               const uint64_t* kernel_shape, const float* kernel, int circular, vk_rl_plan* out) {
   return guarded([&] {
@@ -1622,6 +1671,177 @@ vk_status vk_fft_convolve(int device, int rank, const uint64_t* shape, const flo
   vk_rl_plan_destroy(p);
   g_last_error = keep;
   return st;
+}
+
+vk_status vk_rl_slab_plan_create(int device, const uint64_t* shape, const uint64_t* psf_shape, const float* psf,
+                                 int nslabs, int slab, vk_rl_plan* out, vk_slab_info* info) {
+  return guarded([&] {
+    if (!shape || !psf_shape || !psf || !out) fail(VK_ERR_ARG, "NULL argument");
+    int gm[6];
+    slab_geometry(shape, psf_shape, nslabs, slab, gm);
+    const uint64_t local[3] = {(uint64_t)(gm[5] - gm[4]), shape[1], shape[2]};
+    const int ozg = (int)psf_shape[0] / 2;
+    const int zs[2] = {gm[3] - gm[2], gm[4] + ozg - gm[2]};
+    vk_rl_plan p = create_plan(device, 3, local, 3, psf_shape, psf, 1, 0, zs);
+    p->slab = true;
+    p->own0 = gm[0] - gm[2];
+    p->own1 = gm[1] - gm[2];
+    *out = p;
+    if (info) {
+      info->own_begin = gm[0];
+      info->own_end = gm[1];
+      info->domain_begin = gm[2];
+      info->domain_end = gm[3];
+      info->image_begin = gm[4];
+      info->image_end = gm[5];
+      info->halo_below = p->own0;
+      info->halo_above = (gm[3] - gm[2]) - p->own1;
+      info->spectrum = p->SA.p;
+      info->kx_planes = (uint64_t)p->g.Hx;
+      info->rows = (uint64_t)p->g.Pz;
+      info->row_elems = (uint64_t)p->g.Py;
+    }
+  });
+}
+
+vk_status vk_rl_slab_begin(vk_rl_plan p, const float* d_obs, double* stats, void* stream) {
+  return guarded([&] {
+    if (!p || !p->slab || !d_obs || !stats) fail(VK_ERR_ARG, "not a slab plan / NULL argument");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geom& g = p->g;
+    const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
+    p->launches = 0;
+    vk::ObsStats init{};
+    init.minbits = 0x7f800000u;
+    init.maxbits = 0u;
+    ck(cudaMemcpyAsync(p->stats.p, &init, sizeof(init), cudaMemcpyHostToDevice, s), "stats init");
+    vk::obs_stats_kernel<<<148 * 4, kThreads, 0, s>>>(d_obs, nI, p->stats.p);
+    launch_check(p, "obs_stats");
+    vk::pad_kernel<<<148 * 4, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p, p->own0, p->own1);
+    launch_check(p, "pad");
+    vk::ObsStats st{};
+    ck(cudaMemcpyAsync(&st, p->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s), "stats D2H");
+    ck(cudaStreamSynchronize(s), "stats");
+    float fmin, fmax;
+    std::memcpy(&fmin, &st.minbits, 4);
+    std::memcpy(&fmax, &st.maxbits, 4);
+    stats[0] = st.sr;
+    stats[1] = st.srr;
+    stats[2] = fmin;
+    stats[3] = fmax;
+    stats[4] = st.sump;
+    stats[5] = st.neg ? 1.0 : 0.0;
+    stats[6] = (double)nI;
+    stats[7] = (double)(p->own1 - p->own0) * g.Py * g.Px;
+  });
+}
+
+vk_status vk_rl_slab_start(vk_rl_plan p, int iters, int flat_init, double mean, void* stream) {
+  return guarded([&] {
+    if (!p || !p->slab) fail(VK_ERR_ARG, "not a slab plan");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geom& g = p->g;
+    ensure_iter_buffers(p, iters);
+    ck(cudaMemsetAsync(p->acc.p, 0, (size_t)iters * 4 * sizeof(double), s), "acc");
+    if (flat_init) {  // mean of the whole padded volume, evaluated in double then f32 (deconv.cpp:337-341)
+      vk::fill_value_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, (size_t)g.Pz * g.Py * g.Px, (float)mean);
+      launch_check(p, "fill");
+    }
+    x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr,
+           p->fx ? g.cx : 0);
+  });
+}
+
+vk_status vk_rl_slab_forward(vk_rl_plan p, const float* d_obs, int it, void* stream) {
+  return guarded([&] {
+    if (!p || !p->slab || !d_obs || it < 1 || it > p->acc_cap) fail(VK_ERR_ARG, "bad slab call");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geom& g = p->g;
+    conv_yz(p, s, p->otf.p);
+    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, p->acc.p + (size_t)(it - 1) * 4,
+           nullptr);
+  });
+}
+
+vk_status vk_rl_slab_backward(vk_rl_plan p, const float* d_obs, int it, float* d_out, void* stream) {
+  return guarded([&] {
+    if (!p || !p->slab || !d_obs || it < 1 || it > p->acc_cap) fail(VK_ERR_ARG, "bad slab call");
+    DeviceGuard dg(p->device);
+    cudaStream_t s = (cudaStream_t)stream;
+    const Geom& g = p->g;
+    conv_yz(p, s, p->otf_flip.p);
+    x_pass(p, s, d_out ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
+           p->acc.p + (size_t)(it - 1) * 4, d_out);
+  });
+}
+
+vk_status vk_rl_slab_crop(vk_rl_plan p, float* d_out, void* stream) {
+  return guarded([&] {
+    if (!p || !p->slab || !d_out) fail(VK_ERR_ARG, "bad slab call");
+    DeviceGuard dg(p->device);
+    vk::crop_kernel<<<148 * 4, kThreads, 0, (cudaStream_t)stream>>>(p->est.p, d_out, p->g);
+    launch_check(p, "crop");
+  });
+}
+
+// S_A rows [row, row + n) of every kx plane <-> a packed [Hx][n][Py] buffer,
+// or straight into another slab plan's rows (same device or a peer, UVA).
+void slab_rows_check(vk_rl_plan p, int row, int n) {
+  if (!p || !p->slab) fail(VK_ERR_ARG, "not a slab plan");
+  if (row < 0 || n < 0 || row + n > p->g.Pz) fail(VK_ERR_ARG, "slab rows out of range");
+}
+
+vk_status vk_rl_slab_pack(vk_rl_plan p, int row, int n, void* d_buf, void* stream) {
+  return guarded([&] {
+    slab_rows_check(p, row, n);
+    if (n == 0) return;
+    DeviceGuard dg(p->device);
+    const size_t w = (size_t)n * p->g.Py * sizeof(float2), pitch = (size_t)p->g.Pz * p->g.Py * sizeof(float2);
+    ck(cudaMemcpy2DAsync(d_buf, w, p->SA.p + (size_t)row * p->g.Py, pitch, w, p->g.Hx, cudaMemcpyDeviceToDevice,
+                         (cudaStream_t)stream),
+       "slab pack");
+  });
+}
+
+vk_status vk_rl_slab_unpack(vk_rl_plan p, int row, int n, const void* d_buf, void* stream) {
+  return guarded([&] {
+    slab_rows_check(p, row, n);
+    if (n == 0) return;
+    DeviceGuard dg(p->device);
+    const size_t w = (size_t)n * p->g.Py * sizeof(float2), pitch = (size_t)p->g.Pz * p->g.Py * sizeof(float2);
+    ck(cudaMemcpy2DAsync(p->SA.p + (size_t)row * p->g.Py, pitch, d_buf, w, w, p->g.Hx, cudaMemcpyDeviceToDevice,
+                         (cudaStream_t)stream),
+       "slab unpack");
+  });
+}
+
+vk_status vk_rl_slab_copy_rows(vk_rl_plan src, int src_row, vk_rl_plan dst, int dst_row, int n, void* stream) {
+  return guarded([&] {
+    slab_rows_check(src, src_row, n);
+    slab_rows_check(dst, dst_row, n);
+    if (src->g.Hx != dst->g.Hx || src->g.Py != dst->g.Py) fail(VK_ERR_SHAPE, "ShapeMismatch: slab planes differ");
+    if (n == 0) return;
+    DeviceGuard dg(dst->device);
+    const size_t w = (size_t)n * src->g.Py * sizeof(float2);
+    ck(cudaMemcpy2DAsync(dst->SA.p + (size_t)dst_row * dst->g.Py, (size_t)dst->g.Pz * dst->g.Py * sizeof(float2),
+                         src->SA.p + (size_t)src_row * src->g.Py, (size_t)src->g.Pz * src->g.Py * sizeof(float2), w,
+                         src->g.Hx, cudaMemcpyDefault, (cudaStream_t)stream),
+       "slab copy");
+  });
+}
+
+vk_status vk_rl_slab_sums(vk_rl_plan p, int iters, double* acc, void* stream) {
+  return guarded([&] {
+    if (!p || !p->slab || !acc || iters < 0 || iters > p->acc_cap) fail(VK_ERR_ARG, "bad slab call");
+    DeviceGuard dg(p->device);
+    ck(cudaMemcpyAsync(acc, p->acc.p, (size_t)iters * 4 * sizeof(double), cudaMemcpyDeviceToHost,
+                       (cudaStream_t)stream),
+       "acc D2H");
+    ck(cudaStreamSynchronize((cudaStream_t)stream), "acc");
+  });
 }
 
 }  // extern "C"
