@@ -40,6 +40,7 @@ FastEntry make_entry() {
 }
 
 const FastEntry kTable[] = {
+    make_entry<8, 8, 16, 16>(),    // 64 (FRC half grids, small z)
     make_entry<8, 12, 16, 16>(),   // 96
     make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8>(),  // 144 (z: 8 CTAs/SM)
     make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2>(),  // 192 (z: 48 regs, 5 CTAs/SM)

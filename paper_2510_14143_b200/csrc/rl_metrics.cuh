@@ -39,33 +39,100 @@ __global__ void frc_split_kernel(const float* __restrict__ est, Geom g, int hz, 
 
 // Ring sums over two half spectra laid out [Hx][Wz][Wy] (OTF layout).
 // bins: [3][nbins] = num, den_a, den_b.  Shared scratch: 3*nbins doubles.
+// A warp takes 32 consecutive elements (consecutive ky of one (kx, kz) row),
+// whose ring indices form runs; a segmented shuffle scan sums each run and
+// only its last lane adds to the shared histogram (FP64 shared atomics with
+// 32-way contention were the kernel's cost).
+// The ring index llround(nu / bin_freq) is first estimated in f32 (error
+// < 1e-4 of a ring); only values within 1e-3 of a half-integer are redone in
+// double exactly as the reference computes them.  Each block writes its
+// histogram to partial[blockIdx.x]; frc_bins_reduce adds the blocks in a
+// fixed order (deterministic sums).
+// slices: histogram copies in shared memory (warp w uses slice w % slices),
+// one per warp when they fit, to keep warps off each other's bins.
 __global__ void frc_bins_kernel(const float2* __restrict__ A, const float2* __restrict__ B, int Wz, int Wy, int Wx,
-                                int Hx, double bin_freq, int nbins, double* __restrict__ bins) {
-  extern __shared__ double hist[];
-  for (int i = threadIdx.x; i < 3 * nbins; i += blockDim.x) hist[i] = 0.0;
+                                int Hx, double bin_freq, int nbins, double* __restrict__ partial, int slices) {
+  extern __shared__ double hist[];  // [slices][3][nbins]
+  const int nw = slices;
+  for (int i = threadIdx.x; i < 3 * nbins * nw; i += blockDim.x) hist[i] = 0.0;
   __syncthreads();
-  const size_t n = (size_t)Hx * Wz * Wy;
-  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int ky = (int)(i % Wy);
-    const size_t t = i / Wy;
-    const int kz = (int)(t % Wz), kx = (int)(t / Wz);
-    const double fz = (double)min(kz, Wz - kz) / Wz;
-    const double fy = (double)min(ky, Wy - ky) / Wy;
-    const double fx = (double)min(kx, Wx - kx) / Wx;
-    const double nu = sqrt(fz * fz + fy * fy + fx * fx);
-    const long long bin = llround(nu / bin_freq);  // metrics.cpp:186-187
-    if (bin < nbins) {
-      const bool selfc = kx == 0 || ((Wx % 2 == 0) && 2 * kx == Wx);
-      const double w = selfc ? 1.0 : 2.0;
-      const float2 a = A[i], b = B[i];
-      atomicAdd(&hist[bin], w * ((double)a.x * b.x + (double)a.y * b.y));
-      atomicAdd(&hist[nbins + bin], w * ((double)a.x * a.x + (double)a.y * a.y));
-      atomicAdd(&hist[2 * nbins + bin], w * ((double)b.x * b.x + (double)b.y * b.y));
+  double* wh = hist + (size_t)((threadIdx.x >> 5) % slices) * 3 * nbins;
+  // work item = 32 consecutive ky of one (kx, kz) row: one division per item
+  const int cpr = (Wy + 31) / 32;
+  const int nitems = Hx * Wz * cpr;  // < 2^31 (checked by the host)
+  const int lane = threadIdx.x & 31;
+  const int warp = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5);
+  const int nwarps = (int)((gridDim.x * blockDim.x) >> 5);
+  const unsigned full = 0xffffffffu;
+  const float rz = 1.0f / Wz, ry = 1.0f / Wy, rx = 1.0f / Wx, rb = (float)(1.0 / bin_freq);
+  for (int item = warp; item < nitems; item += nwarps) {
+    const int row = item / cpr, ky = (item - row * cpr) * 32 + lane;
+    const int kx = row / Wz, kz = row - kx * Wz;
+    const size_t i = (size_t)row * Wy + ky;
+    int bin = -1;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0;
+    if (ky < Wy) {
+      const int mz = min(kz, Wz - kz), my = min(ky, Wy - ky), mx = min(kx, Wx - kx);
+      const float gz = mz * rz, gy = my * ry, gx = mx * rx;
+      const float xf = sqrtf(gz * gz + gy * gy + gx * gx) * rb;
+      long long b = (long long)(xf + 0.5f);
+      if (fabsf(xf - floorf(xf) - 0.5f) < 1e-3f) {  // near a tie: the reference's double path
+        const double fz = (double)mz / Wz, fy = (double)my / Wy, fx = (double)mx / Wx;
+        b = llround(sqrt(fz * fz + fy * fy + fx * fx) / bin_freq);  // metrics.cpp:186-187
+      }
+      if (b < nbins) {
+        bin = (int)b;
+        const bool selfc = kx == 0 || ((Wx % 2 == 0) && 2 * kx == Wx);
+        const double w = selfc ? 1.0 : 2.0;
+        const float2 a = A[i], c = B[i];
+        v0 = w * ((double)a.x * c.x + (double)a.y * c.y);
+        v1 = w * ((double)a.x * a.x + (double)a.y * a.y);
+        v2 = w * ((double)c.x * c.x + (double)c.y * c.y);
+      }
+    }
+    // runs of equal ring index -> segment ids
+    const int prevb = __shfl_up_sync(full, bin, 1);
+    const unsigned heads = __ballot_sync(full, lane == 0 || prevb != bin);
+    const int seg = __popc(heads & (lane == 31 ? full : ((2u << lane) - 1u)));
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const double u0 = __shfl_up_sync(full, v0, o), u1 = __shfl_up_sync(full, v1, o),
+                   u2 = __shfl_up_sync(full, v2, o);
+      const int s = __shfl_up_sync(full, seg, o);
+      if (lane >= o && s == seg) {
+        v0 += u0;
+        v1 += u1;
+        v2 += u2;
+      }
+    }
+    const int nextseg = __shfl_down_sync(full, seg, 1);
+    if (bin >= 0 && (lane == 31 || nextseg != seg)) {  // run tails: distinct bins except across the ky fold
+      atomicAdd(&wh[bin], v0);
+      atomicAdd(&wh[nbins + bin], v1);
+      atomicAdd(&wh[2 * nbins + bin], v2);
     }
   }
   __syncthreads();
-  for (int i = threadIdx.x; i < 3 * nbins; i += blockDim.x)
-    if (hist[i] != 0.0) atomicAdd(&bins[i], hist[i]);
+  for (int i = threadIdx.x; i < 3 * nbins; i += blockDim.x) {
+    double s = 0.0;
+    for (int w = 0; w < nw; ++w) s += hist[(size_t)w * 3 * nbins + i];
+    partial[(size_t)blockIdx.x * 3 * nbins + i] = s;
+  }
+}
+
+// One CTA per value: strided per-thread sums then a fixed-shape tree.
+__global__ void frc_bins_reduce(const double* __restrict__ partial, int nblocks, int nvals, double* __restrict__ bins) {
+  __shared__ double red[256];
+  const int i = blockIdx.x;
+  double s = 0.0;
+  for (int b = threadIdx.x; b < nblocks; b += blockDim.x) s += partial[(size_t)b * nvals + i];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = blockDim.x / 2; w > 0; w >>= 1) {
+    if (threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) bins[i] = red[0];
 }
 
 // Direct DFT along one axis, for FRC half extents that are not 5-smooth (the

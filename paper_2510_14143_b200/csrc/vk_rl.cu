@@ -173,6 +173,7 @@ size_t yz_smem(int N, int L) { return 2 * (size_t)N * (L + 1) * sizeof(float2); 
 
 constexpr size_t kSmemCap = 110 * 1024;  // two CTAs per SM
 constexpr int kThreads = 256;
+constexpr int kFrcBlocks = 148 * 6;  // FRC ring-sum blocks (per-block partials, fixed-order reduce)
 
 }  // namespace
 
@@ -214,7 +215,7 @@ struct vk_rl_plan_s {
   DevBuf<float> frc_even, frc_odd;
   DevBuf<double> frc_bins;
   double* h_frc = nullptr;  // pinned [3][nbins]
-  int frc_nbins = 0;
+  int frc_nbins = 0, frc_slices = 1;
   double frc_binf = 0;
   int frc_h[3]{1, 1, 1}, frc_s[3]{0, 0, 0};
   // non-5-smooth half extents: direct per-axis DFTs instead of the sub-plan
@@ -931,6 +932,17 @@ void setup_frc(vk_rl_plan p) {
   for (int a = 0; a < p->rank; ++a) nmax = std::max(nmax, half[a]);
   p->frc_binf = 1.0 / (double)nmax;  // ring_width / n_max (metrics.cpp:166-169)
   p->frc_nbins = (int)std::floor(0.5 / p->frc_binf) + 1;
+  if ((double)p->ishape[0] * p->ishape[p->rank > 1 ? 1 : 0] * 2 > 2e9)
+    fail(VK_ERR_UNSUPPORTED, "frc_resolution: image too large for the ring-sum kernel");
+  {  // per-warp ring histograms while they fit in shared memory, else fewer
+    const size_t one = (size_t)3 * p->frc_nbins * sizeof(double);
+    int sl = kThreads / 32;
+    while (sl > 1 && one * sl > 96 * 1024) sl >>= 1;
+    p->frc_slices = sl;
+    if (one * sl > 200 * 1024) fail(VK_ERR_UNSUPPORTED, "frc_resolution: image too large for the ring histogram");
+    ck(cudaFuncSetAttribute(vk::frc_bins_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)(one * sl)),
+       "frc smem");
+  }
   for (int a3 = 0; a3 < 3; ++a3) {
     const int a = a3 - (3 - p->rank);
     p->frc_h[a3] = a >= 0 ? (int)half[a] : 1;
@@ -955,7 +967,7 @@ void setup_frc(vk_rl_plan p) {
       ck(cudaMemcpy(p->frc_tw[a].p, tw.data(), n * sizeof(float2), cudaMemcpyHostToDevice), "frc twiddles");
     }
   }
-  p->frc_bins.alloc((size_t)3 * p->frc_nbins, "frc bins");
+  p->frc_bins.alloc((size_t)3 * p->frc_nbins * (1 + kFrcBlocks), "frc bins");  // [sums | per-block partials]
   ck(cudaMallocHost(&p->h_frc, (size_t)3 * p->frc_nbins * sizeof(double)), "frc pinned");
 }
 
@@ -964,7 +976,7 @@ void setup_frc(vk_rl_plan p) {
 double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
   vk_rl_plan_s* f = p->frc;
   const int nb = p->frc_nbins;
-  ck(cudaMemsetAsync(p->frc_bins.p, 0, (size_t)3 * nb * sizeof(double), s), "frc bins");
+
   vk::frc_split_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, p->g, p->frc_h[0], p->frc_h[1], p->frc_h[2],
                                                      p->frc_s[0], p->frc_s[1], p->frc_s[2], p->frc_even.p,
                                                      p->frc_odd.p);
@@ -987,17 +999,20 @@ double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
                                                            (long long)hz * hy, p->frc_tw[0].p);
       launch_check(p, "frc dft");
     }
-    vk::frc_bins_kernel<<<148 * 2, kThreads, (size_t)3 * nb * sizeof(double), s>>>(
-        p->frc_A.p, p->frc_B.p, hz, hy, hx, Hx, p->frc_binf, nb, p->frc_bins.p);
+    vk::frc_bins_kernel<<<kFrcBlocks, kThreads, (size_t)3 * nb * p->frc_slices * sizeof(double), s>>>(
+        p->frc_A.p, p->frc_B.p, hz, hy, hx, Hx, p->frc_binf, nb, p->frc_bins.p + 3 * nb, p->frc_slices);
     launch_check(p, "frc bins");
   } else {
     const vk::Geom& fg = f->g;
     spectrum3d(f, s, p->frc_even.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf.p);
     spectrum3d(f, s, p->frc_odd.p, fg.Pz, fg.Py, fg.Px, 1.0f, f->otf_flip.p);
-    vk::frc_bins_kernel<<<148 * 2, kThreads, (size_t)3 * nb * sizeof(double), s>>>(
-        f->otf.p, f->otf_flip.p, fg.Wz, fg.Wy, fg.Wx, fg.Hx, p->frc_binf, nb, p->frc_bins.p);
+    vk::frc_bins_kernel<<<kFrcBlocks, kThreads, (size_t)3 * nb * p->frc_slices * sizeof(double), s>>>(
+        f->otf.p, f->otf_flip.p, fg.Wz, fg.Wy, fg.Wx, fg.Hx, p->frc_binf, nb, p->frc_bins.p + 3 * nb,
+        p->frc_slices);
     launch_check(p, "frc bins");
   }
+  vk::frc_bins_reduce<<<3 * nb, 256, 0, s>>>(p->frc_bins.p + 3 * nb, kFrcBlocks, 3 * nb, p->frc_bins.p);
+  launch_check(p, "frc reduce");
   ck(cudaMemcpyAsync(p->h_frc, p->frc_bins.p, (size_t)3 * nb * sizeof(double), cudaMemcpyDeviceToHost, s),
      "frc D2H");
   ck(cudaStreamSynchronize(s), "frc");

@@ -167,6 +167,7 @@ FAST_CASES = {
     "xy2160_2d": ((2048, 2048), lambda: O.gaussian_psf((31, 31), 3.75)),            # W = 2160 x 2160 (C5 field)
     "c1_grid": ((64, 256, 256), lambda: O.gaussian_psf((15, 15, 15), 1.75)),        # W = 96 x 288 x 288
     "xy256": ((30, 196, 196), lambda: O.gaussian_psf((15, 31, 31), [2.0, 3.0, 3.0])),  # W = 60 x 256 x 256
+    "xyz64": ((44, 44, 44), lambda: O.gaussian_psf((11, 11, 11), 1.5)),             # W = 64 x 64 x 64
 }
 
 
