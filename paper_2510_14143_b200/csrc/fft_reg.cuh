@@ -210,7 +210,12 @@ __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
   }
 #pragma unroll 1
   for (int t = fresh_tid(); t < L * R1; t += NT) {
-    const int l = t % L, j = t / L;
+    // With 8 lines per block a half-warp spans two butterflies j; rows j and
+    // j+1 share a bank pair under the (L+1) pad, rows j and j+8 do not, so
+    // pair groups (2m, 2m+1) map to j = m and m+8 within each 16 butterflies.
+    const int l = t % L, g = t / L;
+    constexpr int G16 = (R1 / 16) * 16;
+    const int j = (L == 8 && LP == 9 && g < G16) ? ((g & ~15) | ((g >> 1) & 7) | ((g & 1) << 3)) : g;
     float2 v[R2];
     v[0] = buf[j * LP + l];
     static_for<1, R2>([&](auto r) {
