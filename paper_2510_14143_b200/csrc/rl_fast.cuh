@@ -41,6 +41,16 @@ __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
+// Group index of thread groups of L lanes, permuted so that the two groups
+// of a half-warp (2m, 2m+1) address rows m and m+8 (within each 16 groups)
+// when L = 8: rows one apart share a bank pair under the (L+1) pad, rows
+// eight apart do not (see reg::fft2 pass 2).  Bijective on [0, ngroups).
+template <int L>
+__device__ __forceinline__ int group_remap(int g, int ngroups) {
+  if (L == 8 && g < (ngroups / 16) * 16) return (g & ~15) | ((g >> 1) & 7) | ((g & 1) << 3);
+  return g;
+}
+
 template <int R1, int R2, int L, bool OTF_PREFETCH = false>
 struct FastCfg {
   static_assert((L & (L - 1)) == 0, "L must be a power of two (cheap line/index split)");
@@ -112,7 +122,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
       const float2* Sa = a.S + ((unsigned)z * g.Py + (va ? ya : 0));
       const float2* Sb = a.S + ((unsigned)z * g.Py + (vb ? yb : 0));
       const unsigned plane = (unsigned)g.Pz * g.Py;
-      for (int kx0 = threadIdx.x / L; kx0 < Hx; kx0 += KS * U) {
+      for (int kx0 = group_remap<L>(threadIdx.x / L, KS); kx0 < Hx; kx0 += KS * U) {
         float2 xa[U], xb[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
@@ -374,7 +384,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
     float2* Sa = a.S + ((unsigned)z * a.rows_y + y0 + l);
     float2* Sb = Sa + L;
     const unsigned plane = (unsigned)a.rows_z * a.rows_y;
-    for (int kx = threadIdx.x / L; kx < Hx; kx += KS) {
+    for (int kx = group_remap<L>(threadIdx.x / L, KS); kx < Hx; kx += KS) {
       const float2 zk = A[sw<L>(kx, l)];
       const float2 zn = A[sw<L>(kx == 0 ? 0 : N - kx, l)];
       const float2 xa = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
