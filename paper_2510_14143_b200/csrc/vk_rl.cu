@@ -813,6 +813,10 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     const size_t sa = (size_t)g.Hx * std::max(g.Pz, p->Kz) * std::max(g.Py, p->Ky);
     const size_t sb = (size_t)g.Hx * std::max(g.Pz, p->Kz) * g.Wy;
     const size_t so = (size_t)g.Hx * g.Wz * g.Wy;
+    // the pass kernels index spectra and the padded domain with 32-bit offsets
+    if (so >= (1ull << 32) || sb >= (1ull << 32) || (size_t)g.Pz * g.Py * g.Px >= (1ull << 32))
+      fail(VK_ERR_UNSUPPORTED, "volume too large for one plan (spectrum >= 2^32 elements): split it into slabs "
+                               "(vk_rl_slab_plan_create)");
     p->SA.alloc(sa, "spectrum A");
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
     p->otf.alloc(so, "otf");
