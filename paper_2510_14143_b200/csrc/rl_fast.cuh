@@ -81,7 +81,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
   pdl_trigger();
   if (!TWG) reg::load_twiddles2<R1, R2>(smem, a.plan.tw);  // constant table: before the wait
   pdl_wait();
-  const int z = blockIdx.y;
+  const int z = blockIdx.y + a.zoff;
   const int y0 = blockIdx.x * 2 * L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Geom& g = a.g;
@@ -414,7 +414,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   for (int l = 0; l < L; ++l) {
     const int line = line0 + l;
     const bool ok = line < a.nlines;
-    const float2* in = a.in + (size_t)(ok ? line : 0) * a.in_pitch;
+    const float2* in = a.in + (size_t)(ok ? y_line(a, line) : 0) * a.in_pitch;
     for (int i = threadIdx.x; i < N; i += NT) {
       if (ok && i < a.n_in)
         cp_async8(&A[sw<L>(i, l)], &in[i]);
@@ -467,7 +467,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT)
   for (int l = 0; l < L; ++l) {
     const int line = line0 + l;
     if (line >= a.nlines) break;
-    float2* out = a.out + (size_t)line * a.out_pitch;
+    float2* out = a.out + (size_t)y_line(a, line) * a.out_pitch;
     for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[sw<L>(j + a.out_off, l)];
   }
 }

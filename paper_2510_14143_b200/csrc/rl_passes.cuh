@@ -64,6 +64,7 @@ struct XArgs {
   const float* obs;     // [Iz][Iy][Ix]
   double* acc;          // RATIO: acc[0] += LL ; UPDATE: acc[1..3] += sx, sxx, sxr
   float* out;           // UPDATE_LAST: cropped f32 estimate [Iz][Iy][Ix]
+  int zoff;             // first z row of this launch (z-chunked iterations)
 };
 
 struct YArgs {
@@ -76,7 +77,17 @@ struct YArgs {
   const float2* in;
   float2* out;
   const float2* otf;    // CONV: otf[line * N + k]
+  // z-chunked passes (zcn > 0): the nlines = Hx * zcn lines are (kx, z) with
+  // z in [zc0, zc0 + zcn) of zrows rows per kx plane
+  int zc0, zcn, zrows;
 };
+
+// Global line of a pass-local line index (identity unless z-chunked).
+__device__ __forceinline__ int y_line(const YArgs& a, int local) {
+  if (a.zcn == 0) return local;
+  const int kx = local / a.zcn;
+  return kx * a.zrows + a.zc0 + (local - kx * a.zcn);
+}
 
 struct ZArgs {
   LinePlan plan;
@@ -142,7 +153,7 @@ __global__ void __launch_bounds__(256) xpass_kernel(const XArgs a) {
   const int L = a.L, LP = L + 1, Wx = a.g.Wx, Hx = a.g.Hx;
   float2* A = smem;
   float2* B = smem + Wx * LP;  // B also stages Hx*2L (host sizes it as max of both)
-  const int z = blockIdx.y;
+  const int z = blockIdx.y + a.zoff;
   const int y0 = blockIdx.x * 2 * L;
 
   if (a.mode == XM_FWD) {
@@ -260,7 +271,7 @@ __global__ void __launch_bounds__(256) ypass_kernel(const YArgs a) {
     const int l = idx / N, i = idx - l * N;
     const int line = line0 + l;
     float2 v = make_float2(0.f, 0.f);
-    if (line < a.nlines && i < a.n_in) v = a.in[(size_t)line * a.in_pitch + i];
+    if (line < a.nlines && i < a.n_in) v = a.in[(size_t)y_line(a, line) * a.in_pitch + i];
     A[i * LP + l] = v;
   }
   __syncthreads();
@@ -282,7 +293,7 @@ __global__ void __launch_bounds__(256) ypass_kernel(const YArgs a) {
   for (int idx = threadIdx.x; idx < L * a.n_out; idx += blockDim.x) {
     const int l = idx / a.n_out, j = idx - l * a.n_out;
     const int line = line0 + l;
-    if (line < a.nlines) a.out[(size_t)line * a.out_pitch + j] = R[(j + a.out_off) * LP + l];
+    if (line < a.nlines) a.out[(size_t)y_line(a, line) * a.out_pitch + j] = R[(j + a.out_off) * LP + l];
   }
 }
 

@@ -206,6 +206,9 @@ struct vk_rl_plan_s {
   DevBuf<int> df_ctr;
   size_t df_window = 0;
   int zpipe_blocks = 0;  // > 0: persistent double-buffered z convolution
+  // z-chunked iterations (3D fast plans): y_inv -> x pass -> y_fwd per chunk
+  // of zchunk rows, so the chunk's spectrum rows stay in L2 between passes
+  int zchunk = 0;
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
   int cl_clusters = 0;
@@ -344,9 +347,12 @@ void launch(const void* k, dim3 grid, int nt, size_t smem, cudaStream_t s, void*
   ck(cudaLaunchKernelExC(&cfg, k, args), "launch");
 }
 
+// zoff / nz: z rows [zoff, zoff + nz) only (z-chunked iterations; nz < 0 = all)
 void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z, int rows_y, int len,
-            float scale, float* est, const float* obs, double* acc, float* out, int xoff = 0) {
+            float scale, float* est, const float* obs, double* acc, float* out, int xoff = 0, int zoff = 0,
+            int nz = -1) {
   vk::XArgs a{};
+  a.zoff = zoff;
   a.plan = p->lpx;
   a.g = p->g;
   a.mode = mode;
@@ -362,7 +368,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   a.obs = obs;
   a.acc = acc;
   a.out = out;
-  dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), rows_z);
+  dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
   if (p->fx)
@@ -373,9 +379,15 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   prof_end(p, s, kind, t);
 }
 
+// zcn > 0: only the lines (kx, z) with z in [zc0, zc0 + zcn) of zrows per kx
+// plane (nlines is then Hx * zcn)
 void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in_pitch, int n_out,
-            int out_pitch, int out_off, const float2* in, float2* out, const float2* otf) {
+            int out_pitch, int out_off, const float2* in, float2* out, const float2* otf, int zc0 = 0, int zcn = 0,
+            int zrows = 0) {
   vk::YArgs a{};
+  a.zc0 = zc0;
+  a.zcn = zcn;
+  a.zrows = zrows;
   a.plan = p->lpy;
   a.mode = mode;
   a.L = p->fy ? p->fy->Lx : p->yL;
@@ -521,6 +533,23 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
   y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, g.cy, p->SB.p, p->SA.p, nullptr);
+}
+
+// One half-iteration of the z-chunked schedule: z convolution of the whole
+// volume, then per chunk of z rows: y inverse -> x pass (mode) -> y forward
+// (skipped when `last`).  The chunk's S_A / S_B rows written by one pass are
+// read by the next while still in L2.
+void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, float* est, const float* obs,
+                  double* acc, float* out, bool fwd_after) {
+  const Geom& g = p->g;
+  z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
+  for (int z0 = 0; z0 < g.Pz; z0 += p->zchunk) {
+    const int zn = std::min(p->zchunk, g.Pz - z0);
+    y_pass(p, s, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, g.cy, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
+    x_pass(p, s, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, acc, out, 0, z0, zn);
+    if (fwd_after)
+      y_pass(p, s, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
+  }
 }
 
 // Full r2c spectrum [Hx][Wz][Wy] of a real block [rz][ry][rx] corner-embedded
@@ -793,6 +822,15 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
         ck(cudaMemcpy(p->twy2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
         p->lpy.tw2 = p->twy2.p;
       }
+    }
+    // z-chunked schedule: opt-in (VK_RL_ZCHUNK=rows).  Measured slower at C2
+    // (rows 8/16/24/40: 2.49/1.80/1.76/1.48 vs 1.25 ms per iteration,
+    // profiles/r01/final/zchunk.log): the L2 reuse does not pay for
+    // launches that no longer fill the GPU.
+    const char* zc = std::getenv("VK_RL_ZCHUNK");
+    if (zc && p->fx && p->fy && p->fz && g.Wz > 1 && !p->df && !p->cl && !conv && !zslab) {
+      const int rows = std::atoi(zc);
+      p->zchunk = rows > 0 && rows < g.Pz ? rows : 0;
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
@@ -1180,6 +1218,9 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
   x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr,
          p->fx ? g.cx : 0);
+  const bool chunked = p->zchunk > 0;
+  if (chunked)  // the chunked schedule enters each iteration at the z convolution
+    y_pass(p, s, vk::YM_FWD, g.Hx * g.Pz, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
 
   // Early stop is only possible from iteration patience+1 on (fails counts
   // from iteration 2); before that no host round-trip is needed.
@@ -1191,14 +1232,20 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   ck(cudaEventRecord(p->events[0], s), "event");
   for (int it = 1; it <= iters; ++it) {
     double* acc = p->acc.p + (size_t)(it - 1) * 4;
-    conv_yz(p, s, p->otf.p);
-    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc, nullptr);
-    conv_yz(p, s, p->otf_flip.p);
     // the last iteration writes the cropped output directly unless a metric
     // still needs the updated estimate
     const bool last = it == iters && !frc && !ssim;
-    x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc,
-           last ? d_out : nullptr);
+    if (chunked) {
+      chunked_half(p, s, p->otf.p, vk::XM_RATIO, p->est.p, d_obs, acc, nullptr, true);
+      chunked_half(p, s, p->otf_flip.p, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, p->est.p, d_obs, acc,
+                   last ? d_out : nullptr, it < iters);
+    } else {
+      conv_yz(p, s, p->otf.p);
+      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc, nullptr);
+      conv_yz(p, s, p->otf_flip.p);
+      x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
+             acc, last ? d_out : nullptr);
+    }
     if (frc) values.push_back(frc_eval(p, s, spacing));  // syncs: the value is needed on the host
     if (ssim) ssim_eval(p, s, it, d_obs);
     ck(cudaEventRecord(p->events[it], s), "event");
@@ -1449,6 +1496,7 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
            ",l2_window=" + std::to_string(p->df_window) + ")";
     else
       s += g.Wz > 1 ? "3-pass" : "y-conv";
+    if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
     buf[len - 1] = 0;
   });
