@@ -12,7 +12,8 @@ struct FastEntry {
   bool pdl;             // launch with programmatic dependent launch
   size_t smem_xp;       // x-pass
   size_t smem_yp;       // y-pass FWD/INV
-  int Lx, NTx;          // x-pass and y-pass: lines per CTA, threads
+  int Lx, NTx;          // x-pass: lines per CTA, threads
+  int Ly, NTy;          // y-pass
   size_t smem_x;        // x-pass, and y-pass FWD/INV
   size_t smem_yconv;    // y-pass CONV (adds the prefetched OTF tile)
   const void* xk;       // xpass_fast<R1,R2,Lx>(XArgs)

@@ -14,8 +14,9 @@ namespace {
 // TWG / YPREF / XMINB / XPB: x and y pass variants (rl_fast.cuh); ZTWG /
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
-          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2>
+          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0>
 FastEntry make_entry() {
+  constexpr int LY = LY0 ? LY0 : LX;  // y-pass lines per CTA (default: the x pass's)
   FastEntry e{};
   e.N = R1 * R2;
   e.pdl = PDL;
@@ -24,11 +25,13 @@ FastEntry make_entry() {
   e.Lx = LX;
   e.NTx = FastCfg<R1, R2, LX>::NT;
   e.smem_x = FastCfg<R1, R2, LX>::smem;
-  e.smem_yp = e.smem_xp;
-  e.smem_yconv = (size_t)(FastCfg<R1, R2, LX, true>::DATA + (TWG ? 0 : R1 * R2) + (YPREF ? R1 * R2 * LX : 0)) *
+  e.Ly = LY;
+  e.NTy = FastCfg<R1, R2, LY, true>::NT;
+  e.smem_yp = (size_t)(FastCfg<R1, R2, LY, true>::DATA + (TWG ? 0 : R1 * R2)) * sizeof(float2);
+  e.smem_yconv = (size_t)(FastCfg<R1, R2, LY, true>::DATA + (TWG ? 0 : R1 * R2) + (YPREF ? R1 * R2 * LY : 0)) *
                  sizeof(float2);
   e.xk = (const void*)xpass_fast<R1, R2, LX, TWG, XMINB, XPB>;
-  e.yk = (const void*)ypass_fast<R1, R2, LX, TWG, YPREF>;
+  e.yk = (const void*)ypass_fast<R1, R2, LY, TWG, YPREF>;
   e.Lz = LZ;
   e.NTz = FastCfg<R1, R2, LZ, true>::NT;
   e.smem_z = (size_t)(FastCfg<R1, R2, LZ, true>::DATA + (ZTWG ? 0 : R1 * R2) + (ZPREF ? R1 * R2 * LZ : 0)) *
@@ -46,12 +49,12 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2>(),  // 192 (z: 48 regs, 5 CTAs/SM)
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM
-    make_entry<30, 36, 8, 4, false, true, 1, true>(),  // 1080 (Ix = 1000: partial chunks are common)
+    make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM (y L=4: slower)
+    make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4>(),  // 1080 (Ix = 1000: partial chunks are common)
     // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
     // in griddepcontrol.wait would hold the scarce slots the batch lanes'
     // kernels need: C5 3.05e10 without vs 2.66e10 with, profiles/r01/pdl.log)
-    make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false>(),
+    make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false, 2, 2>(),  // y L=2
 };
 
 }  // namespace

@@ -390,7 +390,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   a.zrows = zrows;
   a.plan = p->lpy;
   a.mode = mode;
-  a.L = p->fy ? p->fy->Lx : p->yL;
+  a.L = p->fy ? p->fy->Ly : p->yL;
   a.nlines = nlines;
   a.n_in = n_in;
   a.in_pitch = in_pitch;
@@ -404,7 +404,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
   if (p->fy)
-    launch(p->fy->yk, grid, p->fy->NTx, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
+    launch(p->fy->yk, grid, p->fy->NTy, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
            p->fy->pdl);
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
@@ -1485,7 +1485,7 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
     };
     std::string s = "W=" + std::to_string(g.Wz) + "x" + std::to_string(g.Wy) + "x" + std::to_string(g.Wx) +
                     " P=" + std::to_string(g.Pz) + "x" + std::to_string(g.Py) + "x" + std::to_string(g.Px) + " " +
-                    axis("x", p->fx, p->fx ? p->fx->Lx : p->xL) + " " + axis("y", p->fy, p->fy ? p->fy->Lx : p->yL) +
+                    axis("x", p->fx, p->fx ? p->fx->Lx : p->xL) + " " + axis("y", p->fy, p->fy ? p->fy->Ly : p->yL) +
                     " " + axis("z", p->fz, p->fz ? p->fz->Lz : p->zL) + " yz:";
     if (p->cl)
       s += "cluster(C=" + std::to_string(p->cl->C) + ",clusters=" + std::to_string(p->cl_clusters) +
