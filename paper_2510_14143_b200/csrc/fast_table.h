@@ -3,9 +3,18 @@
 #include <cuda_runtime.h>
 #include <stddef.h>
 
+#include <cuda.h>  // CUtensorMap (TMA descriptors)
+
 #include "rl_passes.cuh"
 
 namespace vk {
+
+// Kernel argument of zpass_tma: the S_B tensor map (param space, 64-byte
+// aligned, __grid_constant__) and the usual z-pass arguments.
+struct alignas(64) ZTmaArgs {
+  CUtensorMap map;  // S: dims {Wy, zrows, Hx}, box {16, Pz, 1}, 8-byte elements
+  ZArgs z;
+};
 
 struct FastEntry {
   int N, R1;            // N = R1 * R2 (pass-1 / pass-2 radices)
@@ -23,6 +32,8 @@ struct FastEntry {
   const void* zk;       // zpass_fast<R1,R2,Lz>(ZArgs)
   size_t smem_zp;
   const void* zpk;      // zpass_pipe<R1,R2,Lz>(ZArgs): persistent, double-buffered
+  const void* ztk;      // zpass_tma<R1,R2>(ZTmaArgs): TMA-staged column tile (Lz = 16), or nullptr
+  size_t smem_zt;
 };
 
 const FastEntry* fast_lookup(int n);

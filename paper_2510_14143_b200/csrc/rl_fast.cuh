@@ -552,6 +552,97 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT, MINB == 1 ? 0 : 
   }
 }
 
+// ---- z convolution with a TMA-staged column tile --------------------------
+// The (ky block of 16) x (Pz rows) column tile of kx plane `kx` is one
+// cp.async.bulk.tensor.3d load (box {16, Pz, 1} of the tensor
+// [Hx][zrows][Wy] complex64, 8-byte elements) into a dense [z][16] shared
+// tile, completion tracked by an mbarrier; the transform then runs on the
+// unpadded layout (16-lane rows cover all 32 banks, so the (L+1) pad is not
+// needed at L = 16).  Rows Pz..N-1 are zeroed by the other threads while the
+// copy flies.  The OTF is read from global in the multiply.
+// (ZTmaArgs: fast_table.h)
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(smem_dst)),
+      "l"(map), "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
+template <int R1, int R2, bool TWG, int MINB>
+__global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 : MINB)
+    zpass_tma(const __grid_constant__ ZTmaArgs ta) {
+  constexpr int L = 16;
+  using C = FastCfg<R1, R2, L, true>;
+  constexpr int N = C::N, NT = C::NT;
+  constexpr int ZS = NT / L;
+  constexpr int IT = (N + ZS - 1) / ZS;
+  const ZArgs& a = ta.z;
+  extern __shared__ __align__(128) float2 smem[];
+  float2* tw = TWG ? nullptr : smem;
+  float2* A = TWG ? smem : smem + N;  // dense [z][16]; N*16*8 B, 128-B aligned (N multiple of 8)
+  __shared__ uint64_t bar;
+  const int kx = blockIdx.y, ky0 = blockIdx.x * L;
+  const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
+  const int ky = ky0 + l;
+  const bool kok = ky < a.Wy;
+  const unsigned Wy = a.Wy;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  const float2* twp = TWG ? a.plan.tw2 : tw;
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, (unsigned)(a.n_in * L * sizeof(float2)));
+    tma_load_3d(A, &ta.map, &bar, ky0, 0, kx);
+  }
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {  // zero padding rows, disjoint from the copy
+    const int z = z0 + k * ZS;
+    if (z < N && z >= a.n_in) A[z * L + l] = make_float2(0.f, 0.f);
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  reg::fft2<R1, R2, L, NT, false, L, TWG>(A, twp);
+  const float2* og = a.otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
+#pragma unroll
+  for (int k = 0; k < IT; ++k) {
+    const int z = z0 + k * ZS;
+    if (z < N) A[z * L + l] = cmul(A[z * L + l], kok ? __ldg(&og[(unsigned)z * Wy]) : make_float2(0.f, 0.f));
+  }
+  __syncthreads();
+  reg::fft2<R1, R2, L, NT, true, L, TWG>(A, twp);
+  if (kok) {
+    float2* col = a.S + ((unsigned)kx * a.zrows * Wy + ky);
+    for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[(z + a.out_off) * L + l];
+  }
+}
+
 // Persistent, double-buffered z convolution: each CTA walks tiles
 // (kx, ky-chunk) with stride gridDim.x and keeps the NEXT tile's column block
 // (and, with PREF, its OTF block) in flight (cp.async group) while it

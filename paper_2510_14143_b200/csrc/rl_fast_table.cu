@@ -14,7 +14,8 @@ namespace {
 // TWG / YPREF / XMINB / XPB: x and y pass variants (rl_fast.cuh); ZTWG /
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
-          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0>
+          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0,
+          bool ZTMA = false>
 FastEntry make_entry() {
   constexpr int LY = LY0 ? LY0 : LX;  // y-pass lines per CTA (default: the x pass's)
   FastEntry e{};
@@ -39,6 +40,10 @@ FastEntry make_entry() {
   e.zk = (const void*)zpass_fast<R1, R2, LZ, ZTWG, ZPREF, ZMINB>;
   e.smem_zp = ZPipeCfg<R1, R2, LZ, ZTWG, ZPREF>::smem;
   e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
+  if constexpr (ZTMA && LZ == 16) {
+    e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZMINB>;
+    e.smem_zt = (size_t)(R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);
+  }
   return e;
 }
 
@@ -46,7 +51,7 @@ const FastEntry kTable[] = {
     make_entry<8, 8, 16, 16>(),    // 64 (FRC half grids, small z)
     make_entry<8, 12, 16, 16>(),   // 96
     make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8>(),  // 144 (z: 8 CTAs/SM)
-    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2>(),  // 192 (z: 48 regs, 5 CTAs/SM)
+    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 0, true>(),  // 192 (z: 48 regs, 5 CTAs/SM; TMA tile)
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
     make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM (y L=4: slower)
@@ -117,6 +122,8 @@ cudaError_t fast_init_attributes() {
     if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yconv))) return r;
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
     if ((r = cudaFuncSetAttribute(e.zpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zp))) return r;
+    if (e.ztk && (r = cudaFuncSetAttribute(e.ztk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zt)))
+      return r;
     // prefer the full shared-memory carveout: occupancy is smem-limited
     for (const void* k : {e.xk, e.yk, e.zk, e.zpk})
       if ((r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100))) return r;

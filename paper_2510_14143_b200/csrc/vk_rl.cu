@@ -209,6 +209,9 @@ struct vk_rl_plan_s {
   // z-chunked iterations (3D fast plans): y_inv -> x pass -> y_fwd per chunk
   // of zchunk rows, so the chunk's spectrum rows stay in L2 between passes
   int zchunk = 0;
+  // TMA descriptor of S_B for the z convolution (zpass_tma), when available
+  bool ztma = false;
+  CUtensorMap zmap{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
   int cl_clusters = 0;
@@ -427,6 +430,17 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
   a.otf = otf;
   a.otf_out = otf_out;
   a.hx = p->g.Hx;
+  if (p->fz && p->ztma && mode == vk::ZM_CONV && S == p->SB.p && zrows == p->g.Pz && n_in == p->g.Pz) {
+    vk::ZTmaArgs ta{};
+    ta.map = p->zmap;
+    ta.z = a;
+    dim3 grid((p->g.Wy + 15) / 16, p->g.Hx);
+    const size_t t = prof_begin(p, s);
+    launch(p->fz->ztk, grid, p->fz->NTz, p->fz->smem_zt, s, &ta, p->fz->pdl);
+    launch_check(p, "zpass tma");
+    prof_end(p, s, VK_KIND_Z_CONV, t);
+    return;
+  }
   if (p->fz && p->zpipe_blocks && mode == vk::ZM_CONV) {
     const size_t t = prof_begin(p, s);
     launch(p->fz->zpk, dim3(p->zpipe_blocks), p->fz->NTz, p->fz->smem_zp, s, &a, p->fz->pdl);
@@ -631,6 +645,32 @@ void setup_dataflow(vk_rl_plan p) {
     p->df_window = std::min<size_t>(bytes, (size_t)max_window);
     cudaGetLastError();
   }
+}
+
+// cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda):
+// S_B as a 3D tensor {Wy, zrows, Hx} of 8-byte elements, box {16, Pz, 1}.
+bool encode_zmap(vk_rl_plan p, int zrows) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  static EncodeFn fn = [] {
+    void* f = nullptr;
+    cudaDriverEntryPointQueryResult q{};
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+        q != cudaDriverEntryPointSuccess)
+      f = nullptr;
+    cudaGetLastError();
+    return (EncodeFn)f;
+  }();
+  if (!fn) return false;
+  const Geom& g = p->g;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.Wy, (cuuint64_t)zrows, (cuuint64_t)g.Hx};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.Wy * 8, (cuuint64_t)zrows * g.Wy * 8};
+  const cuuint32_t box[3] = {16, (cuuint32_t)g.Pz, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return fn(&p->zmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, p->SB.p, dims, strides, box, estr,
+            CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+            CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
 void to3(int rank, const uint64_t* in, uint64_t* out3) {
@@ -857,6 +897,13 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
                                "(vk_rl_slab_plan_create)");
     p->SA.alloc(sa, "spectrum A");
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
+    // TMA-staged z tile (zpass_tma): opt-in.  Parity-green but slower at C2
+    // (0.386 vs 0.345 ms per iteration for the two z convolutions,
+    // profiles/r01/final/tma.log): one thread's bulk copy plus an mbarrier
+    // spin per CTA does not beat 256 threads' cp.async at this tile size.
+    const char* tma = std::getenv("VK_RL_TMA");
+    if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && tma && tma[0] == '1')
+      p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     p->otf.alloc(so, "otf");
     if (!conv) p->otf_flip.alloc(so, "otf_flip");
     p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
@@ -1497,6 +1544,7 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
     else
       s += g.Wz > 1 ? "3-pass" : "y-conv";
     if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
+    if (p->ztma) s += " z:tma";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
     buf[len - 1] = 0;
   });
