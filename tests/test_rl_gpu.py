@@ -243,6 +243,21 @@ def test_fused_yz_conv_matches_three_pass(name, shape, mk):
     assert rel_l2(r1.estimate, its[0]) <= TOL_1
 
 
+def test_opt_in_schedules_match_default():
+    """The opt-in variants kept for measurement: TMA-staged z tile
+    (VK_RL_TMA), pipelined z (VK_RL_ZPIPE) and the z-chunked schedule
+    (VK_RL_ZCHUNK) against the default path on a 192-point z grid."""
+    psf = O.gaussian_psf((15, 15, 15), 1.75)
+    obs = synth.blurred(synth.blobs((160, 256, 256), 60, 5, 9, seed=12), psf)  # W = 192 x 288 x 288
+    rule = fixed_rule(3)
+    ref = vk.richardson_lucy(obs, psf, rule)
+    for env, tag in (({"VK_RL_TMA": "1"}, "z:tma"), ({"VK_RL_ZPIPE": "1"}, None), ({"VK_RL_ZCHUNK": "24"}, "zchunk")):
+        got = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule))
+        assert rel_l2(got.estimate, ref.estimate) <= 1e-6, env
+        if tag:
+            assert tag in _with_env(env, lambda: vk.RlPlan(obs.shape, psf)).describe()
+
+
 def test_frc_default_rule_c1():
     """The reference's DEFAULT rule (frc_resolution, 1e-3, patience 3) on the
     C1 shape: per-iteration FRC resolution on the device vs the oracle's
