@@ -598,7 +598,11 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   constexpr int N = C::N, NT = C::NT;
   constexpr int ZS = NT / L;
   constexpr int IT = (N + ZS - 1) / ZS;
-  const ZArgs& a = ta.z;
+  // scalar fields straight from param space (a reference to the struct would
+  // force a local copy)
+  const int n_in = ta.z.n_in, n_out = ta.z.n_out, out_off = ta.z.out_off, zrows = ta.z.zrows;
+  float2* const S = ta.z.S;
+  const float2* const otf = ta.z.otf;
   extern __shared__ __align__(128) float2 smem[];
   float2* tw = TWG ? nullptr : smem;
   float2* A = TWG ? smem : smem + N;  // dense [z][16]; N*16*8 B, 128-B aligned (N multiple of 8)
@@ -606,30 +610,30 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   const int kx = blockIdx.y, ky0 = blockIdx.x * L;
   const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
   const int ky = ky0 + l;
-  const bool kok = ky < a.Wy;
-  const unsigned Wy = a.Wy;
+  const unsigned Wy = ta.z.Wy;
+  const bool kok = ky < (int)Wy;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
-  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
-  const float2* twp = TWG ? a.plan.tw2 : tw;
+  if (!TWG) reg::load_twiddles2<R1, R2>(tw, ta.z.plan.tw);
+  const float2* twp = TWG ? ta.z.plan.tw2 : tw;
   __syncthreads();
   pdl_trigger();
   pdl_wait();
   if (threadIdx.x == 0) {
-    mbar_expect_tx(&bar, (unsigned)(a.n_in * L * sizeof(float2)));
+    mbar_expect_tx(&bar, (unsigned)(n_in * L * sizeof(float2)));
     tma_load_3d(A, &ta.map, &bar, ky0, 0, kx);
   }
 #pragma unroll
   for (int k = 0; k < IT; ++k) {  // zero padding rows, disjoint from the copy
     const int z = z0 + k * ZS;
-    if (z < N && z >= a.n_in) A[z * L + l] = make_float2(0.f, 0.f);
+    if (z < N && z >= n_in) A[z * L + l] = make_float2(0.f, 0.f);
   }
   mbar_wait(&bar, 0);
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false, L, TWG>(A, twp);
-  const float2* og = a.otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
+  const float2* og = otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
 #pragma unroll
   for (int k = 0; k < IT; ++k) {
     const int z = z0 + k * ZS;
@@ -638,8 +642,8 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true, L, TWG>(A, twp);
   if (kok) {
-    float2* col = a.S + ((unsigned)kx * a.zrows * Wy + ky);
-    for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[(z + a.out_off) * L + l];
+    float2* col = S + ((unsigned)kx * zrows * Wy + ky);
+    for (int z = z0; z < n_out; z += ZS) col[(unsigned)z * Wy] = A[(z + out_off) * L + l];
   }
 }
 

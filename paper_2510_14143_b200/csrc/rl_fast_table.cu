@@ -15,7 +15,7 @@ namespace {
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
           bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0,
-          bool ZTMA = false>
+          int ZTMA = 0>  // ZTMA: resident-CTA floor of the TMA z kernel (0 = no TMA variant)
 FastEntry make_entry() {
   constexpr int LY = LY0 ? LY0 : LX;  // y-pass lines per CTA (default: the x pass's)
   FastEntry e{};
@@ -40,8 +40,8 @@ FastEntry make_entry() {
   e.zk = (const void*)zpass_fast<R1, R2, LZ, ZTWG, ZPREF, ZMINB>;
   e.smem_zp = ZPipeCfg<R1, R2, LZ, ZTWG, ZPREF>::smem;
   e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
-  if constexpr (ZTMA && LZ == 16) {
-    e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZMINB>;
+  if constexpr (ZTMA > 0 && LZ == 16) {
+    e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;
     e.smem_zt = (size_t)(R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);
   }
   return e;
@@ -49,9 +49,9 @@ FastEntry make_entry() {
 
 const FastEntry kTable[] = {
     make_entry<8, 8, 16, 16>(),    // 64 (FRC half grids, small z)
-    make_entry<8, 12, 16, 16>(),   // 96
-    make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8>(),  // 144 (z: 8 CTAs/SM)
-    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 0, true>(),  // 192 (z: 48 regs, 5 CTAs/SM; TMA tile)
+    make_entry<8, 12, 16, 16, false, true, 1, false, false, true, 1, true, 2, 0, 6>(),   // 96 (z: TMA 6)
+    make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8, true, 2, 0, 6>(),  // 144 (z: 8 CTAs/SM; TMA 6)
+    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 0, 4>(),  // 192 (z: TMA tile, 4 CTAs/SM)
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
     make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM (y L=4: slower)

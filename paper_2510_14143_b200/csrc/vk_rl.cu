@@ -897,12 +897,11 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
                                "(vk_rl_slab_plan_create)");
     p->SA.alloc(sa, "spectrum A");
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
-    // TMA-staged z tile (zpass_tma): opt-in.  Parity-green but slower at C2
-    // (0.386 vs 0.345 ms per iteration for the two z convolutions,
-    // profiles/r01/final/tma.log): one thread's bulk copy plus an mbarrier
-    // spin per CTA does not beat 256 threads' cp.async at this tile size.
-    const char* tma = std::getenv("VK_RL_TMA");
-    if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && tma && tma[0] == '1')
+    // TMA-staged z tile (zpass_tma) where the length has one and the box
+    // fits (Pz <= 256): C2 z convolutions 0.313 vs 0.345 ms per iteration
+    // with cp.async (profiles/r01/final/tma.log).  VK_RL_NO_TMA=1 disables.
+    const char* notma = std::getenv("VK_RL_NO_TMA");
+    if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     p->otf.alloc(so, "otf");
     if (!conv) p->otf_flip.alloc(so, "otf_flip");

@@ -244,14 +244,18 @@ def test_fused_yz_conv_matches_three_pass(name, shape, mk):
 
 
 def test_opt_in_schedules_match_default():
-    """The opt-in variants kept for measurement: TMA-staged z tile
-    (VK_RL_TMA), pipelined z (VK_RL_ZPIPE) and the z-chunked schedule
-    (VK_RL_ZCHUNK) against the default path on a 192-point z grid."""
+    """Schedule variants against each other on a 192-point z grid: the
+    TMA-staged z tile (default there) vs cp.async (VK_RL_NO_TMA), and the
+    opt-in pipelined z (VK_RL_ZPIPE) and z-chunked schedule (VK_RL_ZCHUNK)."""
     psf = O.gaussian_psf((15, 15, 15), 1.75)
     obs = synth.blurred(synth.blobs((160, 256, 256), 60, 5, 9, seed=12), psf)  # W = 192 x 288 x 288
     rule = fixed_rule(3)
     ref = vk.richardson_lucy(obs, psf, rule)
-    for env, tag in (({"VK_RL_TMA": "1"}, "z:tma"), ({"VK_RL_ZPIPE": "1"}, None), ({"VK_RL_ZCHUNK": "24"}, "zchunk")):
+    assert "z:tma" in vk.RlPlan(obs.shape, psf).describe()
+    its, _ = run_oracle(obs, psf, 3)
+    assert rel_l2(ref.estimate, its[-1]) <= TOL_1
+    for env, tag in (({"VK_RL_NO_TMA": "1"}, None), ({"VK_RL_ZPIPE": "1", "VK_RL_NO_TMA": "1"}, None),
+                     ({"VK_RL_ZCHUNK": "24"}, "zchunk")):
         got = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule))
         assert rel_l2(got.estimate, ref.estimate) <= 1e-6, env
         if tag:
