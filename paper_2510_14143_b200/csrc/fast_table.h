@@ -12,8 +12,10 @@ namespace vk {
 // Kernel argument of zpass_tma: the S_B tensor map (param space, 64-byte
 // aligned, __grid_constant__) and the usual z-pass arguments.
 struct alignas(64) ZTmaArgs {
-  CUtensorMap map;  // S: dims {Wy, zrows, Hx}, box {16, Pz, 1}, 8-byte elements
+  CUtensorMap map;   // S: dims {Wy, zrows, Hx}, box {16, Pz, 1}, 8-byte elements
+  CUtensorMap omap;  // OTF: dims {Wy, Wz, Hx}, box {16, Wz, 1} (when otf_tma)
   ZArgs z;
+  int otf_tma;
 };
 
 struct FastEntry {

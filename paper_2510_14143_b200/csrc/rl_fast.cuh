@@ -606,7 +606,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   extern __shared__ __align__(128) float2 smem[];
   float2* tw = TWG ? nullptr : smem;
   float2* A = TWG ? smem : smem + N;  // dense [z][16]; N*16*8 B, 128-B aligned (N multiple of 8)
-  __shared__ uint64_t bar;
+  float2* O = A + N * L;              // OTF tile [kz][16] when ta.otf_tma
+  __shared__ uint64_t bar, obar;
+  const bool otma = ta.otf_tma != 0;
   const int kx = blockIdx.y, ky0 = blockIdx.x * L;
   const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
   const int ky = ky0 + l;
@@ -614,6 +616,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   const bool kok = ky < (int)Wy;
   if (threadIdx.x == 0) {
     mbar_init(&bar, 1);
+    mbar_init(&obar, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   if (!TWG) reg::load_twiddles2<R1, R2>(tw, ta.z.plan.tw);
@@ -624,6 +627,10 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, (unsigned)(n_in * L * sizeof(float2)));
     tma_load_3d(A, &ta.map, &bar, ky0, 0, kx);
+    if (otma) {  // the OTF tile lands while the forward transform runs
+      mbar_expect_tx(&obar, (unsigned)(N * L * sizeof(float2)));
+      tma_load_3d(O, &ta.omap, &obar, ky0, 0, kx);
+    }
   }
 #pragma unroll
   for (int k = 0; k < IT; ++k) {  // zero padding rows, disjoint from the copy
@@ -634,10 +641,19 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false, L, TWG>(A, twp);
   const float2* og = otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
+  if (otma) {
+    mbar_wait(&obar, 0);
 #pragma unroll
-  for (int k = 0; k < IT; ++k) {
-    const int z = z0 + k * ZS;
-    if (z < N) A[z * L + l] = cmul(A[z * L + l], kok ? __ldg(&og[(unsigned)z * Wy]) : make_float2(0.f, 0.f));
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N) A[z * L + l] = cmul(A[z * L + l], O[z * L + l]);
+    }
+  } else {
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N) A[z * L + l] = cmul(A[z * L + l], kok ? __ldg(&og[(unsigned)z * Wy]) : make_float2(0.f, 0.f));
+    }
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true, L, TWG>(A, twp);

@@ -42,7 +42,7 @@ FastEntry make_entry() {
   e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
   if constexpr (ZTMA > 0 && LZ == 16) {
     e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;
-    e.smem_zt = (size_t)(R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);
+    e.smem_zt = (size_t)(2 * R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);  // tile + OTF tile
   }
   return e;
 }

@@ -210,8 +210,8 @@ struct vk_rl_plan_s {
   // of zchunk rows, so the chunk's spectrum rows stay in L2 between passes
   int zchunk = 0;
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
-  bool ztma = false;
-  CUtensorMap zmap{};
+  bool ztma = false, otma = false;
+  CUtensorMap zmap{}, omap{}, omap_flip{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
   int cl_clusters = 0;
@@ -434,6 +434,8 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
     vk::ZTmaArgs ta{};
     ta.map = p->zmap;
     ta.z = a;
+    ta.otf_tma = p->otma && (otf == p->otf.p || otf == p->otf_flip.p);
+    if (ta.otf_tma) ta.omap = otf == p->otf.p ? p->omap : p->omap_flip;
     dim3 grid((p->g.Wy + 15) / 16, p->g.Hx);
     const size_t t = prof_begin(p, s);
     launch(p->fz->ztk, grid, p->fz->NTz, p->fz->smem_zt, s, &ta, p->fz->pdl);
@@ -673,6 +675,28 @@ bool encode_zmap(vk_rl_plan p, int zrows) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// OTF [Hx][Wz][Wy] as {Wy, Wz, Hx}, box {16, Wz, 1}.
+bool encode_otf_map(vk_rl_plan p, void* base, CUtensorMap* m) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const Geom& g = p->g;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.Wy, (cuuint64_t)g.Wz, (cuuint64_t)g.Hx};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.Wy * 8, (cuuint64_t)g.Wz * g.Wy * 8};
+  const cuuint32_t box[3] = {16, (cuuint32_t)g.Wz, 1};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  return ((EncodeFn)f)(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, estr,
+                       CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
+}
+
 void to3(int rank, const uint64_t* in, uint64_t* out3) {
   for (int i = 0; i < 3; ++i) out3[i] = 1;
   for (int i = 0; i < rank; ++i) out3[3 - rank + i] = in[i];
@@ -905,6 +929,11 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     p->otf.alloc(so, "otf");
     if (!conv) p->otf_flip.alloc(so, "otf_flip");
+    if (p->ztma && !conv && g.Wz <= 256) {  // OTF tiles by TMA too (VK_RL_NO_OTF_TMA=1 disables)
+      const char* no = std::getenv("VK_RL_NO_OTF_TMA");
+      p->otma = !(no && no[0] == '1') && encode_otf_map(p, p->otf.p, &p->omap) &&
+                encode_otf_map(p, p->otf_flip.p, &p->omap_flip);
+    }
     p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
     if (p->df) setup_dataflow(p);
     p->stats.alloc(1, "stats");
