@@ -475,3 +475,29 @@ def test_ssim_rule_matches_oracle_run():
     assert rel_l2(r.estimate, e) <= TOL_N
 
 
+
+
+# ---- randomized shapes over the fast z lengths (TMA tiles) and generic x/y ---
+_RNG_CASES = []
+_r = np.random.default_rng(2026)
+for _wz, _kz in ((96, 15), (144, 21), (192, 31), (96, 7), (144, 5), (192, 9)):
+    # image z extent so that good_size(Iz + 2 floor(Kz/2) + Kz - 1) == Wz
+    _iz = max(4, _wz - (_kz - 1) - 2 * (_kz // 2) - int(_r.integers(0, 3)))
+    _iy, _ix = int(_r.integers(9, 60)), int(_r.integers(9, 70))
+    _ky, _kx = int(_r.integers(1, 6)) * 2 - 1, int(_r.integers(1, 6)) * 2
+    _RNG_CASES.append(((_iz, _iy, _ix), (_kz, _ky, _kx)))
+
+
+@pytest.mark.parametrize("shape,kshape", _RNG_CASES, ids=lambda v: "x".join(map(str, v)))
+def test_random_shapes_fast_z(shape, kshape):
+    rng = np.random.default_rng(sum(shape) * 7 + sum(kshape))
+    k = rng.random(kshape) + 0.1
+    psf = (k / k.sum()).astype(np.float32)
+    obs = (rng.random(shape) * 3 + 0.05).astype(np.float32)
+    its, t = run_oracle(obs, psf, 3)
+    r = vk.richardson_lucy(obs, psf, fixed_rule(3))
+    assert tuple(r.trace.fft_shape) == tuple(t.fft_shape)
+    assert rel_l2(r.estimate, its[-1]) <= TOL_1
+    rf = vk.richardson_lucy(obs, psf, fixed_rule(3), True)
+    itf, _ = run_oracle(obs, psf, 3, True)
+    assert rel_l2(rf.estimate, itf[-1]) <= TOL_1
