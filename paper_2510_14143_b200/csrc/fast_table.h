@@ -36,6 +36,8 @@ struct FastEntry {
   const void* zpk;      // zpass_pipe<R1,R2,Lz>(ZArgs): persistent, double-buffered
   const void* ztk;      // zpass_tma<R1,R2>(ZTmaArgs): TMA-staged column tile (Lz = 16), or nullptr
   size_t smem_zt;
+  const void* ytk;      // ypass_tma<R1,R2,Ly>(YArgs): bulk-copied lines (FWD/INV), or nullptr
+  size_t smem_yt;
 };
 
 const FastEntry* fast_lookup(int n);

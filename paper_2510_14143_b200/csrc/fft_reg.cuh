@@ -188,7 +188,10 @@ __device__ __forceinline__ int sw(int i, int l) {
 // and writes the same index set per thread.  Caller syncs before.
 // TWG: `tw` is the butterfly-major table in global memory (read through L1)
 // instead of shared memory.
-template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1, bool TWG = false>
+// Element (i, l) lives at buf[i * LP + l * LS]: LS = 1 is the interleaved
+// layout (LP = L+1 pad, or LP = L for 16-lane rows); LP = 1 with LS = row
+// pitch is the line-major layout bulk copies land in.
+template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1, bool TWG = false, int LS = 1>
 __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
   static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
 #ifdef VK_DEBUG_NOFFT  // experiment builds only: isolate the memory cost of a pass
@@ -200,11 +203,11 @@ __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
     const int l = t % L, j = t / L;
     const bool act = t < L * R2;
     float2 v[R1];
-    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l]; });
+    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l * LS]; });
     __syncthreads();
     if (act) {
       rdft<R1, INV>(v);
-      static_for<0, R1>([&](auto q) { buf[(j * R1 + decltype(q)::value) * LP + l] = v[decltype(q)::value]; });
+      static_for<0, R1>([&](auto q) { buf[(j * R1 + decltype(q)::value) * LP + l * LS] = v[decltype(q)::value]; });
     }
     __syncthreads();
   }
@@ -215,17 +218,17 @@ __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
     // pair groups (2m, 2m+1) map to j = m and m+8 within each 16 butterflies.
     const int l = t % L, g = t / L;
     constexpr int G16 = (R1 / 16) * 16;
-    const int j = (L == 8 && LP == 9 && g < G16) ? ((g & ~15) | ((g >> 1) & 7) | ((g & 1) << 3)) : g;
+    const int j = (L == 8 && LP == 9 && LS == 1 && g < G16) ? ((g & ~15) | ((g >> 1) & 7) | ((g & 1) << 3)) : g;
     float2 v[R2];
-    v[0] = buf[j * LP + l];
+    v[0] = buf[j * LP + l * LS];
     static_for<1, R2>([&](auto r) {
       constexpr int rr = decltype(r)::value;
       const float2 w = TWG ? __ldg(tw + j * R2 + rr) : tw[j * R2 + rr];  // load_twiddles2 layout
-      const float2 x = buf[(j + rr * R1) * LP + l];
+      const float2 x = buf[(j + rr * R1) * LP + l * LS];
       v[rr] = INV ? cmulc(x, w) : cmul(x, w);
     });
     rdft<R2, INV>(v);
-    static_for<0, R2>([&](auto q) { buf[(j + decltype(q)::value * R1) * LP + l] = v[decltype(q)::value]; });
+    static_for<0, R2>([&](auto q) { buf[(j + decltype(q)::value * R1) * LP + l * LS] = v[decltype(q)::value]; });
   }
   __syncthreads();
 }

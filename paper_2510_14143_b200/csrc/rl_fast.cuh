@@ -663,6 +663,65 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   }
 }
 
+// ---- y forward / inverse with bulk-copied lines ---------------------------
+// Each of the L input lines (n_in contiguous complex) is one
+// cp.async.bulk global->shared copy into a line-major tile of pitch YNP
+// (YNP = 2 mod 16: the pass-1 loads and pass 2 of the FFT are then free of
+// bank conflicts with lanes along l), completion on one mbarrier; the zero
+// padding [n_in, N) is written by the other threads meanwhile.  Requires an
+// even n_in and in_pitch (16-byte sizes and addresses).
+template <int N>
+struct YTma {
+  static constexpr int NP = ((N + 13) / 16) * 16 + 2;  // >= N, = 2 (mod 16)
+};
+
+__device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, unsigned bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(smem_dst)),
+               "l"(src), "r"(bytes), "r"((unsigned)__cvta_generic_to_shared(bar))
+               : "memory");
+}
+
+template <int R1, int R2, int L, bool TWG>
+__global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const YArgs a) {
+  constexpr int N = R1 * R2, NT = FastCfg<R1, R2, L, true>::NT, NP = YTma<N>::NP;
+  extern __shared__ __align__(128) float2 smem[];
+  float2* tw = TWG ? nullptr : smem;
+  float2* A = TWG ? smem : smem + ((N + 1) / 2) * 2;  // keep 16-byte alignment
+  __shared__ uint64_t bar;
+  const int line0 = blockIdx.x * L;
+  if (threadIdx.x == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
+  const float2* twp = TWG ? a.plan.tw2 : tw;
+  __syncthreads();
+  pdl_trigger();
+  pdl_wait();
+  const int nvalid = min(L, a.nlines - line0);
+  if (threadIdx.x == 0) {
+    mbar_expect_tx(&bar, (unsigned)(nvalid * a.n_in * sizeof(float2)));
+    for (int l = 0; l < nvalid; ++l)
+      bulk_load(A + l * NP, a.in + (size_t)y_line(a, line0 + l) * a.in_pitch, (unsigned)(a.n_in * sizeof(float2)),
+                &bar);
+  }
+  for (int idx = threadIdx.x; idx < L * N; idx += NT) {  // padding and missing lines
+    const int l = idx / N, i = idx - l * N;
+    if (l >= nvalid || i >= a.n_in) A[l * NP + i] = make_float2(0.f, 0.f);
+  }
+  mbar_wait(&bar, 0);
+  __syncthreads();
+  if (a.mode == YM_INV)
+    reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
+  else
+    reg::fft2<R1, R2, L, NT, false, 1, TWG, NP>(A, twp);
+  for (int l = 0; l < nvalid; ++l) {
+    float2* out = a.out + (size_t)y_line(a, line0 + l) * a.out_pitch;
+    for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[l * NP + j + a.out_off];
+  }
+}
+
 // Persistent, double-buffered z convolution: each CTA walks tiles
 // (kx, ky-chunk) with stride gridDim.x and keeps the NEXT tile's column block
 // (and, with PREF, its OTF block) in flight (cp.async group) while it

@@ -15,7 +15,8 @@ namespace {
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
           bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0,
-          int ZTMA = 0>  // ZTMA: resident-CTA floor of the TMA z kernel (0 = no TMA variant)
+          int ZTMA = 0,  // ZTMA: resident-CTA floor of the TMA z kernel (0 = no TMA variant)
+          bool YTMA = false>
 FastEntry make_entry() {
   constexpr int LY = LY0 ? LY0 : LX;  // y-pass lines per CTA (default: the x pass's)
   FastEntry e{};
@@ -40,6 +41,10 @@ FastEntry make_entry() {
   e.zk = (const void*)zpass_fast<R1, R2, LZ, ZTWG, ZPREF, ZMINB>;
   e.smem_zp = ZPipeCfg<R1, R2, LZ, ZTWG, ZPREF>::smem;
   e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
+  if constexpr (YTMA) {
+    e.ytk = (const void*)ypass_tma<R1, R2, LY, TWG>;
+    e.smem_yt = (size_t)(LY * YTma<R1 * R2>::NP + (TWG ? 0 : ((R1 * R2 + 1) / 2) * 2)) * sizeof(float2);
+  }
   if constexpr (ZTMA > 0 && LZ == 16) {
     e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;
     e.smem_zt = (size_t)(2 * R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);  // tile + OTF tile
@@ -54,7 +59,7 @@ const FastEntry kTable[] = {
     make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 0, 4>(),  // 192 (z: TMA tile, 4 CTAs/SM)
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
-    make_entry<24, 24, 8, 8, true, true, 5>(),  // 576: global twiddles -> 5 x/y-pass CTAs per SM (y L=4: slower)
+    make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(),  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
     make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4>(),  // 1080 (Ix = 1000: partial chunks are common)
     // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
     // in griddepcontrol.wait would hold the scarce slots the batch lanes'
@@ -123,6 +128,8 @@ cudaError_t fast_init_attributes() {
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
     if ((r = cudaFuncSetAttribute(e.zpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zp))) return r;
     if (e.ztk && (r = cudaFuncSetAttribute(e.ztk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zt)))
+      return r;
+    if (e.ytk && (r = cudaFuncSetAttribute(e.ytk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yt)))
       return r;
     // prefer the full shared-memory carveout: occupancy is smem-limited
     for (const void* k : {e.xk, e.yk, e.zk, e.zpk})

@@ -210,7 +210,7 @@ struct vk_rl_plan_s {
   // of zchunk rows, so the chunk's spectrum rows stay in L2 between passes
   int zchunk = 0;
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
-  bool ztma = false, otma = false;
+  bool ztma = false, otma = false, ytma = false;
   CUtensorMap zmap{}, omap{}, omap_flip{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
@@ -407,8 +407,13 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
   if (p->fy)
-    launch(p->fy->yk, grid, p->fy->NTy, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
-           p->fy->pdl);
+  {
+    if (p->ytma && mode != vk::YM_CONV && n_in % 2 == 0 && in_pitch % 2 == 0)
+      launch(p->fy->ytk, grid, p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
+    else
+      launch(p->fy->yk, grid, p->fy->NTy, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
+             p->fy->pdl);
+  }
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
@@ -925,6 +930,8 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     // fits (Pz <= 256): C2 z convolutions 0.313 vs 0.345 ms per iteration
     // with cp.async (profiles/r01/final/tma.log).  VK_RL_NO_TMA=1 disables.
     const char* notma = std::getenv("VK_RL_NO_TMA");
+    const char* noyt = std::getenv("VK_RL_NO_YTMA");
+    p->ytma = p->fy && p->fy->ytk && !(notma && notma[0] == '1') && !(noyt && noyt[0] == '1');
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     p->otf.alloc(so, "otf");
@@ -1573,6 +1580,7 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
       s += g.Wz > 1 ? "3-pass" : "y-conv";
     if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
     if (p->ztma) s += " z:tma";
+    if (p->ytma) s += " y:bulk";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
     buf[len - 1] = 0;
   });
