@@ -670,9 +670,13 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
 // bank conflicts with lanes along l), completion on one mbarrier; the zero
 // padding [n_in, N) is written by the other threads meanwhile.  Requires an
 // even n_in and in_pitch (16-byte sizes and addresses).
-template <int N>
+// Row pitch: the smallest NP >= N with NP = 16/L (mod 16) (L <= 8: the L
+// lines of a half-warp land on disjoint bank pairs next to consecutive
+// butterflies, and NP stays even so every row is 16-byte aligned).
+template <int N, int L>
 struct YTma {
-  static constexpr int NP = ((N + 13) / 16) * 16 + 2;  // >= N, = 2 (mod 16)
+  static constexpr int RES = L >= 16 ? 1 : 16 / L;
+  static constexpr int NP = N + ((RES - N % 16) % 16 + 16) % 16;
 };
 
 __device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, unsigned bytes, uint64_t* bar) {
@@ -684,7 +688,8 @@ __device__ __forceinline__ void bulk_load(void* smem_dst, const void* src, unsig
 
 template <int R1, int R2, int L, bool TWG>
 __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const YArgs a) {
-  constexpr int N = R1 * R2, NT = FastCfg<R1, R2, L, true>::NT, NP = YTma<N>::NP;
+  static_assert(L <= 8, "16-byte aligned rows need an even pitch: L <= 8");
+  constexpr int N = R1 * R2, NT = FastCfg<R1, R2, L, true>::NT, NP = YTma<N, L>::NP;
   extern __shared__ __align__(128) float2 smem[];
   float2* tw = TWG ? nullptr : smem;
   float2* A = TWG ? smem : smem + ((N + 1) / 2) * 2;  // keep 16-byte alignment
@@ -712,10 +717,19 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
   }
   mbar_wait(&bar, 0);
   __syncthreads();
-  if (a.mode == YM_INV)
+  if (a.mode == YM_INV) {
     reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
-  else
+  } else {
     reg::fft2<R1, R2, L, NT, false, 1, TWG, NP>(A, twp);
+    if (a.mode == YM_CONV) {  // 2D: x OTF (line-major reads, coalesced) then inverse
+      for (int l = 0; l < nvalid; ++l) {
+        const float2* o = a.otf + (size_t)(line0 + l) * N;
+        for (int k = threadIdx.x; k < N; k += NT) A[l * NP + k] = cmul(A[l * NP + k], __ldg(o + k));
+      }
+      __syncthreads();
+      reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
+    }
+  }
   for (int l = 0; l < nvalid; ++l) {
     float2* out = a.out + (size_t)y_line(a, line0 + l) * a.out_pitch;
     for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[l * NP + j + a.out_off];

@@ -43,7 +43,7 @@ FastEntry make_entry() {
   e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
   if constexpr (YTMA) {
     e.ytk = (const void*)ypass_tma<R1, R2, LY, TWG>;
-    e.smem_yt = (size_t)(LY * YTma<R1 * R2>::NP + (TWG ? 0 : ((R1 * R2 + 1) / 2) * 2)) * sizeof(float2);
+    e.smem_yt = (size_t)(LY * YTma<R1 * R2, LY>::NP + (TWG ? 0 : ((R1 * R2 + 1) / 2) * 2)) * sizeof(float2);
   }
   if constexpr (ZTMA > 0 && LZ == 16) {
     e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;
@@ -60,11 +60,11 @@ const FastEntry kTable[] = {
     make_entry<16, 16, 16, 16>(),  // 256
     make_entry<16, 18, 16, 16>(),  // 288
     make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(),  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
-    make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4>(),  // 1080 (Ix = 1000: partial chunks are common)
+    make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4, 0, true>(),  // 1080 (Ix = 1000: partial chunks are common)
     // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
     // in griddepcontrol.wait would hold the scarce slots the batch lanes'
     // kernels need: C5 3.05e10 without vs 2.66e10 with, profiles/r01/pdl.log)
-    make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false, 2, 2>(),  // y L=2
+    make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false, 2, 2, 0, true>(),  // y L=2
 };
 
 }  // namespace

@@ -408,7 +408,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   const size_t t = prof_begin(p, s);
   if (p->fy)
   {
-    if (p->ytma && mode != vk::YM_CONV && n_in % 2 == 0 && in_pitch % 2 == 0)
+    if (p->ytma && n_in % 2 == 0 && in_pitch % 2 == 0)
       launch(p->fy->ytk, grid, p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
     else
       launch(p->fy->yk, grid, p->fy->NTy, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
