@@ -53,12 +53,12 @@ FastEntry make_entry() {
 }
 
 const FastEntry kTable[] = {
-    make_entry<8, 8, 16, 16>(),    // 64 (FRC half grids, small z)
-    make_entry<8, 12, 16, 16, false, true, 1, false, false, true, 1, true, 2, 0, 6>(),   // 96 (z: TMA 6)
-    make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8, true, 2, 0, 6>(),  // 144 (z: 8 CTAs/SM; TMA 6)
-    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 0, 4>(),  // 192 (z: TMA tile, 4 CTAs/SM)
-    make_entry<16, 16, 16, 16>(),  // 256
-    make_entry<16, 18, 16, 16>(),  // 288
+    make_entry<8, 8, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(),  // 64 (FRC half grids, small z)
+    make_entry<8, 12, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 6, true>(),  // 96 (z: TMA 6; y bulk L=8)
+    make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8, true, 2, 8, 6, true>(),  // 144 (z: TMA 6; y bulk L=8)
+    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 8, 4, true>(),  // 192 (z: TMA tile, 4 CTAs/SM; y bulk L=8)
+    make_entry<16, 16, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(),  // 256 (y bulk L=8)
+    make_entry<16, 18, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(),  // 288 (y: bulk, L=8)
     make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(),  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
     make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4, 0, true>(),  // 1080 (Ix = 1000: partial chunks are common)
     // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
