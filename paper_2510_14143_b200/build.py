@@ -39,8 +39,20 @@ CLI_SRC = os.path.join(PKG, "host", "vk_cli.cu")
 CLI = os.path.join(LIBDIR, "voxelkit_b200")
 
 
+# rl_fast_len.cu is compiled once per compile-time FFT length (-DVK_LEN=N)
+FAST_LENGTHS = (64, 96, 144, 192, 256, 288, 576, 1080, 2160)
+
+
 def sources():
-    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cu", ".cpp")))
+    return sorted(os.path.join(CSRC, f) for f in os.listdir(CSRC)
+                  if f.endswith((".cu", ".cpp")) and f != "rl_fast_len.cu")
+
+
+def units():
+    """(source, extra flags, object name) for every object of the library."""
+    u = [(src, [], os.path.splitext(os.path.basename(src))[0] + ".o") for src in sources()]
+    u += [(os.path.join(CSRC, "rl_fast_len.cu"), [f"-DVK_LEN={n}"], f"rl_fast_len_{n}.o") for n in FAST_LENGTHS]
+    return u
 
 
 def deps():
@@ -74,15 +86,36 @@ def build(force: bool = False, verbose: bool = False) -> str:
     if not force and up_to_date():
         return LIB
     os.makedirs(LIBDIR, exist_ok=True)
+    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(objdir, exist_ok=True)
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(unit):
+        src, extra, obj = unit
+        cmd = [_nvcc(), *compile_flags, *extra, "-c", "-o", os.path.join(objdir, obj), src]
+        r = subprocess.run(cmd, capture_output=True, text=True)
+        return cmd, r
+
+    from concurrent.futures import ThreadPoolExecutor
+
+    # the per-length kernels dominate the build: compile every object at once
+    with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
+        results = list(ex.map(compile_one, units()))
+    for cmd, r in results:
+        if verbose:
+            print(" ".join(cmd))
+        if r.returncode != 0:
+            raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
+        if verbose and r.stderr:
+            print(r.stderr)
     tmp = LIB + ".tmp"
-    cmd = [_nvcc(), *NVCC_FLAGS, "-o", tmp, *sources()]
+    cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
+           *[os.path.join(objdir, u[2]) for u in units()]]
     if verbose:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
-        raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
-    if verbose and r.stderr:
-        print(r.stderr)
+        raise RuntimeError(f"nvcc (link) failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
     os.replace(tmp, LIB)
     build_cli(verbose)
     return LIB

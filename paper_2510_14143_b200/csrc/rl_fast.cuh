@@ -29,6 +29,9 @@ __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
   const unsigned s = (unsigned)__cvta_generic_to_shared(smem_dst);
   asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(s), "l"(gsrc) : "memory");
 }
+__device__ __forceinline__ void prefetch_l2(const void* p) {
+  asm volatile("prefetch.global.L2 [%0];" ::"l"(p));
+}
 __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
@@ -115,6 +118,33 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
     // NT/L; spectrum offsets are 32-bit and incremental.
     constexpr int KS = NT / L;  // kx stride per thread
     const float2 zero = make_float2(0.f, 0.f);
+    // L2 prefetch at entry: every load round of this CTA after the first, and
+    // the epilogue's observed / estimate rows, then hit L2 instead of HBM (the
+    // epilogue walks its rows in ~12 dependent load rounds per warp).
+    if (a.pf & 1) {
+      const unsigned plane = (unsigned)g.Pz * g.Py;
+      const float2* base = a.S + (unsigned)z * g.Py + y0;
+      for (int i = threadIdx.x; i < 2 * Hx; i += NT)
+        if (y0 + (i & 1) * L < g.Py) prefetch_l2(base + (unsigned)(i >> 1) * plane + (i & 1) * L);
+    }
+    if (a.pf & 2) {
+      const int iz = clampi(z - g.oz, 0, g.Iz - 1);
+      const int nlo = (g.Ix + 31) / 32 + 1, nle = (g.Px + 31) / 32 + 1;
+      const bool upd = a.mode != XM_RATIO;
+      const int per = nlo + (upd ? nle : 0);
+      for (int i = threadIdx.x; i < 2 * L * per; i += NT) {
+        const int r = i / per, k = i - r * per;
+        const int y = min(y0 + r, g.Py - 1);
+        if (k < nlo) {
+          const int iy = clampi(y - g.oy, 0, g.Iy - 1);
+          const float* row = a.obs + ((size_t)iz * g.Iy + iy) * g.Ix;
+          prefetch_l2(row + min(k * 32, g.Ix - 1));
+        } else {
+          const float* row = a.est + ((size_t)z * g.Py + y) * g.Px;
+          prefetch_l2(row + min((k - nlo) * 32, g.Px - 1));
+        }
+      }
+    }
     {
       const int l = threadIdx.x & (L - 1);
       const int ya = y0 + l, yb = y0 + L + l;
@@ -825,6 +855,7 @@ __global__ void __launch_bounds__(ZPipeCfg<R1, R2, L, TWG, PREF>::NT, MINB == 1 
   cp_async_wait_all();
 }
 
+#ifdef VK_FAST_TABLE_MAIN  // defined once, in rl_fast_table.cu
 // Phase ramp exp(+2 pi i cx kx / Wx) over an OTF laid out [Hx][Wz][Wy].
 __global__ void otf_ramp_kernel(float2* __restrict__ otf, int Hx, size_t plane, int Wx, int cx) {
   const size_t n = (size_t)Hx * plane;
@@ -836,5 +867,6 @@ __global__ void otf_ramp_kernel(float2* __restrict__ otf, int Hx, size_t plane, 
     otf[i] = cmul(otf[i], make_float2((float)c, (float)s));
   }
 }
+#endif
 
 }  // namespace vk

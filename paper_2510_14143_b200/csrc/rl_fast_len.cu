@@ -1,0 +1,38 @@
+// One translation unit per compile-time FFT length: build.py compiles this
+// file once per length with -DVK_LEN=N (the lengths' kernels are the bulk of
+// the build and compile in parallel).  Variant choices per length come from
+// B200 measurements (see the comments).
+#include "fast_entry.cuh"
+
+#ifndef VK_LEN
+#error "compile with -DVK_LEN=<fft length>"
+#endif
+
+namespace vk {
+
+#if VK_LEN == 64
+FastEntry fast_entry_64() { return make_entry<8, 8, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(); }  // 64 (FRC half grids, small z)
+#elif VK_LEN == 96
+FastEntry fast_entry_96() { return make_entry<8, 12, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 6, true>(); }  // 96 (z: TMA 6; y bulk L=8)
+#elif VK_LEN == 144
+FastEntry fast_entry_144() { return make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8, true, 2, 8, 6, true>(); }  // 144 (z: TMA 6; y bulk L=8)
+#elif VK_LEN == 192
+FastEntry fast_entry_192() { return make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 8, 4, true>(); }  // 192 (z: TMA tile, 4 CTAs/SM; y bulk L=8)
+#elif VK_LEN == 256
+FastEntry fast_entry_256() { return make_entry<16, 16, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(); }  // 256 (y bulk L=8)
+#elif VK_LEN == 288
+FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(); }  // 288 (y: bulk, L=8)
+#elif VK_LEN == 576
+FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(); }  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
+#elif VK_LEN == 1080
+FastEntry fast_entry_1080() { return make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4, 0, true>(); }  // 1080 (Ix = 1000: partial chunks are common)
+#elif VK_LEN == 2160
+// 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
+// in griddepcontrol.wait would hold the scarce slots the batch lanes'
+// kernels need: C5 3.05e10 without vs 2.66e10 with, profiles/r01/pdl.log)
+FastEntry fast_entry_2160() { return make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false, 2, 2, 0, true>(); }  // y L=2
+#else
+#error "no fast-table entry for VK_LEN"
+#endif
+
+}  // namespace vk

@@ -3,68 +3,37 @@
 // 288, 576, 1080, 2160) plus a few common neighbours.  Any other 5-smooth
 // length runs the generic Stockham kernels of rl_passes.cuh.
 #define VK_NO_GENERIC_KERNELS
+#define VK_FAST_TABLE_MAIN  // otf_ramp_kernel lives in this TU
 #include "fast_table.h"
+#include "rl_fast.cuh"
 #include "rl_cluster.cuh"
 #include "rl_dataflow.cuh"
 
 namespace vk {
 
+// rl_fast_len.cu, one object per length
+FastEntry fast_entry_64();
+FastEntry fast_entry_96();
+FastEntry fast_entry_144();
+FastEntry fast_entry_192();
+FastEntry fast_entry_256();
+FastEntry fast_entry_288();
+FastEntry fast_entry_576();
+FastEntry fast_entry_1080();
+FastEntry fast_entry_2160();
+
 namespace {
 
-// TWG / YPREF / XMINB / XPB: x and y pass variants (rl_fast.cuh); ZTWG /
-// ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
-template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
-          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0,
-          int ZTMA = 0,  // ZTMA: resident-CTA floor of the TMA z kernel (0 = no TMA variant)
-          bool YTMA = false>
-FastEntry make_entry() {
-  constexpr int LY = LY0 ? LY0 : LX;  // y-pass lines per CTA (default: the x pass's)
-  FastEntry e{};
-  e.N = R1 * R2;
-  e.pdl = PDL;
-  e.R1 = R1;
-  e.smem_xp = TWG ? FastCfg<R1, R2, LX>::smem_x : FastCfg<R1, R2, LX>::smem;
-  e.Lx = LX;
-  e.NTx = FastCfg<R1, R2, LX>::NT;
-  e.smem_x = FastCfg<R1, R2, LX>::smem;
-  e.Ly = LY;
-  e.NTy = FastCfg<R1, R2, LY, true>::NT;
-  e.smem_yp = (size_t)(FastCfg<R1, R2, LY, true>::DATA + (TWG ? 0 : R1 * R2)) * sizeof(float2);
-  e.smem_yconv = (size_t)(FastCfg<R1, R2, LY, true>::DATA + (TWG ? 0 : R1 * R2) + (YPREF ? R1 * R2 * LY : 0)) *
-                 sizeof(float2);
-  e.xk = (const void*)xpass_fast<R1, R2, LX, TWG, XMINB, XPB>;
-  e.yk = (const void*)ypass_fast<R1, R2, LY, TWG, YPREF>;
-  e.Lz = LZ;
-  e.NTz = FastCfg<R1, R2, LZ, true>::NT;
-  e.smem_z = (size_t)(FastCfg<R1, R2, LZ, true>::DATA + (ZTWG ? 0 : R1 * R2) + (ZPREF ? R1 * R2 * LZ : 0)) *
-             sizeof(float2);
-  e.zk = (const void*)zpass_fast<R1, R2, LZ, ZTWG, ZPREF, ZMINB>;
-  e.smem_zp = ZPipeCfg<R1, R2, LZ, ZTWG, ZPREF>::smem;
-  e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
-  if constexpr (YTMA) {
-    e.ytk = (const void*)ypass_tma<R1, R2, LY, TWG>;
-    e.smem_yt = (size_t)(LY * YTma<R1 * R2, LY>::NP + (TWG ? 0 : ((R1 * R2 + 1) / 2) * 2)) * sizeof(float2);
-  }
-  if constexpr (ZTMA > 0 && LZ == 16) {
-    e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;
-    e.smem_zt = (size_t)(2 * R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);  // tile + OTF tile
-  }
-  return e;
-}
-
 const FastEntry kTable[] = {
-    make_entry<8, 8, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(),  // 64 (FRC half grids, small z)
-    make_entry<8, 12, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 6, true>(),  // 96 (z: TMA 6; y bulk L=8)
-    make_entry<12, 12, 16, 16, false, true, 1, false, true, false, 8, true, 2, 8, 6, true>(),  // 144 (z: TMA 6; y bulk L=8)
-    make_entry<12, 16, 16, 16, false, true, 1, false, true, false, 5, true, 2, 8, 4, true>(),  // 192 (z: TMA tile, 4 CTAs/SM; y bulk L=8)
-    make_entry<16, 16, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(),  // 256 (y bulk L=8)
-    make_entry<16, 18, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(),  // 288 (y: bulk, L=8)
-    make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(),  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
-    make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4, 0, true>(),  // 1080 (Ix = 1000: partial chunks are common)
-    // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
-    // in griddepcontrol.wait would hold the scarce slots the batch lanes'
-    // kernels need: C5 3.05e10 without vs 2.66e10 with, profiles/r01/pdl.log)
-    make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false, 2, 2, 0, true>(),  // y L=2
+    fast_entry_64(),
+    fast_entry_96(),
+    fast_entry_144(),
+    fast_entry_192(),
+    fast_entry_256(),
+    fast_entry_288(),
+    fast_entry_576(),
+    fast_entry_1080(),
+    fast_entry_2160(),
 };
 
 }  // namespace

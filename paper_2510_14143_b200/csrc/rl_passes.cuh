@@ -65,6 +65,7 @@ struct XArgs {
   double* acc;          // RATIO: acc[0] += LL ; UPDATE: acc[1..3] += sx, sxx, sxr
   float* out;           // UPDATE_LAST: cropped f32 estimate [Iz][Iy][Ix]
   int zoff;             // first z row of this launch (z-chunked iterations)
+  int pf;               // fast path: L2 prefetch of the CTA's inputs at entry (1 spectrum, 2 rows)
 };
 
 struct YArgs {

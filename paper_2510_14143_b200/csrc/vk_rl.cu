@@ -211,6 +211,7 @@ struct vk_rl_plan_s {
   int zchunk = 0;
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
   bool ztma = false, otma = false, ytma = false;
+  int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
   CUtensorMap zmap{}, omap{}, omap_flip{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
@@ -371,6 +372,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   a.obs = obs;
   a.acc = acc;
   a.out = out;
+  a.pf = p->xpf;
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
@@ -932,6 +934,12 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     const char* notma = std::getenv("VK_RL_NO_TMA");
     const char* noyt = std::getenv("VK_RL_NO_YTMA");
     p->ytma = p->fy && p->fy->ytk && !(notma && notma[0] == '1') && !(noyt && noyt[0] == '1');
+    // x-pass L2 prefetch of the CTA's spectrum chunks and observed/estimate
+    // rows at entry, for 3D grids: C2 -4.1%, C4 -5.9%, C1 -1.6% per
+    // iteration; 2D fields +3% (profiles/r01/final/xpf.log).  VK_RL_XPF=mask
+    // overrides (1 spectrum, 2 rows).
+    p->xpf = g.Wz > 1 ? 3 : 0;
+    if (const char* xpf = std::getenv("VK_RL_XPF")) p->xpf = std::atoi(xpf);
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     p->otf.alloc(so, "otf");
