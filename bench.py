@@ -308,7 +308,33 @@ def main():
     # ---- end-to-end through the public host API ---------------------------
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
     e2e_value = None
-    if e2e_steps > 0:
+    e2e_vols = 0
+    if e2e_steps > 0 and n_batch:
+        # batch configs: the whole block through the host-pointer batch API
+        # (vk_rl_run_batch), pinned host volumes in and out every step
+        # (at most 64 volumes per rank: pinned host memory for the whole C5
+        # block would be 2 x 69 GB)
+        e2e_block = vols[-64:]
+        obs_hs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in e2e_block]
+        est_hs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in e2e_block]
+        for h, v in zip(obs_hs, e2e_block):
+            h.copy_(v.cpu())
+        hin, hout = [h.data_ptr() for h in obs_hs], [h.data_ptr() for h in est_hs]
+        plan.run_batch_ptr(hin, hout, rule)  # warm
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            plan.run_batch_ptr(hin, hout, rule)
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_vols = len(e2e_block)
+        e2e_value = ws * e2e_vols * e2e_steps * iters * n_img / float(te.item())
+        assert torch.equal(est_hs[-1], outs[-1].cpu()), "host-API and device-API results differ"
+    elif e2e_steps > 0:
+        e2e_vols = 1
         obs_h = torch.empty(shape, dtype=torch.float32, pin_memory=True)
         obs_h.copy_(vols[-1].cpu())  # `outs[-1]` holds the device result of the block's last volume
         est_h = torch.empty(shape, dtype=torch.float32, pin_memory=True)
@@ -361,8 +387,11 @@ def main():
                      "per_kernel_ms": {k: round(v[0] / args.steps, 4) for k, v in prof.items() if v[1]},
                      "iteration_B_alg_bytes": b_alg,
                      "iteration_frac": value / n_img / ws * b_alg / 1e9 / peak},
-        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": n_img * 4,
-                "d2h_bytes_per_step": n_img * 4 + iters * 4 * 8 + 48, "steps": e2e_steps},
+        "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_vols * n_img * 4,
+                "d2h_bytes_per_step": e2e_vols * (n_img * 4 + iters * 4 * 8 + 48), "bytes_scope": "per rank",
+                "api": "vk_rl_run_batch (host pointers, batch lanes)" if n_batch else "vk_rl_run (host pointers)",
+                "volumes_per_rank": e2e_vols,
+                "steps": e2e_steps},
         "gpu_launches": launches,
         "clocks": clk.summary(),
     }

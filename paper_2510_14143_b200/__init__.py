@@ -429,6 +429,16 @@ class RlPlan(_Plan):
         _check(lib().vk_rl_plan_lanes(self._h, ctypes.byref(v)))
         return int(v.value)
 
+    def run_batch_ptr(self, obs_ptrs: Sequence[int], est_ptrs: Sequence[int], rule: StoppingRule,
+                      flat_init: bool = False) -> None:
+        """Host-pointer batch (vk_rl_run_batch): each lane copies its volume in
+        (pinned host memory is DMA'd directly), runs it, and copies it out
+        while the other lanes compute."""
+        n = len(obs_ptrs)
+        ip = (_vp * max(n, 1))(*obs_ptrs)
+        op = (_vp * max(n, 1))(*est_ptrs)
+        _check(lib().vk_rl_run_batch(self._h, n, ip, op, ctypes.byref(rule._c()), int(bool(flat_init)), None))
+
     def run_batch(self, observed: Sequence[np.ndarray], rule: StoppingRule = StoppingRule(),
                   flat_init: bool = False) -> List[RlResult]:
         obs = [_f32(o) for o in observed]

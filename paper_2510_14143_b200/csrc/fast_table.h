@@ -16,6 +16,7 @@ struct alignas(64) ZTmaArgs {
   CUtensorMap omap;  // OTF: dims {Wy, Wz, Hx}, box {16, Wz, 1} (when otf_tma)
   ZArgs z;
   int otf_tma;
+  int tma_store;  // write the cropped tile back with one TMA tensor store (same map)
 };
 
 struct FastEntry {

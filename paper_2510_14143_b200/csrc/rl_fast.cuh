@@ -670,6 +670,22 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
       "r"(phase)
       : "memory");
 }
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"((unsigned)__cvta_generic_to_shared(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(smem_src)), "r"(bytes)
+               : "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_commit_and_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
   asm volatile(
@@ -746,6 +762,15 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true, L, TWG>(A, twp);
+  if (ta.tma_store) {  // rows [out_off, out_off+n_out) of the tile ARE the box (n_out = Pz): one TMA store
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      tma_store_3d(&ta.map, A + out_off * L, ky0, 0, kx);  // columns ky >= Wy are clipped
+      bulk_commit_and_wait();
+    }
+    return;
+  }
   if (kok) {
     float2* col = S + ((unsigned)kx * zrows * Wy + ky);
     for (int z = z0; z < n_out; z += ZS) col[(unsigned)z * Wy] = A[(z + out_off) * L + l];
@@ -818,6 +843,17 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
       __syncthreads();
       reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
     }
+  }
+  if (a.bst && a.mode == YM_FWD) {  // 16-byte aligned output lines: one bulk store per line
+    fence_proxy_async_smem();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      for (int l = 0; l < nvalid; ++l)
+        bulk_store(a.out + (size_t)y_line(a, line0 + l) * a.out_pitch, A + l * NP + a.out_off,
+                   (unsigned)(a.n_out * sizeof(float2)));
+      bulk_commit_and_wait();
+    }
+    return;
   }
   for (int l = 0; l < nvalid; ++l) {
     float2* out = a.out + (size_t)y_line(a, line0 + l) * a.out_pitch;

@@ -90,6 +90,7 @@ struct YArgs {
   // kx-blocked S_A side (ypass_blk, lb > 0): S_A holds [Hx/B][bz][rows][B]
   // with B = 1 << lb = the pass's lines per CTA; CTA = (kx block, z row)
   int lb, bz;
+  int bst;  // ypass_tma FWD: bulk-store each output line (16-byte aligned lines only)
 };
 
 // Global line of a pass-local line index (identity unless z-chunked).

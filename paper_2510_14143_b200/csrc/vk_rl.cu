@@ -212,7 +212,8 @@ struct vk_rl_plan_s {
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
   bool ztma = false, otma = false, ytma = false;
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
-  int blk_lb = 0;  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
+  int blk_lb = 0;
+  bool tma_store = true;  // TMA/bulk stores of the z tile and y-forward lines (VK_RL_NO_TMA_STORE=1: thread stores)  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
   CUtensorMap zmap{}, omap{}, omap_flip{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
@@ -418,6 +419,8 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
     launch(p->fy->ybk, dim3(nkb * a.bz), p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
   } else if (p->fy)
   {
+    a.bst = p->tma_store && mode == vk::YM_FWD && out_off % 2 == 0 && out_pitch % 2 == 0 && n_out % 2 == 0 &&
+            (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     if (p->ytma && n_in % 2 == 0 && in_pitch % 2 == 0)
       launch(p->fy->ytk, grid, p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
     else
@@ -450,6 +453,7 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
     ta.map = p->zmap;
     ta.z = a;
     ta.otf_tma = p->otma && (otf == p->otf.p || otf == p->otf_flip.p);
+    ta.tma_store = p->tma_store && n_out == p->g.Pz;
     if (ta.otf_tma) ta.omap = otf == p->otf.p ? p->omap : p->omap_flip;
     dim3 grid((p->g.Wy + 15) / 16, p->g.Hx);
     const size_t t = prof_begin(p, s);
@@ -963,6 +967,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     // iteration; 2D fields +3% (profiles/r01/final/xpf.log).  VK_RL_XPF=mask
     // overrides (1 spectrum, 2 rows).
     p->xpf = g.Wz > 1 ? 3 : 0;
+    if (const char* nts = std::getenv("VK_RL_NO_TMA_STORE")) p->tma_store = nts[0] != '1';
     if (const char* xpf = std::getenv("VK_RL_XPF")) p->xpf = std::atoi(xpf);
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
