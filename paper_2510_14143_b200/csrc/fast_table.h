@@ -46,7 +46,7 @@ const FastEntry* fast_lookup(int n);
 cudaError_t fast_init_attributes();
 
 // OTF *= exp(+2 pi i cx kx / Wx) for every kx plane (layout [Hx][plane]).
-cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, cudaStream_t s);
+cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, int Wy, int cy, cudaStream_t s);
 
 }  // namespace vk
 

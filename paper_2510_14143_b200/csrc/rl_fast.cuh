@@ -844,7 +844,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
       reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
     }
   }
-  if (a.bst && a.mode == YM_FWD) {  // 16-byte aligned output lines: one bulk store per line
+  if (a.bst) {  // 16-byte aligned output lines: one bulk store per line
     fence_proxy_async_smem();
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -1017,14 +1017,17 @@ __global__ void __launch_bounds__(ZPipeCfg<R1, R2, L, TWG, PREF>::NT, MINB == 1 
 }
 
 #ifdef VK_FAST_TABLE_MAIN  // defined once, in rl_fast_table.cu
-// Phase ramp exp(+2 pi i cx kx / Wx) over an OTF laid out [Hx][Wz][Wy].
-__global__ void otf_ramp_kernel(float2* __restrict__ otf, int Hx, size_t plane, int Wx, int cx) {
+// Phase ramp exp(+2 pi i (cx kx / Wx + cy ky / Wy)) over an OTF laid out
+// [Hx][Wz][Wy]: the x crop offset (fast x pass) and, where the y inverse
+// bulk-stores its lines, the y crop offset (the cropped y output then starts
+// at slot 0, a 16-byte aligned shared address).
+__global__ void otf_ramp_kernel(float2* __restrict__ otf, int Hx, size_t plane, int Wx, int cx, int Wy, int cy) {
   const size_t n = (size_t)Hx * plane;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
-    const int kx = (int)(i / plane);
-    const long long m = ((long long)cx * kx) % Wx;
+    const int kx = (int)(i / plane), ky = (int)(i % Wy);
+    const long long m = ((long long)cx * kx) % Wx, my = ((long long)cy * ky) % Wy;
     double s, c;
-    sincospi(2.0 * (double)m / (double)Wx, &s, &c);
+    sincospi(2.0 * ((double)m / (double)Wx + (double)my / (double)Wy), &s, &c);
     otf[i] = cmul(otf[i], make_float2((float)c, (float)s));
   }
 }

@@ -109,8 +109,8 @@ cudaError_t fast_init_attributes() {
   return cudaSuccess;
 }
 
-cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, cudaStream_t s) {
-  otf_ramp_kernel<<<148 * 8, 256, 0, s>>>(otf, Hx, plane, Wx, cx);
+cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, int Wy, int cy, cudaStream_t s) {
+  otf_ramp_kernel<<<148 * 8, 256, 0, s>>>(otf, Hx, plane, Wx, cx, Wy, cy);
   return cudaGetLastError();
 }
 

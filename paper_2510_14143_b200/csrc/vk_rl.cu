@@ -213,6 +213,7 @@ struct vk_rl_plan_s {
   bool ztma = false, otma = false, ytma = false;
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
   int blk_lb = 0;
+  int ycrop = 0;  // crop offset of the y inverse: g.cy, or 0 when folded into the OTFs as a ramp
   bool tma_store = true;  // TMA/bulk stores of the z tile and y-forward lines (VK_RL_NO_TMA_STORE=1: thread stores)  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
   CUtensorMap zmap{}, omap{}, omap_flip{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
@@ -419,7 +420,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
     launch(p->fy->ybk, dim3(nkb * a.bz), p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
   } else if (p->fy)
   {
-    a.bst = p->tma_store && mode == vk::YM_FWD && out_off % 2 == 0 && out_pitch % 2 == 0 && n_out % 2 == 0 &&
+    a.bst = p->tma_store && out_off % 2 == 0 && out_pitch % 2 == 0 && n_out % 2 == 0 &&
             (reinterpret_cast<uintptr_t>(out) & 15) == 0;
     if (p->ytma && n_in % 2 == 0 && in_pitch % 2 == 0)
       launch(p->fy->ytk, grid, p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
@@ -562,12 +563,12 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
     return;
   }
   if (g.Wz == 1) {
-    y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, g.cy, p->SA.p, p->SA.p, otf);
+    y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, p->ycrop, p->SA.p, p->SA.p, otf);
     return;
   }
   y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
-  y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, g.cy, p->SB.p, p->SA.p, nullptr);
+  y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr);
 }
 
 // One half-iteration of the z-chunked schedule: z convolution of the whole
@@ -580,7 +581,7 @@ void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, fl
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
   for (int z0 = 0; z0 < g.Pz; z0 += p->zchunk) {
     const int zn = std::min(p->zchunk, g.Pz - z0);
-    y_pass(p, s, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, g.cy, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
+    y_pass(p, s, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
     x_pass(p, s, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, acc, out, 0, z0, zn);
     if (fwd_after)
       y_pass(p, s, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
@@ -981,6 +982,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
     if (p->df) setup_dataflow(p);
     p->stats.alloc(1, "stats");
+    p->ycrop = g.cy;  // until the OTF ramp below folds it in
 
     // Both spectra: psf and std::reverse(psf) == flip about every axis.
     std::vector<float> flipped(psf, psf + kn);
@@ -1012,10 +1014,17 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     ck(cudaMemcpyAsync(dpsf.p, flipped.data(), kn * sizeof(float), cudaMemcpyHostToDevice, p->stream),
        "psf H2D");
     build_otf(p, dpsf.p, p->otf_flip.p);
-    if (p->fx && g.cx != 0) {  // the fast x-pass keeps rows at [cx, cx+Px): crop as a phase ramp
+    // The fast x-pass keeps rows at [cx, cx+Px): the x crop is a phase ramp.
+    // Where the y inverse bulk-stores its lines (ypass_tma), the y crop is one
+    // too, so the cropped lines start at slot 0 (16-byte aligned); C2 y inverse
+    // -10% (profiles/r01/final/tst.log).
+    const bool yramp = p->fy && p->ytma && p->tma_store && !p->df && !p->cl && g.cy != 0;
+    p->ycrop = yramp ? 0 : g.cy;
+    const int cxr = p->fx ? g.cx : 0, cyr = yramp ? g.cy : 0;
+    if (cxr != 0 || cyr != 0) {
       const size_t plane = (size_t)g.Wz * g.Wy;
-      ck(vk::launch_otf_ramp(p->otf.p, g.Hx, plane, g.Wx, g.cx, p->stream), "otf ramp");
-      ck(vk::launch_otf_ramp(p->otf_flip.p, g.Hx, plane, g.Wx, g.cx, p->stream), "otf ramp");
+      ck(vk::launch_otf_ramp(p->otf.p, g.Hx, plane, g.Wx, cxr, g.Wy, cyr, p->stream), "otf ramp");
+      ck(vk::launch_otf_ramp(p->otf_flip.p, g.Hx, plane, g.Wx, cxr, g.Wy, cyr, p->stream), "otf ramp");
     }
     ck(cudaStreamSynchronize(p->stream), "otf_flip");
     p->launches = 0;
