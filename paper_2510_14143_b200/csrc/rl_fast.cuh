@@ -25,6 +25,20 @@ namespace vk {
 
 using reg::sw;
 
+// Reciprocal / natural log of a NORMAL float (the ratio's max(model, 1e-12)):
+// the .ftz approximations, without the denormal-range fix-ups __fdividef /
+// __logf carry (same values for normal inputs; 2 ulp / 2^-21 abs as before).
+__device__ __forceinline__ float rcp_n(float x) {
+  float r;
+  asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r;
+}
+__device__ __forceinline__ float log_n(float x) {
+  float r;
+  asm("lg2.approx.ftz.f32 %0, %1;" : "=f"(r) : "f"(x));
+  return r * 0.693147180559945309f;
+}
+
 __host__ __device__ constexpr int ilog2(int v) { return v <= 1 ? 0 : 1 + ilog2(v / 2); }
 
 __device__ __forceinline__ void cp_async8(void* smem_dst, const void* gsrc) {
@@ -217,6 +231,20 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
         }
       }
     }
+    // per-row offsets / flags of the epilogue, once per CTA (visible after
+    // the transform's barriers): observed row (clamped = edge replicate),
+    // estimate row, bit 0 row exists (y < Py), bit 1 row inside the image
+    __shared__ unsigned s_oo[2 * L], s_eo[2 * L];
+    __shared__ unsigned char s_fl[2 * L];
+    if (threadIdx.x < 2 * L) {
+      const int r = threadIdx.x, y = y0 + r;
+      const bool v = y < g.Py;
+      const int iy = y - g.oy, iz = z - g.oz;
+      const bool in = v && iz >= 0 && iz < g.Iz && iy >= 0 && iy < g.Iy;
+      s_oo[r] = ((unsigned)clampi(iz, 0, g.Iz - 1) * g.Iy + clampi(iy, 0, g.Iy - 1)) * (unsigned)g.Ix;
+      s_eo[r] = ((unsigned)z * g.Py + (v ? y : 0)) * (unsigned)g.Px;
+      s_fl[r] = (v ? 1 : 0) | (in ? 2 : 0);
+    }
     __syncthreads();
     reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, tw);
 
@@ -238,23 +266,17 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
       ch -= nch;
       ++l;
     }
-    const int iz = z - g.oz;
-    const bool zin = iz >= 0 && iz < g.Iz;
-    const size_t zoff = (size_t)clampi(iz, 0, g.Iz - 1) * g.Iy;
     for (; l < L; ch += NW) {
       while (ch >= nch) {
         ch -= nch;
         ++l;
       }
       if (l >= L) break;
-      const int ya = y0 + l, yb = y0 + L + l;
-      const bool va = ya < g.Py, vb = yb < g.Py;
-      const int iya = ya - g.oy, iyb = yb - g.oy;
-      const bool ina = va && zin && iya >= 0 && iya < g.Iy, inb = vb && zin && iyb >= 0 && iyb < g.Iy;
-      const size_t oa_off = (zoff + clampi(iya, 0, g.Iy - 1)) * g.Ix;
-      const size_t ob_off = (zoff + clampi(iyb, 0, g.Iy - 1)) * g.Ix;
-      float* ea = a.est + ((size_t)z * g.Py + (va ? ya : 0)) * g.Px;
-      float* eb = a.est + ((size_t)z * g.Py + (vb ? yb : 0)) * g.Px;
+      const int fa = s_fl[l], fb = s_fl[L + l];
+      const bool va = fa & 1, vb = fb & 1, ina = fa & 2, inb = fb & 2;
+      const unsigned oa_off = s_oo[l], ob_off = s_oo[L + l];
+      float* ea = a.est + s_eo[l];
+      float* eb = a.est + s_eo[L + l];
       if (ch >= nci) {
         // pad columns: x in [0, ox) and [ox+Ix, Px)
         const int p = (ch - nci) * 32 + lane;
@@ -266,8 +288,8 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
           const float2 m = A[sidx];
           float2 val;
           if (ratio) {
-            val = make_float2(va ? __fdividef(__ldg(a.obs + oa_off + xo), fmaxf(m.x, kEps)) : 0.f,
-                              vb ? __fdividef(__ldg(a.obs + ob_off + xo), fmaxf(m.y, kEps)) : 0.f);
+            val = make_float2(va ? __ldg(a.obs + oa_off + xo) * rcp_n(fmaxf(m.x, kEps)) : 0.f,
+                              vb ? __ldg(a.obs + ob_off + xo) * rcp_n(fmaxf(m.y, kEps)) : 0.f);
           } else {
             val = make_float2(va ? fmaxf(ea[x] * m.x, 0.f) : 0.f, vb ? fmaxf(eb[x] * m.y, 0.f) : 0.f);
             if (!last) {
@@ -308,9 +330,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
             // fast reciprocal/log (<= 2 ulp / 2^-21 abs): the f32 path's own
             // rounding (~1e-7 rel) dominates either way
             const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
-            val = make_float2(__fdividef(o_a[u], ma), __fdividef(o_b[u], mb));
-            fa0 += fmaf(o_a[u], __logf(ma), -ma);
-            fb0 += fmaf(o_b[u], __logf(mb), -mb);
+            val = make_float2(o_a[u] * rcp_n(ma), o_b[u] * rcp_n(mb));
+            fa0 += fmaf(o_a[u], log_n(ma), -ma);
+            fb0 += fmaf(o_b[u], log_n(mb), -mb);
           } else {
             val = make_float2(fmaxf(e_a[u] * m[u].x, 0.f), fmaxf(e_b[u] * m[u].y, 0.f));
             if (!last) {
@@ -365,9 +387,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
           float2 val;
           if (ratio) {
             const float ma = fmaxf(m[u].x, kEps), mb = fmaxf(m[u].y, kEps);
-            val = make_float2(va ? __fdividef(o_a[u], ma) : 0.f, vb ? __fdividef(o_b[u], mb) : 0.f);
-            fa0 += fmaf(o_a[u], __logf(ma), -ma);
-            fb0 += fmaf(o_b[u], __logf(mb), -mb);
+            val = make_float2(va ? o_a[u] * rcp_n(ma) : 0.f, vb ? o_b[u] * rcp_n(mb) : 0.f);
+            fa0 += fmaf(o_a[u], log_n(ma), -ma);
+            fb0 += fmaf(o_b[u], log_n(mb), -mb);
           } else {
             val = make_float2(fmaxf(e_a[u] * m[u].x, 0.f), fmaxf(e_b[u] * m[u].y, 0.f));
             if (!last) {
@@ -407,9 +429,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
           float2 val;
           if (ratio) {
             const float ma = fmaxf(m.x, kEps), mb = fmaxf(m.y, kEps);
-            val = make_float2(va ? __fdividef(o_a, ma) : 0.f, vb ? __fdividef(o_b, mb) : 0.f);
-            if (ina) acc0 += fmaf(o_a, __logf(ma), -ma);
-            if (inb) acc0 += fmaf(o_b, __logf(mb), -mb);
+            val = make_float2(va ? o_a * rcp_n(ma) : 0.f, vb ? o_b * rcp_n(mb) : 0.f);
+            if (ina) acc0 += fmaf(o_a, log_n(ma), -ma);
+            if (inb) acc0 += fmaf(o_b, log_n(mb), -mb);
           } else {
             val = make_float2(va ? fmaxf(ea2[u * 32] * m.x, 0.f) : 0.f, vb ? fmaxf(eb2[u * 32] * m.y, 0.f) : 0.f);
             if (!last) {
