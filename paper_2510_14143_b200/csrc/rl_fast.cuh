@@ -99,13 +99,13 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
   float2* A = TWG ? smem : smem + N;
   pdl_trigger();
   if (!TWG) reg::load_twiddles2<R1, R2>(smem, a.plan.tw);  // constant table: before the wait
-  pdl_wait();
   const int z = blockIdx.y + a.zoff;
   const int y0 = blockIdx.x * 2 * L;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const Geom& g = a.g;
 
   if (a.mode == XM_FWD) {
+    pdl_wait();
     // real rows (l, L+l) -> line l, samples at slots [xoff, xoff+len)
     const int nch = (N + CH - 1) / CH;
     for (int item = warp; item < L * nch; item += NW) {
@@ -169,6 +169,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
         }
       }
     }
+    // the prefetches are hints (L2 is coherent): issued before the wait, they
+    // overlap the previous pass's tail
+    pdl_wait();
     if (a.lb) {
       // kx-blocked S_A: work item i = (kb, l, k), k fastest, so a warp reads
       // 32*8 contiguous bytes of rows l (and of rows L+l)
