@@ -1,5 +1,5 @@
 set -x
-D=gpurun_out/r01j; mkdir -p $D
+D=gpurun_out/r01o; mkdir -p $D
 nvidia-smi --query-gpu=name,clocks.sm,clocks.max.sm,temperature.gpu,power.draw --format=csv > $D/smi.txt
 timeout 400 python bench.py > $D/bench_c2.json 2> $D/bench_c2.err
 for c in c1 c3 c4 c5; do timeout 500 python bench.py --config $c > $D/bench_$c.json 2> $D/bench_$c.err; done
