@@ -44,7 +44,6 @@ FastEntry make_entry() {
   if constexpr (YTMA) {
     e.ytk = (const void*)ypass_tma<R1, R2, LY, TWG>;
     e.smem_yt = (size_t)(LY * YTma<R1 * R2, LY>::NP + (TWG ? 0 : ((R1 * R2 + 1) / 2) * 2)) * sizeof(float2);
-    if constexpr (LY >= 2 && LY <= 8) e.ybk = (const void*)ypass_blk<R1, R2, LY, TWG>;
   }
   if constexpr (ZTMA > 0 && LZ == 16) {
     e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;

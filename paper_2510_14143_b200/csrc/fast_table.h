@@ -39,7 +39,6 @@ struct FastEntry {
   size_t smem_zt;
   const void* ytk;      // ypass_tma<R1,R2,Ly>(YArgs): bulk-copied lines (FWD/INV), or nullptr
   size_t smem_yt;
-  const void* ybk;      // ypass_blk<R1,R2,Ly>(YArgs): y pass against the kx-blocked S_A (smem_yt), or nullptr
 };
 
 const FastEntry* fast_lookup(int n);

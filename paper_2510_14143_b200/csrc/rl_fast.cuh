@@ -137,15 +137,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
     // L2 prefetch at entry: every load round of this CTA after the first, and
     // the epilogue's observed / estimate rows, then hit L2 instead of HBM (the
     // epilogue walks its rows in ~12 dependent load rounds per warp).
-    if ((a.pf & 1) && a.lb) {  // kx-blocked: one 2L*B*8-byte piece per block
-      const unsigned plane = (unsigned)g.Pz * g.Py;
-      const float2* base = a.S + (((unsigned)z * g.Py + y0) << a.lb);
-      const int per = (2 * L) << a.lb >> 4, nkb = (Hx + (1 << a.lb) - 1) >> a.lb;  // 128-byte lines per block
-      for (int i = threadIdx.x; i < nkb * per; i += NT) {
-        const int kb = i / per, q = i - kb * per;
-        if (y0 + ((q * 16) >> a.lb) < g.Py) prefetch_l2(base + (((unsigned)kb * plane) << a.lb) + q * 16);
-      }
-    } else if (a.pf & 1) {
+    if (a.pf & 1) {
       const unsigned plane = (unsigned)g.Pz * g.Py;
       const float2* base = a.S + (unsigned)z * g.Py + y0;
       for (int i = threadIdx.x; i < 2 * Hx; i += NT)
@@ -172,40 +164,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
     // the prefetches are hints (L2 is coherent): issued before the wait, they
     // overlap the previous pass's tail
     pdl_wait();
-    if (a.lb) {
-      // kx-blocked S_A: work item i = (kb, l, k), k fastest, so a warp reads
-      // 32*8 contiguous bytes of rows l (and of rows L+l)
-      constexpr int LL = ilog2(L);
-      const int lb = a.lb, B = 1 << lb;
-      const unsigned plane = (unsigned)g.Pz * g.Py;
-      const float2* S0 = a.S + (((unsigned)z * g.Py + y0) << lb);
-      const int total = ((Hx + B - 1) >> lb) << (lb + LL);
-      for (int i0 = threadIdx.x; i0 < total; i0 += NT * U) {
-        float2 xa[U], xb[U];
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * NT;
-          const int k = i & (B - 1), l = (i >> lb) & (L - 1), kb = i >> (lb + LL);
-          const bool ok = i < total && (kb << lb) + k < Hx;
-          const unsigned off = (((unsigned)kb * plane) << lb) + (l << lb) + k;
-          xa[u] = (ok && y0 + l < g.Py) ? S0[off] : zero;
-          xb[u] = (ok && y0 + L + l < g.Py) ? S0[off + (L << lb)] : zero;
-        }
-#pragma unroll
-        for (int u = 0; u < U; ++u) {
-          const int i = i0 + u * NT;
-          const int k = i & (B - 1), l = (i >> lb) & (L - 1), kb = i >> (lb + LL);
-          const int kx = (kb << lb) + k;
-          if (i >= total || kx >= Hx) continue;
-          if (kx == 0 || 2 * kx == N) {
-            A[sw<L>(kx, l)] = make_float2(xa[u].x, xb[u].x);
-          } else {
-            A[sw<L>(kx, l)] = make_float2(xa[u].x - xb[u].y, xa[u].y + xb[u].x);
-            A[sw<L>(N - kx, l)] = make_float2(xa[u].x + xb[u].y, xb[u].x - xa[u].y);
-          }
-        }
-      }
-    } else {
+    {
       const int l = threadIdx.x & (L - 1);
       const int ya = y0 + l, yb = y0 + L + l;
       const bool va = ya < g.Py, vb = yb < g.Py;
@@ -475,23 +434,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, tw);
-  if (a.lb) {  // kx-blocked S_A, items (kb, l, k) as in the loads
-    constexpr int LL = ilog2(L);
-    const int lb = a.lb, B = 1 << lb;
-    const unsigned plane = (unsigned)a.rows_z * a.rows_y;
-    float2* S0 = a.S + (((unsigned)z * a.rows_y + y0) << lb);
-    const int total = ((Hx + B - 1) >> lb) << (lb + LL);
-    for (int i = threadIdx.x; i < total; i += NT) {
-      const int k = i & (B - 1), l = (i >> lb) & (L - 1), kb = i >> (lb + LL);
-      const int kx = (kb << lb) + k;
-      if (kx >= Hx) continue;
-      const float2 zk = A[sw<L>(kx, l)];
-      const float2 zn = A[sw<L>(kx == 0 ? 0 : N - kx, l)];
-      const unsigned off = (((unsigned)kb * plane) << lb) + (l << lb) + k;
-      if (y0 + l < a.rows_y) S0[off] = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
-      if (y0 + L + l < a.rows_y) S0[off + (L << lb)] = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
-    }
-  } else {
+  {
     constexpr int KS = NT / L;
     const int l = threadIdx.x & (L - 1);
     const bool va = y0 + l < a.rows_y, vb = y0 + L + l < a.rows_y;
@@ -883,72 +826,6 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
   for (int l = 0; l < nvalid; ++l) {
     float2* out = a.out + (size_t)y_line(a, line0 + l) * a.out_pitch;
     for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[l * NP + j + a.out_off];
-  }
-}
-
-// y pass against the kx-blocked S_A ([Hx/L][bz][rows][L], see XArgs::lb):
-// CTA = (kx block kb, z row), its L lines are kx = kb*L + l.
-//  FWD: the block's rows are ONE contiguous bulk copy (n_in*L*8 bytes) into
-//       an interleaved tile [i][l] (no pad: a warp's pass-1 loads and pass-2
-//       accesses cover 4 consecutive rows = 2 wavefronts); the L output
-//       lines go to S_B [Hx][bz][Wy].
-//  INV: the L input lines of S_B are bulk-copied line-major as in
-//       ypass_tma; the cropped output is written as the contiguous
-//       [n_out][L] block of S_A (zeros for kx >= Hx).
-template <int R1, int R2, int L, bool TWG>
-__global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_blk(const YArgs a) {
-  static_assert(L >= 2 && L <= 8, "16-byte aligned blocks and rows: 2 <= L <= 8");
-  constexpr int N = R1 * R2, NT = FastCfg<R1, R2, L, true>::NT, NP = YTma<N, L>::NP;
-  extern __shared__ __align__(128) float2 smem[];
-  float2* tw = TWG ? nullptr : smem;
-  float2* A = TWG ? smem : smem + ((N + 1) / 2) * 2;  // keep 16-byte alignment
-  __shared__ uint64_t bar;
-  const int nz = a.bz;
-  const int kb = blockIdx.x / nz, z = blockIdx.x - kb * nz;
-  const int kx0 = kb * L;
-  const int nvalid = min(L, a.nlines / nz - kx0);
-  if (threadIdx.x == 0) {
-    mbar_init(&bar, 1);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  }
-  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
-  const float2* twp = TWG ? a.plan.tw2 : tw;
-  __syncthreads();
-  pdl_trigger();
-  pdl_wait();
-  if (a.mode == YM_FWD) {
-    if (threadIdx.x == 0) {
-      const unsigned bytes = (unsigned)(a.n_in * L * sizeof(float2));
-      mbar_expect_tx(&bar, bytes);
-      bulk_load(A, a.in + ((size_t)kb * nz + z) * a.in_pitch * L, bytes, &bar);
-    }
-    for (int idx = a.n_in * L + threadIdx.x; idx < N * L; idx += NT) A[idx] = make_float2(0.f, 0.f);
-    mbar_wait(&bar, 0);
-    __syncthreads();
-    reg::fft2<R1, R2, L, NT, false, L, TWG, 1>(A, twp);
-    for (int idx = threadIdx.x; idx < L * a.n_out; idx += NT) {
-      const int l = idx % L, j = idx / L;
-      if (l < nvalid) a.out[((size_t)(kx0 + l) * nz + z) * a.out_pitch + j] = A[(j + a.out_off) * L + l];
-    }
-  } else {
-    if (threadIdx.x == 0) {
-      mbar_expect_tx(&bar, (unsigned)(nvalid * a.n_in * sizeof(float2)));
-      for (int l = 0; l < nvalid; ++l)
-        bulk_load(A + l * NP, a.in + ((size_t)(kx0 + l) * nz + z) * a.in_pitch, (unsigned)(a.n_in * sizeof(float2)),
-                  &bar);
-    }
-    for (int idx = threadIdx.x; idx < L * N; idx += NT) {
-      const int l = idx / N, i = idx - l * N;
-      if (l >= nvalid || i >= a.n_in) A[l * NP + i] = make_float2(0.f, 0.f);
-    }
-    mbar_wait(&bar, 0);
-    __syncthreads();
-    reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
-    float2* out = a.out + ((size_t)kb * nz + z) * a.out_pitch * L;
-    for (int idx = threadIdx.x; idx < L * a.n_out; idx += NT) {
-      const int l = idx % L, y = idx / L;
-      out[idx] = l < nvalid ? A[l * NP + y + a.out_off] : make_float2(0.f, 0.f);
-    }
   }
 }
 

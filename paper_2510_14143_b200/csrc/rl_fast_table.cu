@@ -100,8 +100,6 @@ cudaError_t fast_init_attributes() {
       return r;
     if (e.ytk && (r = cudaFuncSetAttribute(e.ytk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yt)))
       return r;
-    if (e.ybk && (r = cudaFuncSetAttribute(e.ybk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yt)))
-      return r;
     // prefer the full shared-memory carveout: occupancy is smem-limited
     for (const void* k : {e.xk, e.yk, e.zk, e.zpk})
       if ((r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100))) return r;

@@ -10,11 +10,6 @@
 //                      contiguous (Hx = Wx/2+1).  Only the Pz*Py rows that carry
 //                      data exist: rows outside P are zero before the forward
 //                      transform and cropped away after the inverse.
-//                      Fast 3D plans block it by kx instead:
-//                      [ceil(Hx/B)][Pz][Py][B] (B = the y pass's lines per
-//                      CTA), so an x-pass CTA's 16 rows are one contiguous
-//                      16*B*8-byte piece per kx block and a y-pass CTA's B
-//                      lines are one contiguous Py*B*8-byte bulk copy.
 //   S_B [Hx][Pz][Wy]   after the y transform (3D only).
 //   OTF [Hx][Wz][Wy]   PSF spectrum, 1/prod(W) folded in (fft_plan.cpp:95-96).
 //
@@ -71,7 +66,6 @@ struct XArgs {
   float* out;           // UPDATE_LAST: cropped f32 estimate [Iz][Iy][Ix]
   int zoff;             // first z row of this launch (z-chunked iterations)
   int pf;               // fast path: L2 prefetch of the CTA's inputs at entry (1 spectrum, 2 rows)
-  int lb;               // fast path: S is kx-blocked [ceil(Hx/B)][rows_z][rows_y][B], B = 1 << lb (0: [Hx][..][..])
 };
 
 struct YArgs {
@@ -87,9 +81,6 @@ struct YArgs {
   // z-chunked passes (zcn > 0): the nlines = Hx * zcn lines are (kx, z) with
   // z in [zc0, zc0 + zcn) of zrows rows per kx plane
   int zc0, zcn, zrows;
-  // kx-blocked S_A side (ypass_blk, lb > 0): S_A holds [Hx/B][bz][rows][B]
-  // with B = 1 << lb = the pass's lines per CTA; CTA = (kx block, z row)
-  int lb, bz;
   int bst;  // ypass_tma FWD: bulk-store each output line (16-byte aligned lines only)
 };
 

@@ -212,7 +212,6 @@ struct vk_rl_plan_s {
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
   bool ztma = false, otma = false, ytma = false;
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
-  int blk_lb = 0;
   int ycrop = 0;  // crop offset of the y inverse: g.cy, or 0 when folded into the OTFs as a ramp
   bool tma_store = true;  // TMA/bulk stores of the z tile and y-forward lines (VK_RL_NO_TMA_STORE=1: thread stores)  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
   CUtensorMap zmap{}, omap{}, omap_flip{};
@@ -376,7 +375,6 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   a.acc = acc;
   a.out = out;
   a.pf = p->xpf;
-  a.lb = p->blk_lb;
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
@@ -412,13 +410,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   dim3 grid((nlines + a.L - 1) / a.L);
   const int kind = mode == vk::YM_FWD ? VK_KIND_Y_FWD : mode == vk::YM_INV ? VK_KIND_Y_INV : VK_KIND_Y_CONV;
   const size_t t = prof_begin(p, s);
-  if (p->blk_lb && (in == p->SA.p || out == p->SA.p)) {  // kx-blocked S_A side (ypass_blk)
-    if (zcn || mode == vk::YM_CONV || nlines % p->g.Hx) fail(VK_ERR_CUDA, "internal: blocked y pass shape");
-    a.lb = p->blk_lb;
-    a.bz = nlines / p->g.Hx;
-    const int nkb = (p->g.Hx + a.L - 1) / a.L;
-    launch(p->fy->ybk, dim3(nkb * a.bz), p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
-  } else if (p->fy)
+  if (p->fy)
   {
     a.bst = p->tma_store && out_off % 2 == 0 && out_pitch % 2 == 0 && n_out % 2 == 0 &&
             (reinterpret_cast<uintptr_t>(out) & 15) == 0;
@@ -935,21 +927,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     const char* noyt = std::getenv("VK_RL_NO_YTMA");
     const char* notma0 = std::getenv("VK_RL_NO_TMA");
     p->ytma = p->fy && p->fy->ytk && !(notma0 && notma0[0] == '1') && !(noyt && noyt[0] == '1');
-    // kx-blocked S_A (XArgs::lb, opt-in VK_RL_BLK=1): fast x and y passes,
-    // 3D, the plain 3-pass y/z schedule; not for slabs (their halo exchange
-    // copies kx-plane rows) or conv plans.  Measured slower: C2 1.124 vs
-    // 1.060 ms per iteration (y fwd 0.215 vs 0.156: pass-1 stores of the
-    // unpadded interleaved tile conflict 2-way and the output lines are
-    // written in 32-byte pieces; the x passes did not gain), C4 3.28 vs 3.16
-    // (profiles/r01/final/blk.log).
-    {
-      const char* bk = std::getenv("VK_RL_BLK");
-      if (p->fx && p->fy && p->fz && p->fy->ybk && p->ytma && g.Wz > 1 && !p->df && !p->cl && !p->zchunk &&
-          !conv && !zslab && bk && bk[0] == '1')
-        p->blk_lb = __builtin_ctz((unsigned)p->fy->Ly);
-    }
-    const size_t hxb = ((size_t)g.Hx + (1u << p->blk_lb) - 1) >> p->blk_lb << p->blk_lb;
-    const size_t sa = hxb * std::max(g.Pz, p->Kz) * std::max(g.Py, p->Ky);
+    const size_t sa = (size_t)g.Hx * std::max(g.Pz, p->Kz) * std::max(g.Py, p->Ky);
     const size_t sb = (size_t)g.Hx * std::max(g.Pz, p->Kz) * g.Wy;
     const size_t so = (size_t)g.Hx * g.Wz * g.Wy;
     // the pass kernels index spectra and the padded domain with 32-bit offsets
@@ -957,7 +935,6 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       fail(VK_ERR_UNSUPPORTED, "volume too large for one plan (spectrum >= 2^32 elements): split it into slabs "
                                "(vk_rl_slab_plan_create)");
     p->SA.alloc(sa, "spectrum A");
-    if (p->blk_lb) ck(cudaMemset(p->SA.p, 0, sa * sizeof(float2)), "memset");  // kx >= Hx stays defined
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
     // TMA-staged z tile (zpass_tma) where the length has one and the box
     // fits (Pz <= 256): C2 z convolutions 0.313 vs 0.345 ms per iteration
@@ -1627,7 +1604,6 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
     if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
     if (p->ztma) s += " z:tma";
     if (p->ytma) s += " y:bulk";
-    if (p->blk_lb) s += " S_A:kx-blocked(" + std::to_string(1 << p->blk_lb) + ")";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
     buf[len - 1] = 0;
   });
