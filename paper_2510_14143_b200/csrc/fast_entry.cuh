@@ -16,14 +16,17 @@ namespace vk {
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
           bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0,
           int ZTMA = 0,  // ZTMA: resident-CTA floor of the TMA z kernel (0 = no TMA variant)
-          bool YTMA = false>
+          bool YTMA = false,
+          bool XTMA = false>  // XTMA: TMA-staged RATIO/UPDATE x pass (xpass_tma)
 FastEntry make_entry() {
   constexpr int LY = LY0 ? LY0 : LX;  // y-pass lines per CTA (default: the x pass's)
   FastEntry e{};
   e.N = R1 * R2;
   e.pdl = PDL;
   e.R1 = R1;
-  e.smem_xp = TWG ? FastCfg<R1, R2, LX>::smem_x : FastCfg<R1, R2, LX>::smem;
+  // x pass: the transform tile, after the shared twiddle table rounded up to
+  // 128 bytes when there is one (TMA destinations)
+  e.smem_xp = FastCfg<R1, R2, LX>::smem_x + (TWG ? 0 : (size_t)((R1 * R2 + 15) / 16 * 16) * sizeof(float2));
   e.Lx = LX;
   e.NTx = FastCfg<R1, R2, LX>::NT;
   e.smem_x = FastCfg<R1, R2, LX>::smem;
@@ -33,6 +36,7 @@ FastEntry make_entry() {
   e.smem_yconv = (size_t)(FastCfg<R1, R2, LY, true>::DATA + (TWG ? 0 : R1 * R2) + (YPREF ? R1 * R2 * LY : 0)) *
                  sizeof(float2);
   e.xk = (const void*)xpass_fast<R1, R2, LX, TWG, XMINB, XPB>;
+  if constexpr (XTMA) e.xtk = (const void*)xpass_tma<R1, R2, LX, TWG, XMINB, XPB>;
   e.yk = (const void*)ypass_fast<R1, R2, LY, TWG, YPREF>;
   e.Lz = LZ;
   e.NTz = FastCfg<R1, R2, LZ, true>::NT;

@@ -19,6 +19,13 @@ struct alignas(64) ZTmaArgs {
   int tma_store;  // write the cropped tile back with one TMA tensor store (same map)
 };
 
+// Kernel argument of xpass_tma: the S_A tensor map {Py, Pz, Hx}, box
+// {2L, 1, tbk} (8-byte elements), and the usual x-pass arguments.
+struct alignas(64) XTmaArgs {
+  CUtensorMap map;
+  XArgs x;
+};
+
 struct FastEntry {
   int N, R1;            // N = R1 * R2 (pass-1 / pass-2 radices)
   bool pdl;             // launch with programmatic dependent launch
@@ -29,6 +36,7 @@ struct FastEntry {
   size_t smem_x;        // x-pass, and y-pass FWD/INV
   size_t smem_yconv;    // y-pass CONV (adds the prefetched OTF tile)
   const void* xk;       // xpass_fast<R1,R2,Lx>(XArgs)
+  const void* xtk;      // xpass_tma<R1,R2,Lx>(XTmaArgs): TMA-staged spectrum rows (RATIO/UPDATE)
   const void* yk;       // ypass_fast<R1,R2,Lx>(YArgs)
   int Lz, NTz;          // z-pass
   size_t smem_z;

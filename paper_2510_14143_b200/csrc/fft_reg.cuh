@@ -191,7 +191,24 @@ __device__ __forceinline__ int sw(int i, int l) {
 // Element (i, l) lives at buf[i * LP + l * LS]: LS = 1 is the interleaved
 // layout (LP = L+1 pad, or LP = L for 16-lane rows); LP = 1 with LS = row
 // pitch is the line-major layout bulk copies land in.
-template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1, bool TWG = false, int LS = 1>
+// C2R input of line l, sample i, read from the x pass's TMA-staged spectrum
+// tile st = [k][2L] (k = kx <= N/2, rows 2l / 2l+1 = the line's real and
+// imaginary halves, one 16-byte pair): Z[i] = Xa[i] + i Xb[i] for i <= N/2,
+// conj(Xa[N-i]) + i conj(Xb[N-i]) above; DC / Nyquist imaginary parts
+// dropped as FFTW's c2r does.
+template <int N, int L>
+__device__ __forceinline__ float2 c2r_staged(const float2* st, int i, int l) {
+  const bool hi = 2 * i > N;
+  const int k = hi ? N - i : i;
+  const float4 p = reinterpret_cast<const float4*>(st)[k * L + l];
+  if (k == 0 || 2 * k == N) return make_float2(p.x, p.z);
+  return hi ? make_float2(p.x + p.w, p.z - p.y) : make_float2(p.x - p.w, p.y + p.z);
+}
+
+// STG: pass 1 gathers its inputs with c2r_staged from the staged tile that
+// occupies the front of `buf` (all reads complete before the barrier that
+// precedes the first store, so the tile may alias the transform buffer).
+template <int R1, int R2, int L, int NT, bool INV, int LP = L + 1, bool TWG = false, int LS = 1, bool STG = false>
 __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
   static_assert(NT >= L * R2, "pass 1 needs one butterfly per thread");
 #ifdef VK_DEBUG_NOFFT  // experiment builds only: isolate the memory cost of a pass
@@ -203,7 +220,12 @@ __device__ __forceinline__ void fft2(float2* buf, const float2* tw) {
     const int l = t % L, j = t / L;
     const bool act = t < L * R2;
     float2 v[R1];
-    if (act) static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l * LS]; });
+    if (act) {
+      if constexpr (STG)
+        static_for<0, R1>([&](auto r) { v[decltype(r)::value] = c2r_staged<R1 * R2, L>(buf, j + decltype(r)::value * R2, l); });
+      else
+        static_for<0, R1>([&](auto r) { v[decltype(r)::value] = buf[(j + decltype(r)::value * R2) * LP + l * LS]; });
+    }
     __syncthreads();
     if (act) {
       rdft<R1, INV>(v);

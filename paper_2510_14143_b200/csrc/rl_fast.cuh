@@ -52,6 +52,51 @@ __device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commi
 __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;\n" ::: "memory"); }
 __device__ __forceinline__ void cp_async_wait_1() { asm volatile("cp.async.wait_group 1;\n" ::: "memory"); }
 
+// mbarrier / TMA helpers (tx-count completion, bulk and tensor copies)
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
+  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
+               "r"((unsigned)__cvta_generic_to_shared(smem_src)), "r"(c0), "r"(c1), "r"(c2)
+               : "memory");
+}
+__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, unsigned bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
+               "r"((unsigned)__cvta_generic_to_shared(smem_src)), "r"(bytes)
+               : "memory");
+}
+// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
+__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void bulk_commit_and_wait() {
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
+                                            int c2) {
+  asm volatile(
+      "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(smem_dst)),
+      "l"(map), "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(c0), "r"(c1), "r"(c2)
+      : "memory");
+}
+
 // Programmatic dependent launch: the host launches the fast pass kernels
 // with cudaLaunchAttributeProgrammaticStreamSerialization.  Each grid lets
 // the next one launch as soon as all of its CTAs are resident (the next
@@ -85,18 +130,26 @@ struct FastCfg {
 // MINB: resident CTAs per SM the register allocation must allow.  PB: the
 // partial-chunk epilogue batches its loads like the full one (worth its
 // registers only where partial chunks are common, e.g. Ix = 1000).
-template <int R1, int R2, int L, bool TWG, int MINB, bool PB>
-__global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB)  // 1: leave the heuristic alone
-    xpass_fast(const XArgs a) {
+//
+// Row pairing: the CTA's 2L rows y0 .. y0+2L-1 are packed as line l = rows
+// (y0+2l, y0+2l+1), so both halves of a line are adjacent in S_A (one
+// 16-byte access) and in the TMA-staged tile.
+// STAGED (xpass_tma, RATIO/UPDATE): the CTA's spectrum rows arrive as TMA
+// boxes {2L rows, 1, BK kx} of the tensor S_A {Py, Pz, Hx} -- a dense [kx][2L]
+// tile in the same shared buffer -- and the C2R transform's first pass reads
+// the Hermitian pairs straight from it (reg::fft2 STG), so there is no pack
+// phase and no per-thread global load of the spectrum.
+template <int R1, int R2, int L, bool TWG, bool PB, bool STAGED>
+__device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xmap) {
   using C = FastCfg<R1, R2, L>;
   constexpr int N = C::N, NT = C::NT;
   constexpr int Hx = N / 2 + 1;
   constexpr int NW = NT / 32;
   constexpr int U = 4;
   constexpr int CH = 32 * U;  // samples per work item
-  extern __shared__ float2 smem[];
+  extern __shared__ __align__(128) float2 smem[];
   const float2* tw = TWG ? a.plan.tw2 : smem;
-  float2* A = TWG ? smem : smem + N;
+  float2* A = TWG ? smem : smem + (N + 15) / 16 * 16;  // 128-byte aligned (TMA boxes land here)
   pdl_trigger();
   if (!TWG) reg::load_twiddles2<R1, R2>(smem, a.plan.tw);  // constant table: before the wait
   const int z = blockIdx.y + a.zoff;
@@ -106,11 +159,11 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
 
   if (a.mode == XM_FWD) {
     pdl_wait();
-    // real rows (l, L+l) -> line l, samples at slots [xoff, xoff+len)
+    // real rows (2l, 2l+1) -> line l, samples at slots [xoff, xoff+len)
     const int nch = (N + CH - 1) / CH;
     for (int item = warp; item < L * nch; item += NW) {
       const int l = item / nch, x0 = (item % nch) * CH;
-      const int ya = y0 + l, yb = y0 + L + l;
+      const int ya = y0 + 2 * l, yb = ya + 1;
       const bool va = ya < a.rows_y, vb = yb < a.rows_y;
       const float* ra = a.src + ((size_t)z * a.rows_y + (va ? ya : 0)) * a.len;
       const float* rb = a.src + ((size_t)z * a.rows_y + (vb ? yb : 0)) * a.len;
@@ -129,15 +182,23 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
       }
     }
   } else {
-    // Hermitian halves of row pair (l, L+l) -> Z[k] = Xa[k] + i Xb[k], k < N.
+    // Hermitian halves of row pair (2l, 2l+1) -> Z[k] = Xa[k] + i Xb[k], k < N.
     // NT is a multiple of L, so a thread keeps one line l and strides kx by
     // NT/L; spectrum offsets are 32-bit and incremental.
     constexpr int KS = NT / L;  // kx stride per thread
     const float2 zero = make_float2(0.f, 0.f);
+    __shared__ uint64_t xbar;
+    if (STAGED) {
+      if (threadIdx.x == 0) {
+        mbar_init(&xbar, 1);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+      }
+      __syncthreads();
+    }
     // L2 prefetch at entry: every load round of this CTA after the first, and
     // the epilogue's observed / estimate rows, then hit L2 instead of HBM (the
     // epilogue walks its rows in ~12 dependent load rounds per warp).
-    if (a.pf & 1) {
+    if (a.pf & 1) {  // (also ahead of the TMA boxes: issued before the PDL wait)
       const unsigned plane = (unsigned)g.Pz * g.Py;
       const float2* base = a.S + (unsigned)z * g.Py + y0;
       for (int i = threadIdx.x; i < 2 * Hx; i += NT)
@@ -164,9 +225,16 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
     // the prefetches are hints (L2 is coherent): issued before the wait, they
     // overlap the previous pass's tail
     pdl_wait();
-    {
+    if (STAGED) {
+      // rows [y0, y0+2L) of kx in [b*BK, b*BK+BK): box b lands at A + b*BK*2L;
+      // rows >= Py and kx >= Hx arrive as zeros (TMA out-of-bounds fill)
+      if (threadIdx.x == 0) {
+        mbar_expect_tx(&xbar, (unsigned)(a.tnb * a.tbk * 2 * L * sizeof(float2)));
+        for (int b = 0; b < a.tnb; ++b) tma_load_3d(A + b * a.tbk * 2 * L, xmap, &xbar, y0, z, b * a.tbk);
+      }
+    } else {
       const int l = threadIdx.x & (L - 1);
-      const int ya = y0 + l, yb = y0 + L + l;
+      const int ya = y0 + 2 * l, yb = ya + 1;
       const bool va = ya < g.Py, vb = yb < g.Py;
       const float2* Sa = a.S + ((unsigned)z * g.Py + (va ? ya : 0));
       const float2* Sb = a.S + ((unsigned)z * g.Py + (vb ? yb : 0));
@@ -207,8 +275,9 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
       s_eo[r] = ((unsigned)z * g.Py + (v ? y : 0)) * (unsigned)g.Px;
       s_fl[r] = (v ? 1 : 0) | (in ? 2 : 0);
     }
+    if (STAGED) mbar_wait(&xbar, 0);
     __syncthreads();
-    reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, tw);
+    reg::fft2<R1, R2, L, NT, true, L + 1, TWG, 1, STAGED>(A, tw);
 
     const bool last = a.mode == XM_UPDATE_LAST;
     const bool ratio = a.mode == XM_RATIO;
@@ -234,11 +303,11 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
         ++l;
       }
       if (l >= L) break;
-      const int fa = s_fl[l], fb = s_fl[L + l];
+      const int fa = s_fl[2 * l], fb = s_fl[2 * l + 1];
       const bool va = fa & 1, vb = fb & 1, ina = fa & 2, inb = fb & 2;
-      const unsigned oa_off = s_oo[l], ob_off = s_oo[L + l];
-      float* ea = a.est + s_eo[l];
-      float* eb = a.est + s_eo[L + l];
+      const unsigned oa_off = s_oo[2 * l], ob_off = s_oo[2 * l + 1];
+      float* ea = a.est + s_eo[2 * l];
+      float* eb = a.est + s_eo[2 * l + 1];
       if (ch >= nci) {
         // pad columns: x in [0, ox) and [ox+Ix, Px)
         const int p = (ch - nci) * 32 + lane;
@@ -437,19 +506,38 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB) 
   {
     constexpr int KS = NT / L;
     const int l = threadIdx.x & (L - 1);
-    const bool va = y0 + l < a.rows_y, vb = y0 + L + l < a.rows_y;
-    float2* Sa = a.S + ((unsigned)z * a.rows_y + y0 + l);
-    float2* Sb = Sa + L;
+    const int ya = y0 + 2 * l;
+    const bool va = ya < a.rows_y, vb = ya + 1 < a.rows_y;
+    // rows (2l, 2l+1) adjacent: one 16-byte store when rows_y is even
+    const bool vec = vb && (a.rows_y & 1) == 0;
+    float2* Sa = a.S + ((unsigned)z * a.rows_y + ya);
     const unsigned plane = (unsigned)a.rows_z * a.rows_y;
     for (int kx = group_remap<L>(threadIdx.x / L, KS); kx < Hx; kx += KS) {
       const float2 zk = A[sw<L>(kx, l)];
       const float2 zn = A[sw<L>(kx == 0 ? 0 : N - kx, l)];
       const float2 xa = make_float2(0.5f * (zk.x + zn.x), 0.5f * (zk.y - zn.y));
       const float2 xb = make_float2(0.5f * (zk.y + zn.y), -0.5f * (zk.x - zn.x));
-      if (va) Sa[(unsigned)kx * plane] = xa;
-      if (vb) Sb[(unsigned)kx * plane] = xb;
+      float2* d = Sa + (unsigned)kx * plane;
+      if (vec) {
+        *reinterpret_cast<float4*>(d) = make_float4(xa.x, xa.y, xb.x, xb.y);
+      } else {
+        if (va) d[0] = xa;
+        if (vb) d[1] = xb;
+      }
     }
   }
+}
+
+template <int R1, int R2, int L, bool TWG, int MINB, bool PB>
+__global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB)  // 1: leave the heuristic alone
+    xpass_fast(const __grid_constant__ XArgs a) {
+  xpass_body<R1, R2, L, TWG, PB, false>(a, nullptr);
+}
+
+template <int R1, int R2, int L, bool TWG, int MINB, bool PB>
+__global__ void __launch_bounds__(FastCfg<R1, R2, L>::NT, MINB == 1 ? 0 : MINB)
+    xpass_tma(const __grid_constant__ XTmaArgs t) {
+  xpass_body<R1, R2, L, TWG, PB, true>(t.x, &t.map);
 }
 
 // PREF: the CONV mode stages the OTF tile in shared memory with cp.async
@@ -618,50 +706,6 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT, MINB == 1 ? 0 : 
 // needed at L = 16).  Rows Pz..N-1 are zeroed by the other threads while the
 // copy flies.  The OTF is read from global in the multiply.
 // (ZTmaArgs: fast_table.h)
-
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((unsigned)__cvta_generic_to_shared(bar)), "r"(count)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
-                   (unsigned)__cvta_generic_to_shared(bar)),
-               "r"(bytes)
-               : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned phase) {
-  asm volatile(
-      "{\n\t.reg .pred p;\n\t"
-      "WAIT_%=:\n\t"
-      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-      "@!p bra WAIT_%=;\n\t}" ::"r"((unsigned)__cvta_generic_to_shared(bar)),
-      "r"(phase)
-      : "memory");
-}
-__device__ __forceinline__ void tma_store_3d(const CUtensorMap* map, const void* smem_src, int c0, int c1, int c2) {
-  asm volatile("cp.async.bulk.tensor.3d.global.shared::cta.bulk_group [%0, {%2, %3, %4}], [%1];" ::"l"(map),
-               "r"((unsigned)__cvta_generic_to_shared(smem_src)), "r"(c0), "r"(c1), "r"(c2)
-               : "memory");
-}
-__device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, unsigned bytes) {
-  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(gdst),
-               "r"((unsigned)__cvta_generic_to_shared(smem_src)), "r"(bytes)
-               : "memory");
-}
-// generic-proxy shared-memory writes -> visible to the async (TMA) proxy
-__device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void bulk_commit_and_wait() {
-  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
-}
-__device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
-                                            int c2) {
-  asm volatile(
-      "cp.async.bulk.tensor.3d.shared::cta.global.mbarrier::complete_tx::bytes [%0], [%1, {%3, %4, %5}], [%2];" ::"r"(
-          (unsigned)__cvta_generic_to_shared(smem_dst)),
-      "l"(map), "r"((unsigned)__cvta_generic_to_shared(bar)), "r"(c0), "r"(c1), "r"(c2)
-      : "memory");
-}
 
 template <int R1, int R2, bool TWG, int MINB>
 __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 : MINB)

@@ -93,6 +93,8 @@ cudaError_t fast_init_attributes() {
   for (const auto& e : kTable) {
     cudaError_t r;
     if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_xp))) return r;
+    if (e.xtk && (r = cudaFuncSetAttribute(e.xtk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_xp)))
+      return r;
     if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yconv))) return r;
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
     if ((r = cudaFuncSetAttribute(e.zpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zp))) return r;
@@ -101,8 +103,8 @@ cudaError_t fast_init_attributes() {
     if (e.ytk && (r = cudaFuncSetAttribute(e.ytk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yt)))
       return r;
     // prefer the full shared-memory carveout: occupancy is smem-limited
-    for (const void* k : {e.xk, e.yk, e.zk, e.zpk})
-      if ((r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100))) return r;
+    for (const void* k : {e.xk, e.xtk, e.yk, e.zk, e.zpk})
+      if (k && (r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100))) return r;
   }
   return cudaSuccess;
 }

@@ -66,6 +66,7 @@ struct XArgs {
   float* out;           // UPDATE_LAST: cropped f32 estimate [Iz][Iy][Ix]
   int zoff;             // first z row of this launch (z-chunked iterations)
   int pf;               // fast path: L2 prefetch of the CTA's inputs at entry (1 spectrum, 2 rows)
+  int tbk, tnb;         // xpass_tma: kx per TMA box, boxes per CTA
 };
 
 struct YArgs {

@@ -212,7 +212,10 @@ struct vk_rl_plan_s {
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
   bool ztma = false, otma = false, ytma = false;
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
-  int ycrop = 0;  // crop offset of the y inverse: g.cy, or 0 when folded into the OTFs as a ramp
+  int ycrop = 0;
+  bool xtma = false;  // xpass_tma for the RATIO/UPDATE x passes (S_A rows staged by TMA)
+  CUtensorMap xmap{};
+  int xtbk = 0, xtnb = 0;  // crop offset of the y inverse: g.cy, or 0 when folded into the OTFs as a ramp
   bool tma_store = true;  // TMA/bulk stores of the z tile and y-forward lines (VK_RL_NO_TMA_STORE=1: thread stores)  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
   CUtensorMap zmap{}, omap{}, omap_flip{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
@@ -378,7 +381,14 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
-  if (p->fx)
+  if (p->fx && p->xtma && mode != vk::XM_FWD) {
+    vk::XTmaArgs ta{};
+    ta.map = p->xmap;
+    a.tbk = p->xtbk;
+    a.tnb = p->xtnb;
+    ta.x = a;
+    launch(p->fx->xtk, grid, p->fx->NTx, p->fx->smem_xp, s, &ta, p->fx->pdl);
+  } else if (p->fx)
     launch(p->fx->xk, grid, p->fx->NTx, p->fx->smem_xp, s, &a, p->fx->pdl);
   else
     vk::xpass_kernel<<<grid, kThreads, p->xs, s>>>(a);
@@ -687,6 +697,39 @@ bool encode_zmap(vk_rl_plan p, int zrows) {
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// S_A [Hx][Pz][Py] as {Py, Pz, Hx}, box {2L rows, 1, tbk kx} for xpass_tma:
+// nb = ceil(Hx / 256) boxes of tbk kx each, tbk a multiple of 128 / (16 L)
+// so every box lands 128-byte aligned; the staged tile must fit the x tile.
+bool encode_xmap(vk_rl_plan p) {
+  using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                                const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                                CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+  void* f = nullptr;
+  cudaDriverEntryPointQueryResult q{};
+  if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &f, cudaEnableDefault, &q) != cudaSuccess ||
+      q != cudaDriverEntryPointSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  const Geom& g = p->g;
+  const int L = p->fx->Lx;
+  if (g.Py % 2 || 2 * L > 256) return false;  // global strides must be multiples of 16 bytes
+  const int nb = (g.Hx + 255) / 256, m = std::max(1, 128 / (16 * L));
+  const int bk = ((g.Hx + nb - 1) / nb + m - 1) / m * m;
+  if (bk > 256 || (size_t)nb * bk * 2 * L > (size_t)g.Wx * (L + 1)) return false;
+  const cuuint64_t dims[3] = {(cuuint64_t)g.Py, (cuuint64_t)g.Pz, (cuuint64_t)g.Hx};
+  const cuuint64_t strides[2] = {(cuuint64_t)g.Py * 8, (cuuint64_t)g.Pz * g.Py * 8};
+  const cuuint32_t box[3] = {(cuuint32_t)(2 * L), 1, (cuuint32_t)bk};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  if (((EncodeFn)f)(&p->xmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, p->SA.p, dims, strides, box, estr,
+                    CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                    CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) != CUDA_SUCCESS)
+    return false;
+  p->xtbk = bk;
+  p->xtnb = nb;
+  return true;
+}
+
 // OTF [Hx][Wz][Wy] as {Wy, Wz, Hx}, box {16, Wz, 1}.
 bool encode_otf_map(vk_rl_plan p, void* base, CUtensorMap* m) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
@@ -935,6 +978,12 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       fail(VK_ERR_UNSUPPORTED, "volume too large for one plan (spectrum >= 2^32 elements): split it into slabs "
                                "(vk_rl_slab_plan_create)");
     p->SA.alloc(sa, "spectrum A");
+    // TMA-staged x passes (xpass_tma) wherever the fast x pass runs and S_A's
+    // rows are 16-byte multiples; VK_RL_NO_XTMA=1 keeps the per-thread loads
+    if (p->fx && p->fx->xtk) {
+      const char* nx = std::getenv("VK_RL_NO_XTMA");
+      p->xtma = !(nx && nx[0] == '1') && encode_xmap(p);
+    }
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
     // TMA-staged z tile (zpass_tma) where the length has one and the box
     // fits (Pz <= 256): C2 z convolutions 0.313 vs 0.345 ms per iteration
@@ -1604,6 +1653,7 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
     if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
     if (p->ztma) s += " z:tma";
     if (p->ytma) s += " y:bulk";
+    if (p->xtma) s += " x:tma";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
     buf[len - 1] = 0;
   });
