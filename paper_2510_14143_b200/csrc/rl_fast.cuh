@@ -239,14 +239,22 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
       const float2* Sa = a.S + ((unsigned)z * g.Py + (va ? ya : 0));
       const float2* Sb = a.S + ((unsigned)z * g.Py + (vb ? yb : 0));
       const unsigned plane = (unsigned)g.Pz * g.Py;
+      const bool vec = (g.Py & 1) == 0;  // then vb == va (ya even)
       for (int kx0 = group_remap<L>(threadIdx.x / L, KS); kx0 < Hx; kx0 += KS * U) {
         float2 xa[U], xb[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
           const int kx = kx0 + u * KS;
           const bool ok = kx < Hx;
-          xa[u] = (ok && va) ? Sa[(unsigned)kx * plane] : zero;
-          xb[u] = (ok && vb) ? Sb[(unsigned)kx * plane] : zero;
+          if (vec) {  // rows 2l, 2l+1 adjacent and 16-byte aligned: one load
+            const float4 v = (ok && va) ? *reinterpret_cast<const float4*>(Sa + (unsigned)kx * plane)
+                                        : make_float4(0.f, 0.f, 0.f, 0.f);
+            xa[u] = make_float2(v.x, v.y);
+            xb[u] = make_float2(v.z, v.w);
+          } else {
+            xa[u] = (ok && va) ? Sa[(unsigned)kx * plane] : zero;
+            xb[u] = (ok && vb) ? Sb[(unsigned)kx * plane] : zero;
+          }
         }
 #pragma unroll
         for (int u = 0; u < U; ++u) {
