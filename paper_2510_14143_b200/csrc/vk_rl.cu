@@ -1479,13 +1479,11 @@ int lane_count(vk_rl_plan p, int n) {
   if (env && std::atoi(env) > 0) {
     want = std::atoi(env);
   } else {
-    // measured on B200 (profiles/r01/lanes.log): C3 (64^3-class volumes)
-    // 1/2/3/4 lanes = 2.08/2.78/2.83/2.81e10, C5 (2048^2 fields) 1/2/4/6 =
-    // 2.69/3.06/2.84/2.81e10 voxel-iters/s
-    const Geom& g = p->g;
-    const int L = p->fx ? p->fx->Lx : p->xL;
-    const long long ctas = (long long)((g.Py + 2 * L - 1) / (2 * L)) * g.Pz;
-    want = (p->rank == 3 && ctas < 148 * 16) ? 3 : 2;
+    // measured on B200 with the current kernels (profiles/r01/final/lanes_*.json):
+    // C3 (64x256x256 volumes) 2/3/4 lanes = 3.58/3.36/3.33e10, C5 (2048^2
+    // fields) 1/2/3/4 = 3.07/3.57/3.70/3.54e10 voxel-iters/s.  (With the
+    // round's first kernels, profiles/r01/lanes.log, C3 peaked at 3 lanes.)
+    want = p->rank == 2 ? 3 : 2;
   }
   return std::max(1, std::min(want, n));
 }
