@@ -401,7 +401,7 @@ def test_batch_device_lanes_match_single_runs(lanes):
             # the metric sums use FP64 atomics: order-dependent in the last bits
             np.testing.assert_allclose([r.value for r in tr.records], [r.value for r in sgl.trace.records],
                                        rtol=1e-12)
-        assert plan.lanes() == (int(lanes) if lanes else 2)  # 2D default
+        assert plan.lanes() == (int(lanes) if lanes else 3)  # 2D default
         assert plan.launches() > 7 * 5 * 4  # every lane's launches are counted
         host = plan.run_batch(vols, rule)  # the host batch uses the lanes too
         for sgl, h in zip(single, host):
