@@ -252,6 +252,11 @@ struct vk_rl_plan_s {
   int acc_cap = 0;
 
   cudaStream_t stream = nullptr;
+  // z-chunked schedule on two streams (VK_RL_ZSTREAMS=2): odd chunks run on
+  // stream2, forked after the z pass and joined before the next one
+  int zstreams = 1;
+  cudaStream_t stream2 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> events;
   double* h_acc = nullptr;  // pinned
   uint64_t launches = 0;
@@ -275,6 +280,9 @@ struct vk_rl_plan_s {
     for (auto e : prof_pool) cudaEventDestroy(e);
     if (h_acc) cudaFreeHost(h_acc);
     if (stream) cudaStreamDestroy(stream);
+    if (stream2) cudaStreamDestroy(stream2);
+    if (ev_fork) cudaEventDestroy(ev_fork);
+    if (ev_join) cudaEventDestroy(ev_join);
     if (h_frc) cudaFreeHost(h_frc);
     delete frc;
   }
@@ -581,12 +589,28 @@ void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, fl
                   double* acc, float* out, bool fwd_after) {
   const Geom& g = p->g;
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
-  for (int z0 = 0; z0 < g.Pz; z0 += p->zchunk) {
+  const bool two = p->zstreams > 1;
+  if (two) {
+    if (!p->stream2) {
+      ck(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "event");
+      ck(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "event");
+    }
+    ck(cudaEventRecord(p->ev_fork, s), "event");
+    ck(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0), "wait");
+  }
+  int c = 0;
+  for (int z0 = 0; z0 < g.Pz; z0 += p->zchunk, ++c) {
     const int zn = std::min(p->zchunk, g.Pz - z0);
-    y_pass(p, s, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
-    x_pass(p, s, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, acc, out, 0, z0, zn);
+    cudaStream_t cs = two && (c & 1) ? p->stream2 : s;
+    y_pass(p, cs, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
+    x_pass(p, cs, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, acc, out, 0, z0, zn);
     if (fwd_after)
-      y_pass(p, s, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
+      y_pass(p, cs, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
+  }
+  if (two) {
+    ck(cudaEventRecord(p->ev_join, p->stream2), "event");
+    ck(cudaStreamWaitEvent(s, p->ev_join, 0), "wait");
   }
 }
 
@@ -950,6 +974,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     if (zc && p->fx && p->fy && p->fz && g.Wz > 1 && !p->df && !p->cl && !conv && !zslab) {
       const int rows = std::atoi(zc);
       p->zchunk = rows > 0 && rows < g.Pz ? rows : 0;
+      if (const char* zs2 = std::getenv("VK_RL_ZSTREAMS")) p->zstreams = std::max(1, std::atoi(zs2));
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);

@@ -258,7 +258,8 @@ def test_opt_in_schedules_match_default():
     its, _ = run_oracle(obs, psf, 3)
     assert rel_l2(ref.estimate, its[-1]) <= TOL_1
     for env, tag in (({"VK_RL_NO_TMA": "1"}, None), ({"VK_RL_ZPIPE": "1", "VK_RL_NO_TMA": "1"}, None),
-                     ({"VK_RL_ZCHUNK": "24"}, "zchunk"), ({"VK_RL_NO_XTMA": "1"}, None),
+                     ({"VK_RL_ZCHUNK": "24"}, "zchunk"), ({"VK_RL_ZCHUNK": "40", "VK_RL_ZSTREAMS": "2"}, "zchunk"),
+                     ({"VK_RL_NO_XTMA": "1"}, None),
                      ({"VK_RL_NO_TMA_STORE": "1"}, None)):
         got = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule))
         assert rel_l2(got.estimate, ref.estimate) <= 1e-6, env
