@@ -22,12 +22,15 @@ FastEntry fast_entry_192() { return make_entry<12, 16, 16, 16, false, true, 1, f
 FastEntry fast_entry_256() { return make_entry<16, 16, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(); }  // 256 (y bulk L=8)
 #elif VK_LEN == 288
 // 288: TMA-staged x pass (C1 x passes 0.0730 vs 0.0753 ms per iteration; at
-// 576 / 1080 / 2160 it loses: profiles/r01/final/xtma.log)
+// 576 / 2160 it loses: profiles/r01/final/xtma.log)
 FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
 #elif VK_LEN == 576
 FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(); }  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
 #elif VK_LEN == 1080
-FastEntry fast_entry_1080() { return make_entry<30, 36, 8, 4, false, true, 1, true, false, true, 1, true, 2, 4, 0, true>(); }  // 1080 (Ix = 1000: partial chunks are common)
+// 1080: TMA-staged x pass with a 2-CTA register floor (96 regs, 80 B stack;
+// without the floor the staged loads take 129 registers and 1 CTA/SM): C4
+// 2.884 vs 2.940 ms per iteration (profiles/r01/final/x1080.log)
+FastEntry fast_entry_1080() { return make_entry<30, 36, 8, 4, false, true, 2, true, false, true, 1, true, 2, 4, 0, true, true>(); }  // 1080 (Ix = 1000: partial chunks are common)
 #elif VK_LEN == 2160
 // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
 // in griddepcontrol.wait would hold the scarce slots the batch lanes'
