@@ -22,7 +22,7 @@ FastEntry fast_entry_192() { return make_entry<12, 16, 16, 16, false, true, 1, f
 FastEntry fast_entry_256() { return make_entry<16, 16, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true>(); }  // 256 (y bulk L=8)
 #elif VK_LEN == 288
 // 288: TMA-staged x pass (C1 x passes 0.0730 vs 0.0753 ms per iteration; at
-// 576 / 2160 it loses: profiles/r01/final/xtma.log)
+// 576 it loses: profiles/r01/final/xtma.log)
 FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
 #elif VK_LEN == 576
 FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(); }  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
@@ -35,7 +35,9 @@ FastEntry fast_entry_1080() { return make_entry<30, 36, 8, 4, false, true, 2, tr
 // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
 // in griddepcontrol.wait would hold the scarce slots the batch lanes'
 // kernels need: C5 3.05e10 without vs 2.66e10 with, profiles/r01/pdl.log)
-FastEntry fast_entry_2160() { return make_entry<45, 48, 4, 2, true, false, 1, false, false, true, 1, false, 2, 2, 0, true>(); }  // y L=2
+// and the TMA-staged x pass with a 2-CTA register floor (168 regs, 48 B
+// stack): C5 x passes 0.0774 vs 0.0801 ms per field-iteration (final/x2160.log)
+FastEntry fast_entry_2160() { return make_entry<45, 48, 4, 2, true, false, 2, false, false, true, 1, false, 2, 2, 0, true, true>(); }  // y L=2
 #else
 #error "no fast-table entry for VK_LEN"
 #endif
