@@ -196,29 +196,39 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
     // L2 prefetch at entry: every load round of this CTA after the first, and
     // the epilogue's observed / estimate rows, then hit L2 instead of HBM (the
     // epilogue walks its rows in ~12 dependent load rounds per warp).
-    if (a.pf & 1) {  // (also ahead of the TMA boxes: issued before the PDL wait)
-      const unsigned plane = (unsigned)g.Pz * g.Py;
-      const float2* base = a.S + (unsigned)z * g.Py + y0;
-      for (int i = threadIdx.x; i < 2 * Hx; i += NT)
-        if (y0 + (i & 1) * L < g.Py) prefetch_l2(base + (unsigned)(i >> 1) * plane + (i & 1) * L);
-    }
-    if (a.pf & 2) {
-      const int iz = clampi(z - g.oz, 0, g.Iz - 1);
-      const int nlo = (g.Ix + 31) / 32 + 1, nle = (g.Px + 31) / 32 + 1;
-      const bool upd = a.mode != XM_RATIO;
-      const int per = nlo + (upd ? nle : 0);
-      for (int i = threadIdx.x; i < 2 * L * per; i += NT) {
-        const int r = i / per, k = i - r * per;
-        const int y = min(y0 + r, g.Py - 1);
-        if (k < nlo) {
-          const int iy = clampi(y - g.oy, 0, g.Iy - 1);
-          const float* row = a.obs + ((size_t)iz * g.Iy + iy) * g.Ix;
-          prefetch_l2(row + min(k * 32, g.Ix - 1));
-        } else {
-          const float* row = a.est + ((size_t)z * g.Py + y) * g.Px;
-          prefetch_l2(row + min((k - nlo) * 32, g.Px - 1));
+    auto prefetch_tile = [&](const int zz, const int yy0, const int mask) {
+      if (mask & 1) {  // (also ahead of the TMA boxes: issued before the PDL wait)
+        const unsigned plane = (unsigned)g.Pz * g.Py;
+        const float2* base = a.S + (unsigned)zz * g.Py + yy0;
+        for (int i = threadIdx.x; i < 2 * Hx; i += NT)
+          if (yy0 + (i & 1) * L < g.Py) prefetch_l2(base + (unsigned)(i >> 1) * plane + (i & 1) * L);
+      }
+      if (mask & 2) {
+        const int iz = clampi(zz - g.oz, 0, g.Iz - 1);
+        const int nlo = (g.Ix + 31) / 32 + 1, nle = (g.Px + 31) / 32 + 1;
+        const bool upd = a.mode != XM_RATIO;
+        const int per = nlo + (upd ? nle : 0);
+        for (int i = threadIdx.x; i < 2 * L * per; i += NT) {
+          const int r = i / per, k = i - r * per;
+          const int y = min(yy0 + r, g.Py - 1);
+          if (k < nlo) {
+            const int iy = clampi(y - g.oy, 0, g.Iy - 1);
+            const float* row = a.obs + ((size_t)iz * g.Iy + iy) * g.Ix;
+            prefetch_l2(row + min(k * 32, g.Ix - 1));
+          } else {
+            const float* row = a.est + ((size_t)zz * g.Py + y) * g.Px;
+            prefetch_l2(row + min((k - nlo) * 32, g.Px - 1));
+          }
         }
       }
+    };
+    prefetch_tile(z, y0, a.pf & 3);
+    // look-ahead (bits 4, 8): the tile of the CTA about one resident wave
+    // later in launch order (a.pfd blocks on), so its loads hit L2 as well
+    if ((a.pf & 12) && a.pfd > 0) {
+      const unsigned id = blockIdx.y * gridDim.x + blockIdx.x + (unsigned)a.pfd;
+      if (id < gridDim.x * gridDim.y)
+        prefetch_tile((int)(id / gridDim.x) + a.zoff, (int)(id % gridDim.x) * 2 * L, (a.pf >> 2) & 3);
     }
     // the prefetches are hints (L2 is coherent): issued before the wait, they
     // overlap the previous pass's tail

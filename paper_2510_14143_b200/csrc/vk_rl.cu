@@ -212,6 +212,7 @@ struct vk_rl_plan_s {
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
   bool ztma = false, otma = false, ytma = false;
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
+  int xpfd = 0;  // x-pass look-ahead distance in blocks (XArgs::pfd)
   int ycrop = 0;
   bool xtma = false;  // xpass_tma for the RATIO/UPDATE x passes (S_A rows staged by TMA)
   CUtensorMap xmap{};
@@ -386,6 +387,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   a.acc = acc;
   a.out = out;
   a.pf = p->xpf;
+  a.pfd = p->xpfd;
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
@@ -1021,6 +1023,16 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->xpf = g.Wz > 1 ? 3 : 0;
     if (const char* nts = std::getenv("VK_RL_NO_TMA_STORE")) p->tma_store = nts[0] != '1';
     if (const char* xpf = std::getenv("VK_RL_XPF")) p->xpf = std::atoi(xpf);
+    if (p->fx && (p->xpf & 12)) {  // look-ahead: one resident wave of x-pass CTAs
+      int dev = 0, nsm = 0, per = 0;
+      const void* k = p->fx->xtk && p->xtma ? p->fx->xtk : p->fx->xk;
+      if (cudaGetDevice(&dev) == cudaSuccess &&
+          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
+          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, p->fx->NTx, p->fx->smem_xp) == cudaSuccess)
+        p->xpfd = per * nsm;
+      cudaGetLastError();
+      if (const char* d = std::getenv("VK_RL_XPFD")) p->xpfd = std::atoi(d);
+    }
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     p->otf.alloc(so, "otf");
