@@ -247,7 +247,8 @@ def test_opt_in_schedules_match_default():
     """Schedule variants against each other on a 192-point z grid: the
     TMA-staged z tile (default there) vs cp.async (VK_RL_NO_TMA), the
     TMA-staged 288-point x pass vs per-thread loads (VK_RL_NO_XTMA), TMA/bulk
-    stores vs thread stores (VK_RL_NO_TMA_STORE), and the opt-in pipelined z
+    stores vs thread stores (VK_RL_NO_TMA_STORE), the look-ahead x-pass L2
+    prefetch (VK_RL_XPF=15), and the opt-in pipelined z
     (VK_RL_ZPIPE) and z-chunked schedule (VK_RL_ZCHUNK)."""
     psf = O.gaussian_psf((15, 15, 15), 1.75)
     obs = synth.blurred(synth.blobs((160, 256, 256), 60, 5, 9, seed=12), psf)  # W = 192 x 288 x 288
@@ -260,7 +261,8 @@ def test_opt_in_schedules_match_default():
     for env, tag in (({"VK_RL_NO_TMA": "1"}, None), ({"VK_RL_ZPIPE": "1", "VK_RL_NO_TMA": "1"}, None),
                      ({"VK_RL_ZCHUNK": "24"}, "zchunk"), ({"VK_RL_ZCHUNK": "40", "VK_RL_ZSTREAMS": "2"}, "zchunk"),
                      ({"VK_RL_NO_XTMA": "1"}, None),
-                     ({"VK_RL_NO_TMA_STORE": "1"}, None)):
+                     ({"VK_RL_NO_TMA_STORE": "1"}, None),
+                     ({"VK_RL_XPF": "15"}, None)):  # look-ahead prefetch: hints only
         got = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule))
         assert rel_l2(got.estimate, ref.estimate) <= 1e-6, env
         if tag:
