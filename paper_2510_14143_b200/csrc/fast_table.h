@@ -17,6 +17,9 @@ struct alignas(64) ZTmaArgs {
   ZArgs z;
   int otf_tma;
   int tma_store;  // write the cropped tile back with one TMA tensor store (same map)
+  // factored OTF of a separable PSF: fx[Hx], fy[Wy], fz[Wz] back to back,
+  // O(kx, kz, ky) = (fx[kx] * fy[ky]) * fz[kz]; nullptr: read the OTF
+  const float2* ofac;
 };
 
 // Kernel argument of xpass_tma: the S_A tensor map {Py, Pz, Hx}, box

@@ -774,7 +774,15 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false, L, TWG>(A, twp);
   const float2* og = otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
-  if (otma) {
+  if (ta.ofac) {  // separable PSF: rebuild the OTF column from its 1D factors
+    const float2* fz = ta.ofac + ta.z.hx + Wy;
+    const float2 c = kok ? cmul(__ldg(ta.ofac + kx), __ldg(ta.ofac + ta.z.hx + ky)) : make_float2(0.f, 0.f);
+#pragma unroll
+    for (int k = 0; k < IT; ++k) {
+      const int z = z0 + k * ZS;
+      if (z < N) A[z * L + l] = cmul(A[z * L + l], cmul(c, __ldg(fz + z)));
+    }
+  } else if (otma) {
     mbar_wait(&obar, 0);
 #pragma unroll
     for (int k = 0; k < IT; ++k) {

@@ -247,6 +247,8 @@ struct vk_rl_plan_s {
   size_t xs = 0, ys = 0, zs = 0;
 
   DevBuf<float2> SA, SB, otf, otf_flip;
+  DevBuf<float2> ofac;  // 1D factors of otf and otf_flip when both are separable (ZTmaArgs::ofac)
+  bool ofactored = false;
   DevBuf<float> est, obs, out;
   DevBuf<double> acc;
   DevBuf<vk::ObsStats> stats;
@@ -467,6 +469,11 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
     ta.z = a;
     ta.otf_tma = p->otma && (otf == p->otf.p || otf == p->otf_flip.p);
     ta.tma_store = p->tma_store && n_out == p->g.Pz;
+    if (p->ofactored) {
+      const size_t nf = (size_t)p->g.Hx + p->g.Wy + p->g.Wz;
+      ta.ofac = otf == p->otf.p ? p->ofac.p : otf == p->otf_flip.p ? p->ofac.p + nf : nullptr;
+      if (ta.ofac) ta.otf_tma = 0;
+    }
     if (ta.otf_tma) ta.omap = otf == p->otf.p ? p->omap : p->omap_flip;
     dim3 grid((p->g.Wy + 15) / 16, p->g.Hx);
     const size_t t = prof_begin(p, s);
@@ -637,6 +644,90 @@ void build_otf(vk_rl_plan p, const float* d_psf, float2* otf_dst) {
   const Geom& g = p->g;
   const float scale = (float)(1.0 / ((double)g.Wz * g.Wy * g.Wx));
   spectrum3d(p, p->stream, d_psf, p->Kz, p->Ky, p->Kx, scale, otf_dst);
+}
+
+// ---- factored OTF (separable PSF) ----------------------------------------
+// A separable PSF has a separable OTF; the per-axis crop ramps are separable
+// too.  Then O(kx, kz, ky) = O(kx,0,0) O(0,kz,0) O(0,0,ky) / O(0,0,0)^2, and
+// the TMA z pass rebuilds each OTF column from three 1D factors instead of
+// reading the OTF (C4: 673 MB per z launch).  The rank-1 property is TESTED
+// on the device OTF, not assumed from the PSF: max |O - product| must be
+// <= kOtfSepTol * max |O| for both OTFs.
+constexpr float kOtfSepTol = 4e-6f;
+
+__global__ void otf_factor_kernel(const float2* __restrict__ otf, int Hx, int Wz, int Wy, float2* __restrict__ fac) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t plane = (size_t)Wz * Wy;
+  if (i < Hx) {  // fx = O(kx,0,0) / O000^2, in double
+    const double2 o = make_double2(otf[0].x, otf[0].y);
+    const double2 o2 = make_double2(o.x * o.x - o.y * o.y, 2.0 * o.x * o.y);
+    const double d = o2.x * o2.x + o2.y * o2.y;
+    const float2 v = otf[(size_t)i * plane];
+    fac[i] = d > 0.0 ? make_float2((float)((v.x * o2.x + v.y * o2.y) / d), (float)((v.y * o2.x - v.x * o2.y) / d))
+                     : make_float2(0.f, 0.f);
+  } else if (i < Hx + Wy) {
+    fac[i] = otf[i - Hx];  // fy = O(0,0,ky)
+  } else if (i < Hx + Wy + Wz) {
+    fac[i] = otf[(size_t)(i - Hx - Wy) * Wy];  // fz = O(0,kz,0)
+  }
+}
+
+// bits[0] = max |O - (fx fy) fz|, bits[1] = max |O| (non-negative floats as uint)
+__global__ void otf_sep_check_kernel(const float2* __restrict__ otf, const float2* __restrict__ fac, int Hx, int Wz,
+                                     int Wy, unsigned* bits) {
+  const size_t n = (size_t)Hx * Wz * Wy;
+  const float2* fy = fac + Hx;
+  const float2* fz = fac + Hx + Wy;
+  float err = 0.f, mx = 0.f;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int ky = (int)(i % Wy);
+    const size_t r = i / Wy;
+    const int kz = (int)(r % Wz), kx = (int)(r / Wz);
+    const float2 o = otf[i];
+    const float2 q = vk::cmul(vk::cmul(fac[kx], fy[ky]), fz[kz]);
+    err = fmaxf(err, hypotf(o.x - q.x, o.y - q.y));
+    mx = fmaxf(mx, hypotf(o.x, o.y));
+  }
+  for (int m = 16; m > 0; m >>= 1) {
+    err = fmaxf(err, __shfl_xor_sync(0xffffffffu, err, m));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&bits[0], __float_as_uint(err));
+    atomicMax(&bits[1], __float_as_uint(mx));
+  }
+}
+
+// Sets p->ofactored when both OTFs pass the rank-1 test (VK_RL_NO_OTF_FACTOR=1
+// keeps the OTF reads).
+void factor_otfs(vk_rl_plan p) {
+  const char* no = std::getenv("VK_RL_NO_OTF_FACTOR");
+  if (no && no[0] == '1') return;
+  const Geom& g = p->g;
+  const size_t nf = (size_t)g.Hx + g.Wy + g.Wz;
+  p->ofac.alloc(2 * nf, "otf factors");
+  DevBuf<unsigned> bits;
+  bits.alloc(4, "otf check");
+  ck(cudaMemsetAsync(bits.p, 0, 4 * sizeof(unsigned), p->stream), "otf check");
+  const float2* o[2] = {p->otf.p, p->otf_flip.p};
+  for (int k = 0; k < 2; ++k) {
+    otf_factor_kernel<<<(unsigned)((nf + 255) / 256), 256, 0, p->stream>>>(o[k], g.Hx, g.Wz, g.Wy, p->ofac.p + k * nf);
+    launch_check(p, "otf factor");
+    otf_sep_check_kernel<<<148 * 8, 256, 0, p->stream>>>(o[k], p->ofac.p + k * nf, g.Hx, g.Wz, g.Wy, bits.p + 2 * k);
+    launch_check(p, "otf separability");
+  }
+  unsigned h[4];
+  ck(cudaMemcpyAsync(h, bits.p, sizeof(h), cudaMemcpyDeviceToHost, p->stream), "otf check D2H");
+  ck(cudaStreamSynchronize(p->stream), "otf check");
+  bool ok = true;
+  for (int k = 0; k < 2; ++k) {
+    float err, mx;
+    std::memcpy(&err, &h[2 * k], 4);
+    std::memcpy(&mx, &h[2 * k + 1], 4);
+    ok = ok && mx > 0.f && err <= kOtfSepTol * mx;
+  }
+  p->ofactored = ok;
+  if (!ok) p->ofac.free();
 }
 
 // Task list, ring and counters of the one-launch y/z convolution.  Lag D (in
@@ -1090,6 +1181,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       ck(vk::launch_otf_ramp(p->otf_flip.p, g.Hx, plane, g.Wx, cxr, g.Wy, cyr, p->stream), "otf ramp");
     }
     ck(cudaStreamSynchronize(p->stream), "otf_flip");
+    if (p->ztma) factor_otfs(p);
     p->launches = 0;
   } catch (...) {
     delete p;
@@ -1649,7 +1741,7 @@ vk_status vk_rl_plan_shapes(vk_rl_plan p, int* rank, uint64_t* image_shape, uint
 vk_status vk_rl_plan_device_bytes(vk_rl_plan p, uint64_t* bytes) {
   return guarded([&] {
     if (!p || !bytes) fail(VK_ERR_ARG, "NULL argument");
-    *bytes = (p->SA.n + p->SB.n + p->otf.n + p->otf_flip.n) * sizeof(float2) +
+    *bytes = (p->SA.n + p->SB.n + p->otf.n + p->otf_flip.n + p->ofac.n) * sizeof(float2) +
              (p->est.n + p->obs.n + p->out.n) * sizeof(float) + p->acc.n * sizeof(double) +
              p->ring.n * sizeof(float2) + (p->ss_img[0].n + p->ss_img[1].n) * sizeof(float) +
              (p->ss_f[0].n + p->ss_f[1].n + p->ss_sum.n) * sizeof(double) +
@@ -1687,6 +1779,7 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
       s += g.Wz > 1 ? "3-pass" : "y-conv";
     if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
     if (p->ztma) s += " z:tma";
+    if (p->ofactored) s += " otf:factored";
     if (p->ytma) s += " y:bulk";
     if (p->xtma) s += " x:tma";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);

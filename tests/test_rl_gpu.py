@@ -269,6 +269,27 @@ def test_opt_in_schedules_match_default():
             assert tag in _with_env(env, lambda: vk.RlPlan(obs.shape, psf)).describe()
 
 
+def test_factored_otf_separable_psf():
+    """Separable (Gaussian) PSF: the plan detects the rank-1 OTF and the TMA z
+    pass rebuilds OTF columns from 1D factors. Checked against the full-OTF
+    read (VK_RL_NO_OTF_FACTOR=1) and the oracle. The non-separable widefield
+    PSF must not be factored. The C4 regime uses a 144-point z grid."""
+    psf = O.gaussian_psf((21, 21, 21), 2.5)
+    obs = synth.blurred(synth.blobs((100, 240, 240), 40, 6, 10, seed=41), psf)  # W = 144 x 288 x 288
+    desc = vk.RlPlan(obs.shape, psf).describe()
+    assert "otf:factored" in desc and "z:tma" in desc, desc
+    rule = fixed_rule(5)
+    got = vk.richardson_lucy(obs, psf, rule)
+    full = _with_env({"VK_RL_NO_OTF_FACTOR": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    assert "otf:factored" not in _with_env({"VK_RL_NO_OTF_FACTOR": "1"},
+                                           lambda: vk.RlPlan(obs.shape, psf)).describe()
+    assert rel_l2(got.estimate, full.estimate) <= 1e-5
+    its, _ = run_oracle(obs, psf, 5)
+    assert rel_l2(got.estimate, its[-1]) <= TOL_1
+    wf = O.widefield_psf(31)
+    assert "otf:factored" not in vk.RlPlan((128, 40, 44), wf).describe()
+
+
 def test_frc_default_rule_c1():
     """The reference's DEFAULT rule (frc_resolution, 1e-3, patience 3) on the
     C1 shape: per-iteration FRC resolution on the device vs the oracle's
