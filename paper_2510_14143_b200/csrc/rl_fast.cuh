@@ -871,7 +871,16 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
     reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
   } else {
     reg::fft2<R1, R2, L, NT, false, 1, TWG, NP>(A, twp);
-    if (a.mode == YM_CONV) {  // 2D: x OTF (line-major reads, coalesced) then inverse
+    if (a.mode == YM_CONV && a.ofac) {  // 2D, separable OTF: rebuilt from its 1D factors
+      const float2* fy = a.ofac + a.ohx;
+      const float2 fz0 = __ldg(fy + N);
+      for (int l = 0; l < nvalid; ++l) {
+        const float2 c = __ldg(a.ofac + line0 + l);
+        for (int k = threadIdx.x; k < N; k += NT) A[l * NP + k] = cmul(A[l * NP + k], cmul(cmul(c, __ldg(fy + k)), fz0));
+      }
+      __syncthreads();
+      reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
+    } else if (a.mode == YM_CONV) {  // 2D: x OTF (line-major reads, coalesced) then inverse
       for (int l = 0; l < nvalid; ++l) {
         const float2* o = a.otf + (size_t)(line0 + l) * N;
         for (int k = threadIdx.x; k < N; k += NT) A[l * NP + k] = cmul(A[l * NP + k], __ldg(o + k));

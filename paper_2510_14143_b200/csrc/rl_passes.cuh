@@ -84,6 +84,10 @@ struct YArgs {
   // z in [zc0, zc0 + zcn) of zrows rows per kx plane
   int zc0, zcn, zrows;
   int bst;  // ypass_tma FWD: bulk-store each output line (16-byte aligned lines only)
+  // ypass_tma CONV (2D) with a separable OTF: fx[Hx], fy[Wy], fz[1] back to
+  // back (factor_otfs), O(kx, ky) = (fx[kx] * fy[ky]) * fz[0]; nullptr: read otf
+  const float2* ofac;
+  int ohx;
 };
 
 // Global line of a pass-local line index (identity unless z-chunked).

@@ -436,8 +436,14 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   {
     a.bst = p->tma_store && out_off % 2 == 0 && out_pitch % 2 == 0 && n_out % 2 == 0 &&
             (reinterpret_cast<uintptr_t>(out) & 15) == 0;
-    if (p->ytma && n_in % 2 == 0 && in_pitch % 2 == 0)
+    if (p->ytma && n_in % 2 == 0 && in_pitch % 2 == 0) {
+      if (mode == vk::YM_CONV && p->ofactored && p->g.Wz == 1 && a.zcn == 0) {
+        const size_t nf = (size_t)p->g.Hx + p->g.Wy + p->g.Wz;
+        a.ofac = otf == p->otf.p ? p->ofac.p : otf == p->otf_flip.p ? p->ofac.p + nf : nullptr;
+        a.ohx = p->g.Hx;
+      }
       launch(p->fy->ytk, grid, p->fy->NTy, p->fy->smem_yt, s, &a, p->fy->pdl);
+    }
     else
       launch(p->fy->yk, grid, p->fy->NTy, mode == vk::YM_CONV ? p->fy->smem_yconv : p->fy->smem_yp, s, &a,
              p->fy->pdl);
@@ -1181,7 +1187,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       ck(vk::launch_otf_ramp(p->otf_flip.p, g.Hx, plane, g.Wx, cxr, g.Wy, cyr, p->stream), "otf ramp");
     }
     ck(cudaStreamSynchronize(p->stream), "otf_flip");
-    if (p->ztma) factor_otfs(p);
+    if (p->ztma || (g.Wz == 1 && p->fy && p->ytma)) factor_otfs(p);
     p->launches = 0;
   } catch (...) {
     delete p;

@@ -288,6 +288,15 @@ def test_factored_otf_separable_psf():
     assert rel_l2(got.estimate, its[-1]) <= TOL_1
     wf = O.widefield_psf(31)
     assert "otf:factored" not in vk.RlPlan((128, 40, 44), wf).describe()
+    # 2D fields (C5 regime): the y convolution rebuilds OTF lines from factors
+    psf2 = O.gaussian_psf((31, 31), 3.75)
+    obs2 = synth.blurred(synth.blobs((512, 512), 60, 6, 12, seed=5001), psf2)  # W = 576 x 576
+    assert "otf:factored" in vk.RlPlan(obs2.shape, psf2).describe()
+    got2 = vk.richardson_lucy(obs2, psf2, rule)
+    full2 = _with_env({"VK_RL_NO_OTF_FACTOR": "1"}, lambda: vk.richardson_lucy(obs2, psf2, rule))
+    assert rel_l2(got2.estimate, full2.estimate) <= 1e-5
+    its2, _ = run_oracle(obs2, psf2, 5)
+    assert rel_l2(got2.estimate, its2[-1]) <= TOL_1
 
 
 def test_frc_default_rule_c1():
