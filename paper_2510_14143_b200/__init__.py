@@ -355,6 +355,23 @@ class _Plan:
             pass
 
 
+def _checked_out(out: Optional[np.ndarray], shape) -> np.ndarray:
+    """A caller-supplied output array must be a writable C-contiguous float32
+    array of the plan's image shape: the C ABI writes prod(shape) floats."""
+    if out is None:
+        return np.empty(shape, np.float32)
+    if not isinstance(out, np.ndarray) or out.dtype != np.float32 or tuple(out.shape) != tuple(shape) \
+            or not out.flags.c_contiguous or not out.flags.writeable:
+        raise ShapeMismatch(f"ShapeMismatch: out must be a writable C-contiguous float32 array of shape "
+                            f"{list(shape)}")
+    return out
+
+
+def _check_image(a: np.ndarray, shape, what: str = "observed") -> None:
+    if tuple(a.shape) != tuple(shape):
+        raise ShapeMismatch(f"ShapeMismatch: {what} {list(a.shape)} vs plan {list(shape)}")
+
+
 class RlTransforms(_Plan):
     """RlTransforms(image_shape, psf, threads) (reference src/deconv.cpp:98-176):
     PSF spectra for 'same' convolutions on `image_shape`, built once on the GPU.
@@ -380,9 +397,8 @@ class RlPlan(_Plan):
     def run(self, observed, rule: StoppingRule = StoppingRule(), flat_init: bool = False,
             out: Optional[np.ndarray] = None) -> RlResult:
         obs = _f32(observed)
-        if obs.shape != self.image_shape_:
-            raise ShapeMismatch(f"ShapeMismatch: observed {list(obs.shape)} vs plan {list(self.image_shape_)}")
-        est = np.empty_like(obs) if out is None else out
+        _check_image(obs, self.image_shape_)
+        est = _checked_out(out, self.image_shape_)
         tb = _TraceBuf(max(int(rule.max_iters), 1))
         _check(lib().vk_rl_run(self._h, obs.ctypes.data, est.ctypes.data, ctypes.byref(rule._c()),
                                int(bool(flat_init)), ctypes.byref(tb.c)))
@@ -442,6 +458,8 @@ class RlPlan(_Plan):
     def run_batch(self, observed: Sequence[np.ndarray], rule: StoppingRule = StoppingRule(),
                   flat_init: bool = False) -> List[RlResult]:
         obs = [_f32(o) for o in observed]
+        for i, o in enumerate(obs):  # the C ABI copies prod(plan shape) floats per volume
+            _check_image(o, self.image_shape_, f"observed[{i}]")
         outs = [np.empty_like(o) for o in obs]
         n = len(obs)
         tbs = [_TraceBuf(max(int(rule.max_iters), 1)) for _ in range(n)]
@@ -507,9 +525,8 @@ class ConvPlan(_Plan):
 
     def run(self, image, out: Optional[np.ndarray] = None) -> np.ndarray:
         a = _f32(image)
-        if a.shape != self.image_shape_:
-            raise ShapeMismatch(f"ShapeMismatch: image {list(a.shape)} vs plan {list(self.image_shape_)}")
-        o = np.empty_like(a) if out is None else out
+        _check_image(a, self.image_shape_, "image")
+        o = _checked_out(out, self.image_shape_)
         _check(lib().vk_conv_run(self._h, a.ctypes.data, o.ctypes.data))
         return o
 

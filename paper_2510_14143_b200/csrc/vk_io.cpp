@@ -378,10 +378,19 @@ const char* axes_for_rank(int rank) {  // io.cpp:33-41
   bad_header("unsupported rank " + std::to_string(rank));
 }
 
-uint64_t payload_bytes(const vk_volume_info& info) {
+// Element count x element size; false when it does not fit in 64 bits (a
+// crafted header could otherwise wrap to the real file size).
+bool payload_bytes_checked(const vk_volume_info& info, uint64_t* out) {
   uint64_t n = 1;
-  for (int a = 0; a < info.rank; ++a) n *= info.shape[a];
-  return n * elem_bytes(info.elem);
+  for (int a = 0; a < info.rank; ++a)
+    if (__builtin_mul_overflow(n, info.shape[a], &n)) return false;
+  return !__builtin_mul_overflow(n, (uint64_t)elem_bytes(info.elem), out);
+}
+
+uint64_t payload_bytes(const vk_volume_info& info) {
+  uint64_t b = 0;
+  if (!payload_bytes_checked(info, &b)) io_fail(VK_ERR_ARG, "volume too large (element count overflows)");
+  return b;
 }
 
 struct File {
@@ -405,6 +414,10 @@ vk_volume_info read_info(const char* path, File& file) {
   if (std::fread(len_le, 1, 4, file.f) != 4) bad_header("missing header length");
   const uint32_t len = (uint32_t)len_le[0] | ((uint32_t)len_le[1] << 8) | ((uint32_t)len_le[2] << 16) |
                        ((uint32_t)len_le[3] << 24);
+  struct stat st {};
+  if (fstat(fileno(file.f), &st) != 0) io_fail(VK_ERR_ARG, "cannot stat '" + sp + "'");
+  // never allocate more header than the file holds
+  if (8ull + len > (uint64_t)st.st_size) bad_header("truncated header");
   std::string head(len, '\0');
   if (len && std::fread(&head[0], 1, len, file.f) != len) bad_header("truncated header");
   const JVal h = JParser(head).document();
@@ -429,9 +442,7 @@ vk_volume_info read_info(const char* path, File& file) {
   info.rank = (int)js->arr.size();
   for (int a = 0; a < info.rank; ++a) info.shape[a] = js->arr[a].u;
   info.payload_offset = 8ull + len;
-  info.payload_bytes = payload_bytes(info);
-  struct stat st {};
-  if (fstat(fileno(file.f), &st) != 0) io_fail(VK_ERR_ARG, "cannot stat '" + sp + "'");
+  if (!payload_bytes_checked(info, &info.payload_bytes)) bad_header("shape overflows the payload size");
   const uint64_t have = (uint64_t)st.st_size - std::min<uint64_t>((uint64_t)st.st_size, info.payload_offset);
   if (have < info.payload_bytes)
     truncated("expected " + std::to_string(info.payload_bytes) + " payload bytes in '" + sp + "'");

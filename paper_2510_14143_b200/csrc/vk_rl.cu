@@ -16,6 +16,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <new>
 #include <string>
 #include <thread>
@@ -875,6 +876,20 @@ bool encode_otf_map(vk_rl_plan p, void* base, CUtensorMap* m) {
                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
 
+// Kernel attributes (dynamic shared memory, carveout) are per device
+// context: set them once for every device a plan is created on.
+cudaError_t fast_attributes_for_device(int device) {
+  static std::mutex mu;
+  static std::vector<int> done;  // 0 not yet, 1 ok
+  std::lock_guard<std::mutex> lock(mu);
+  if (device < 0) return cudaErrorInvalidDevice;
+  if ((int)done.size() <= device) done.resize(device + 1, 0);
+  if (done[device]) return cudaSuccess;
+  const cudaError_t e = vk::fast_init_attributes();  // on the current device (the caller's DeviceGuard)
+  if (e == cudaSuccess) done[device] = 1;
+  return e;
+}
+
 void to3(int rank, const uint64_t* in, uint64_t* out3) {
   for (int i = 0; i < 3; ++i) out3[i] = 1;
   for (int i = 0; i < rank; ++i) out3[3 - rank + i] = in[i];
@@ -987,8 +1002,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->lpz = make_line_plan(g.Wz, p->twz.p);
     const char* gen = std::getenv("VK_RL_GENERIC");
     if (!(gen && gen[0] == '1')) {
-      static const cudaError_t attr = vk::fast_init_attributes();
-      ck(attr, "fast kernel attributes");
+      ck(fast_attributes_for_device(device), "fast kernel attributes");
       p->fx = vk::fast_lookup(g.Wx);
       p->fy = vk::fast_lookup(g.Wy);
       p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
@@ -1221,6 +1235,18 @@ double relative_change(double prev, double cur) {  // deconv.cpp:296-300
   if (std::isinf(prev) && std::isinf(cur) && prev == cur) return 0.0;
   if (std::isinf(prev) || std::isinf(cur)) return std::numeric_limits<double>::infinity();
   return std::abs(cur - prev) / std::max(std::abs(prev), 1e-30);
+}
+
+// Replays the stopping rule over metric values 1..n (deconv.cpp:409-423):
+// from iteration 2 on, a relative change below rel_tol counts a failure,
+// anything else resets; patience failures in a row stop the run.
+bool rule_fires(const std::vector<double>& values, int n, const vk_stop_rule* rule) {
+  int fails = 0;
+  for (int k = 1; k < n; ++k) {
+    fails = relative_change(values[k - 1], values[k]) < rule->rel_tol ? fails + 1 : 0;
+    if (fails >= rule->patience) return true;
+  }
+  return false;
 }
 
 struct RefStats {
@@ -1514,9 +1540,8 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   // Early stop is only possible from iteration patience+1 on (fails counts
   // from iteration 2); before that no host round-trip is needed.
   const bool may_stop = rule->patience + 1 <= iters;
-  int fails = 0, run = 0;
-  bool have_prev = false, stopped = false;
-  double prev = 0;
+  int run = 0;
+  bool stopped = false;
   std::vector<double> values;
   ck(cudaEventRecord(p->events[0], s), "event");
   for (int it = 1; it <= iters; ++it) {
@@ -1555,20 +1580,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
           values.push_back(si_psnr_from_sums(rs, a[1], a[2], a[3]));
         }
       }
-      // replay the stopping rule over the values so far (deconv.cpp:409-423)
-      fails = 0;
-      have_prev = false;
-      for (int k = 0; k < it; ++k) {
-        if (have_prev) {
-          fails = relative_change(prev, values[k]) < rule->rel_tol ? fails + 1 : 0;
-          if (fails >= rule->patience) {
-            stopped = true;
-            break;
-          }
-        }
-        prev = values[k];
-        have_prev = true;
-      }
+      stopped = rule_fires(values, it, rule);
       if (stopped) {
         vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
         launch_check(p, "crop");
@@ -1587,7 +1599,17 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     ck(cudaMemcpy(sums.data(), p->ss_sum.p, (size_t)run * sizeof(double), cudaMemcpyDeviceToHost), "ssim D2H");
     values.resize(run);
     for (int k = 0; k < run; ++k) values[k] = sums[k] / (double)nI;
+  } else if (!frc) {
+    values.resize(run);
+    for (int k = 0; k < run; ++k) {
+      const double* a = p->h_acc + (size_t)k * 4;
+      values[k] = si_psnr_from_sums(rs, a[1], a[2], a[3]);
+    }
   }
+  // The reference checks the rule after the last iteration too
+  // (deconv.cpp:409-423): a run whose rule fires exactly at max_iters is
+  // "converged".  Only the reason can change here (the estimate is final).
+  if (!stopped) stopped = rule_fires(values, run, rule);
   prof_collect(p);
   if (trace) {
     trace->iters_run = run;

@@ -243,6 +243,18 @@ def _check_psf(psf: np.ndarray) -> None:  # deconv.cpp:319-326
         raise UnnormalizedPsf("UnnormalizedPsf: psf sums to %f" % s)
 
 
+def _rule_stops(values: Sequence[float], rule: StoppingRule) -> bool:
+    """Replays the stopping rule over metric values 1..n (deconv.cpp:409-423)."""
+    fails, have_prev, prev = 0, False, 0.0
+    for v in values:
+        if have_prev:
+            fails = fails + 1 if _relative_change(prev, v) < rule.rel_tol else 0
+            if fails >= rule.patience:
+                return True
+        prev, have_prev = v, True
+    return False
+
+
 def run_slabs(plans: Sequence[SlabPlan], obs_ptrs: Sequence[int], out_ptrs: Sequence[int], psf,
               rule: StoppingRule, flat_init: bool, exchange: Callable[[int], None],
               allreduce: Callable[[np.ndarray, str], np.ndarray], stream: int = 0) -> IterationTrace:
@@ -281,14 +293,7 @@ def run_slabs(plans: Sequence[SlabPlan], obs_ptrs: Sequence[int], out_ptrs: Sequ
         if may_stop and it >= rule.patience + 1 and not last:
             acc = allreduce(sum(p.sums(it, stream) for p in plans), "sum")
             values = [_si_psnr(n_img, sr, srr, rng, a[1], a[2], a[3]) for a in acc]
-            fails, have_prev, prev = 0, False, 0.0
-            for v in values:  # deconv.cpp:409-423
-                if have_prev:
-                    fails = fails + 1 if _relative_change(prev, v) < rule.rel_tol else 0
-                    if fails >= rule.patience:
-                        stopped = True
-                        break
-                prev, have_prev = v, True
+            stopped = _rule_stops(values, rule)
             if stopped:
                 for p, out in zip(plans, out_ptrs):
                     p.crop(out, stream)
@@ -298,6 +303,10 @@ def run_slabs(plans: Sequence[SlabPlan], obs_ptrs: Sequence[int], out_ptrs: Sequ
     acc = allreduce(sum(p.sums(run, stream) for p in plans), "sum")
     recs = [IterationRecord(i + 1, StopMetric.si_psnr_vs_input, _si_psnr(n_img, sr, srr, rng, a[1], a[2], a[3]), 0.0)
             for i, a in enumerate(acc)]
+    # the reference checks the rule on the last iteration too (deconv.cpp:409-423):
+    # a run that converges exactly at max_iters reports "converged"
+    if not stopped:
+        stopped = _rule_stops([r.value for r in recs], rule)
     return IterationTrace(recs, [float(a[0]) for a in acc], (), "converged" if stopped else "max_iters")
 
 

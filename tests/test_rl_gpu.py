@@ -408,6 +408,23 @@ def test_stopping_semantics_tol_inf():
     assert rel_l2(r.estimate, its[-1]) <= TOL_N
 
 
+@pytest.mark.parametrize("metric", ["si_psnr_vs_input", "frc_resolution", "ssim_vs_prev"])
+def test_rule_fires_exactly_at_max_iters(metric):
+    """the rule is checked after the last iteration too
+    (deconv.cpp:409-423): rel_tol = inf, patience 3, max_iters 4 -> the
+    reference reports "converged" with 4 records, for every metric."""
+    psf = O.gaussian_psf((5, 5, 5), 1.0)
+    obs = synth.blurred(synth.blobs((16, 48, 48), 5, 4, 6, seed=6), psf)
+    r = vk.richardson_lucy(obs, psf, vk.StoppingRule(metric, math.inf, 3, 4))
+    _, t = O.richardson_lucy(obs, psf, metric, math.inf, 3, 4)
+    if metric == "si_psnr_vs_input":
+        assert t.stop_reason == "converged"
+    assert len(r.trace.records) == len(t.metric) == 4 and r.trace.stop_reason == t.stop_reason
+    # one iteration short of the rule: max_iters
+    r3 = vk.richardson_lucy(obs, psf, vk.StoppingRule(metric, math.inf, 3, 3))
+    assert len(r3.trace.records) == 3 and r3.trace.stop_reason == "max_iters"
+
+
 @pytest.mark.parametrize("lanes", ["", "1", "3"])
 def test_batch_device_lanes_match_single_runs(lanes):
     """vk_rl_run_batch_device: volumes on concurrent lanes (own buffers,
