@@ -7,15 +7,25 @@ A step is one full Richardson-Lucy run (all of the config's iterations) over
 one synthetic volume per GPU.  At N=1 the workload is BASELINE.json
 configs[1] (C2: 128x512x512 float32, 31^3 widefield PSF, 50 iterations); with
 N>1 every rank deconvolves its own independent volume (weak scaling, no
-collective on the data path; NCCL only for the max-over-ranks timing).
+collective on the data path); the batch configs (c3, c5) split their volumes
+across ranks in contiguous blocks (strong scaling).  `--gpus N` without a
+torchrun environment re-launches itself under torch.distributed.run with N
+ranks; under torchrun, --gpus must equal WORLD_SIZE.  NCCL only gathers:
+the per-rank counters (all_gather) and, after the timed region, every rank's
+estimates onto rank 0 (point-to-point over NVLink).
 
 `value`   device-resident throughput: observed already in HBM, CUDA events on
           the launch stream around exactly K steps, max over ranks.
-`e2e`     the same metric through the public host-pointer API (vk_rl_run):
-          pinned host observed -> H2D -> RL -> D2H estimate, every step.
-`roofline` the dominant kernel's algorithmic bytes per launch / its mean
-          launch time (CUDA events around every launch in the timed region),
-          against MEASURED_PEAKS.json hbm_gbs.
+`e2e`     the same metric through the reference-facing one-shot call
+          (vk_richardson_lucy / vk_richardson_lucy_batch, i.e.
+          deconv::richardson_lucy[_batch]) with PAGEABLE host arrays: H2D,
+          plan lookup (cached after the warm-up call), RL, D2H every step.
+`roofline` SURVEY.md §8(d): the dominant KERNEL (x, y or z pass; the kinds of
+          one kernel are summed) -- its algorithmic bytes (spectra, observed,
+          estimate; OTF excluded, reported beside) per launch over its mean
+          launch time (CUDA events around every launch, on the launch stream),
+          against MEASURED_PEAKS.json hbm_gbs; `iteration_frac` = B_alg x
+          voxel-iters/s per GPU / peak, B_alg = 64 S_p + 4 N_I + 8 N_P.
 `cpu_baseline` the reference's own richardson_lucy (oracle/_ref, the reference
           sources built unmodified with the in-repo FFTW-API shim) on this
           host's cores, bounded sample, rank 0 at N=1.
@@ -145,6 +155,45 @@ def dist_setup(args):
     return ws, rank, local
 
 
+def relaunch_under_torchrun(args) -> int:
+    """`bench.py --gpus N` outside torchrun: one rank per GPU, 127.0.0.1 rendezvous."""
+    import socket
+    import subprocess
+
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.call(cmd)
+
+
+# kernel kinds -> the kernel that runs them (x / y / z pass)
+KERNEL_OF = {"x_fwd": "xpass", "x_ratio": "xpass", "x_update": "xpass", "y_fwd": "ypass", "y_inv": "ypass",
+             "y_conv": "ypass", "z_conv": "zpass", "yz_dataflow": "yzconv", "yz_cluster": "yzconv"}
+
+
+def roofline(prof, otf, peak, steps):
+    """Per-kernel achieved GB/s from the per-launch CUDA-event profile."""
+    kern = {}
+    for kind, (ms, n, alg) in prof.items():
+        if not n:
+            continue
+        k = kern.setdefault(KERNEL_OF.get(kind, kind), {"ms": 0.0, "launches": 0, "bytes": 0, "otf_bytes": 0,
+                                                        "kinds": {}})
+        k["ms"] += ms
+        k["launches"] += n
+        k["bytes"] += alg * n
+        k["otf_bytes"] += otf.get(kind, 0) * n
+        k["kinds"][kind] = {"ms_per_step": round(ms / steps, 4), "launches_per_step": n // steps,
+                            "alg_bytes_per_launch": alg, "otf_bytes_per_launch": otf.get(kind, 0),
+                            "gbs": round(alg * n / (ms * 1e-3) / 1e9, 1) if ms else None}
+    for k in kern.values():
+        k["gbs"] = k["bytes"] / (k["ms"] * 1e-3) / 1e9 if k["ms"] else 0.0
+        k["frac"] = k["gbs"] / peak
+    return kern
+
+
 def cpu_reference_run(cfg, obs, psf, iters, note):
     """The reference's richardson_lucy on the host (accelerated backend = all
     hardware threads).  Returns per-iteration wall times from its own trace."""
@@ -222,7 +271,12 @@ def main():
     ap.add_argument("--volumes", type=int, default=None, help="batch size override for c3/c5")
     args = ap.parse_args()
     cfg = CONFIGS[args.config]
+    if args.impl == "ours" and args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(relaunch_under_torchrun(args))
     ws, rank, local = dist_setup(args)
+    if args.impl == "ours" and "WORLD_SIZE" in os.environ and ws != args.gpus:
+        print(json.dumps({"metric": METRIC, "error": f"--gpus {args.gpus} but WORLD_SIZE={ws}"}), flush=True)
+        sys.exit(2)
 
     if args.impl == "reference":
         run_reference_arm(args, cfg, ws, rank)
@@ -300,62 +354,85 @@ def main():
     t = torch.tensor([elapsed_ms], device="cuda", dtype=torch.float64)
     if dist:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    elapsed_ms = float(t.item())
+    own_ms, elapsed_ms = elapsed_ms, float(t.item())
     units_per_step = n_batch if n_batch else ws  # volumes processed by the whole job per step
     vol_iters = units_per_step * args.steps * iters
     value = vol_iters * n_img / (elapsed_ms * 1e-3)
 
-    # ---- end-to-end through the public host API ---------------------------
+    # ---- NCCL: per-rank counters (all_gather) -----------------------------
+    mine = torch.tensor([own_ms, float(len(block) if n_batch else 1), float(iters), float(launches)],
+                        device="cuda", dtype=torch.float64)
+    per_rank = [mine]
+    if dist:
+        per_rank = [torch.empty_like(mine) for _ in range(ws)]
+        dist.all_gather(per_rank, mine)
+    per_rank = [[float(v) for v in t.tolist()] for t in per_rank]
+
+    # ---- NCCL: every rank's estimates onto rank 0 (after the timed region) --
+    gathered = None
+    if dist:
+        t0g = torch.cuda.Event(enable_timing=True)
+        t1g = torch.cuda.Event(enable_timing=True)
+        counts = [int(r[1]) for r in per_rank]
+        t0g.record(stream)
+        ops, recv = [], []
+        if rank == 0:
+            for src in range(1, ws):
+                for _ in range(counts[src]):
+                    recv.append(torch.empty_like(outs[0]))
+                    ops.append(dist.P2POp(dist.irecv, recv[-1], src))
+        else:
+            ops = [dist.P2POp(dist.isend, o, 0) for o in outs[:counts[rank]]]
+        if ops:
+            for w in dist.batch_isend_irecv(ops):
+                w.wait()
+        t1g.record(stream)
+        torch.cuda.synchronize()
+        if rank == 0:
+            gb = sum(r.numel() * 4 for r in recv)
+            gathered = {"volumes": len(recv) + counts[0], "bytes_received": gb,
+                        "ms": t0g.elapsed_time(t1g), "transport": "NCCL send/recv (batch_isend_irecv)"}
+            del recv
+
+    # ---- end-to-end through the reference-facing one-shot call ----------------
+    # deconv::richardson_lucy[_batch] = vk_richardson_lucy[_batch]: pageable
+    # numpy arrays in and out, host staging, the plan from the call's cache
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
     e2e_value = None
     e2e_vols = 0
-    if e2e_steps > 0 and n_batch:
-        # batch configs: the whole block through the host-pointer batch API
-        # (vk_rl_run_batch), pinned host volumes in and out every step
-        # (at most 64 volumes per rank: pinned host memory for the whole C5
-        # block would be 2 x 69 GB)
-        e2e_block = vols[-64:]
-        obs_hs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in e2e_block]
-        est_hs = [torch.empty(shape, dtype=torch.float32, pin_memory=True) for _ in e2e_block]
-        for h, v in zip(obs_hs, e2e_block):
-            h.copy_(v.cpu())
-        hin, hout = [h.data_ptr() for h in obs_hs], [h.data_ptr() for h in est_hs]
-        plan.run_batch_ptr(hin, hout, rule)  # warm
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            plan.run_batch_ptr(hin, hout, rule)
-        e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_vols = len(e2e_block)
-        e2e_value = ws * e2e_vols * e2e_steps * iters * n_img / float(te.item())
-        assert torch.equal(est_hs[-1], outs[-1].cpu()), "host-API and device-API results differ"
-    elif e2e_steps > 0:
-        e2e_vols = 1
-        obs_h = torch.empty(shape, dtype=torch.float32, pin_memory=True)
-        obs_h.copy_(vols[-1].cpu())  # `outs[-1]` holds the device result of the block's last volume
-        est_h = torch.empty(shape, dtype=torch.float32, pin_memory=True)
-        plan.run_ptr(obs_h.data_ptr(), est_h.data_ptr(), rule)  # warm
-        if dist:
-            dist.barrier()
-        t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            plan.run_ptr(obs_h.data_ptr(), est_h.data_ptr(), rule)
-        e2e_s = time.perf_counter() - t0
-        te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
-        if dist:
-            dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        e2e_value = ws * e2e_steps * iters * n_img / float(te.item())  # one volume per rank per e2e step
-        assert torch.equal(est_h, outs[-1].cpu()), "host-API and device-API results differ"
+    if e2e_steps > 0:
+        # batch configs: at most 64 volumes per rank (pageable host memory for
+        # the whole C5 block would be 2 x 69 GB)
+        e2e_src = vols[-64:] if n_batch else [vols[-1]]
+        host_in = [v.cpu().numpy() for v in e2e_src]  # pageable
+        e2e_vols = len(host_in)
 
-    # ---- roofline of the dominant kernel ------------------------------------
+        def e2e_call():
+            if n_batch:
+                return [r.estimate for r in vk.richardson_lucy_batch(host_in, psf, rule, device=local)]
+            return [vk.richardson_lucy(host_in[0], psf, rule, device=local).estimate]
+
+        e2e_call()  # warm: builds and caches the plan
+        if dist:
+            dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            res = e2e_call()
+        e2e_s = time.perf_counter() - t0
+        te = torch.tensor([e2e_s], device="cuda", dtype=torch.float64)
+        if dist:
+            dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        e2e_value = ws * e2e_vols * e2e_steps * iters * n_img / float(te.item())
+        assert np.array_equal(res[-1], outs[(len(block) - 1) if n_batch else 0].cpu().numpy()), \
+            "host-API and device-API results differ"
+        del res
+        vk.plan_cache_clear()
+
+    # ---- roofline of the dominant kernel -------------------
     peak, peak_src = load_peaks()
-    dom = max(prof, key=lambda k: prof[k][0])
-    ms_tot, n_launch, alg = prof[dom]
-    achieved = alg / (ms_tot / n_launch * 1e-3) / 1e9 if n_launch else 0.0
+    kern = roofline(prof, plan.otf_bytes(), peak, args.steps)
+    dom = max(kern, key=lambda k: kern[k]["ms"])
+    kd = kern[dom]
     g = plan.fft_shape_
     P = plan.domain_shape
     pz, py = (P[-3] if len(P) == 3 else 1), (P[-2] if len(P) >= 2 else 1)
@@ -366,35 +443,46 @@ def main():
     tpath = os.path.join(ROOT, "profiles", f"ncu_traffic_{args.config}.json")
     if os.path.exists(tpath):
         with open(tpath) as f:
-            traffic = json.load(f).get(dom)
-    kernel_total_ms = sum(v[0] for v in prof.values())
+            tj = json.load(f)
+        traffic = tj.get("per_kernel", {}).get(dom, {}).get("dram_bytes_per_launch")
+    kernel_total_ms = sum(k["ms"] for k in kern.values())
+    vox_it_per_gpu = value / ws
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if n_batch else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["label"] + (" per GPU" if ws > 1 else ""), "image": list(shape),
-                   "psf": list(psf.shape), "iters_per_step": iters, "fft_shape": list(g),
-                   "padded_domain": list(P), "parallelism": f"independent volumes x{ws}",
+        "config": {"workload": cfg["label"] + (" per GPU" if ws > 1 and not n_batch else ""),
+                   "image": list(shape), "psf": list(psf.shape), "iters_per_step": iters,
+                   "volumes": n_batch or ws, "fft_shape": list(g), "padded_domain": list(P),
+                   "parallelism": (f"volume blocks over {ws} ranks" if n_batch else f"independent volumes x{ws}"),
                    "plan": plan.describe(),
                    "l2": "inputs larger than L2 (spectrum %.0f MB, observed %.0f MB > 126 MB)"
                          % (s_p * 8 / 1e6, n_img * 4 / 1e6)},
-        "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
-                     "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
-                     "alg_bytes_per_launch": alg, "mean_launch_ms": ms_tot / max(n_launch, 1),
-                     "kernel_share_of_step": ms_tot / kernel_total_ms if kernel_total_ms else None,
+        "roofline": {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
+                     "frac": kd["frac"], "traffic": traffic, "peak_source": peak_src,
+                     "alg_bytes_per_launch": kd["bytes"] / kd["launches"],
+                     "mean_launch_ms": kd["ms"] / kd["launches"],
+                     "kernel_share_of_step": kd["ms"] / kernel_total_ms if kernel_total_ms else None,
+                     "bytes": "SURVEY.md §8(d): spectra + observed + estimate; OTF excluded (otf_bytes_per_launch)",
                      "timing": "CUDA events around every launch on the launch stream, second timed pass of the "
                                "same K steps",
-                     "per_kernel_ms": {k: round(v[0] / args.steps, 4) for k, v in prof.items() if v[1]},
+                     "per_kernel": {k: {"ms_per_step": round(v["ms"] / args.steps, 4), "gbs": round(v["gbs"], 1),
+                                        "frac": round(v["frac"], 4), "kinds": v["kinds"]} for k, v in kern.items()},
                      "iteration_B_alg_bytes": b_alg,
-                     "iteration_frac": value / n_img / ws * b_alg / 1e9 / peak},
+                     "iteration_frac": vox_it_per_gpu / n_img * b_alg / 1e9 / peak},
         "e2e": {"value": e2e_value, "unit": UNIT, "h2d_bytes_per_step": e2e_vols * n_img * 4,
-                "d2h_bytes_per_step": e2e_vols * (n_img * 4 + iters * 4 * 8 + 48), "bytes_scope": "per rank",
-                "api": "vk_rl_run_batch (host pointers, batch lanes)" if n_batch else "vk_rl_run (host pointers)",
-                "volumes_per_rank": e2e_vols,
-                "steps": e2e_steps},
+                "d2h_bytes_per_step": e2e_vols * (n_img * 4 + iters * 3 * 8), "bytes_scope": "per rank",
+                "api": ("vk_richardson_lucy_batch (deconv::richardson_lucy_batch)" if n_batch
+                        else "vk_richardson_lucy (deconv::richardson_lucy)")
+                       + ": pageable host arrays, pinned staging ring, cached plan",
+                "volumes_per_rank": e2e_vols, "steps": e2e_steps},
         "gpu_launches": launches,
         "clocks": clk.summary(),
+        "per_rank": [{"rank": i, "elapsed_ms": r[0], "volumes": int(r[1]), "iters": int(r[2]),
+                      "launches": int(r[3])} for i, r in enumerate(per_rank)],
     }
+    if gathered:
+        line["results_gather"] = gathered
     if rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             host_obs = obs.cpu().numpy()

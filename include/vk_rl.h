@@ -13,7 +13,10 @@
  *    exactly NdImage's layout (proj/include/voxelkit/image.hpp:46-48).
  *  - Functions suffixed _device take device pointers on the plan's GPU and a
  *    cudaStream_t (passed as void*, NULL = legacy default stream); the others
- *    take host pointers and copy through pinned staging.
+ *    take host pointers: pinned (page-locked) buffers are DMA'd directly,
+ *    pageable ones are copied through the plan's ring of pinned chunks, the
+ *    host copy of one chunk (split over a worker pool, VK_RL_HOST_THREADS)
+ *    overlapping the DMA of the previous one.
  *  - Every function returns a vk_status.  On failure vk_last_error() returns
  *    the exact message the reference would put in the exception's what()
  *    (thread-local, valid until the next call on the same thread).
@@ -30,7 +33,7 @@
 extern "C" {
 #endif
 
-#define VK_RL_ABI_VERSION 3
+#define VK_RL_ABI_VERSION 4
 #define VK_MAX_RANK 3
 
 /* Status codes; each maps to one reference exception type
@@ -148,11 +151,25 @@ vk_status vk_rl_step_device(vk_rl_plan plan, const float* d_estimate, const floa
 
 /* richardson_lucy(observed, psf, rule, flat_init) (deconv.cpp:304-431) in one
  * call, with the reference's exact validation order: rule, rank, observed
- * negativity, PSF negativity, PSF sum. */
+ * negativity, PSF negativity, PSF sum.  The reference builds its transforms
+ * per call (deconv.cpp:332); here the one-shot calls (this one,
+ * vk_rl_step_psf, vk_fft_convolve) keep their plans in a process-wide LRU
+ * cache keyed on (device, shapes, PSF values): VK_RL_PLAN_CACHE plans
+ * (default 2; 0 = build and free per call, as the reference does). */
 vk_status vk_richardson_lucy(int device, int rank, const uint64_t* shape, const float* observed,
                              int psf_rank, const uint64_t* psf_shape, const float* psf,
                              const vk_stop_rule* rule, int flat_init, float* estimate,
                              vk_trace* trace);
+
+/* n independent volumes of one shape, each exactly as vk_richardson_lucy
+ * would deconvolve it, through one cached plan and its batch lanes
+ * (include/voxelkit_b200/deconv_batch.hpp; the C3 / C5 batches).  traces may
+ * be NULL or an array of n.  On failure the message names the volume. */
+vk_status vk_richardson_lucy_batch(int device, int rank, const uint64_t* shape, int n,
+                                   const float* const* observed, int psf_rank,
+                                   const uint64_t* psf_shape, const float* psf,
+                                   const vk_stop_rule* rule, int flat_init, float* const* estimate,
+                                   vk_trace* traces);
 
 /* rl_step(estimate, observed, psf) registry form (deconv.cpp:196-200,
  * 437-449): transforms built for the call. */
@@ -226,6 +243,9 @@ vk_status vk_rl_slab_pack(vk_rl_plan plan, int row, int n, void* d_buf, void* st
 vk_status vk_rl_slab_unpack(vk_rl_plan plan, int row, int n, const void* d_buf, void* stream);
 vk_status vk_rl_slab_copy_rows(vk_rl_plan src, int src_row, vk_rl_plan dst, int dst_row, int n, void* stream);
 
+/* Frees every idle plan held by the one-shot calls' cache (device memory). */
+vk_status vk_plan_cache_clear(void);
+
 /* fftx::good_size (fft_plan.cpp:41-49). */
 uint64_t vk_good_size(uint64_t n);
 
@@ -251,9 +271,13 @@ typedef enum vk_kernel_kind {
  * recorded on the launch stream around each kernel). */
 vk_status vk_rl_plan_profile(vk_rl_plan plan, int enable);
 /* Accumulated device ms and launch counts per kind since the last reset, and
- * the algorithmic HBM bytes of one launch of each kind. */
+ * the algorithmic HBM bytes of one launch of each kind (SURVEY.md §8(d):
+ * spectra, observed and estimate; the OTF is not counted). */
 vk_status vk_rl_plan_profile_read(vk_rl_plan plan, int n_kinds, double* ms_total, uint64_t* launches,
                                   uint64_t* alg_bytes_per_launch, int reset);
+
+/* OTF bytes one launch of each kind reads (0 for a factored, separable OTF). */
+vk_status vk_rl_plan_otf_bytes(vk_rl_plan plan, int n_kinds, uint64_t* otf_bytes_per_launch);
 
 const char* vk_last_error(void);
 int vk_abi_version(void);

@@ -188,12 +188,25 @@ def lib() -> ctypes.CDLL:
     for name in ("vk_volume_info_read", "vk_volume_read", "vk_volume_read_device", "vk_volume_write",
                  "vk_volume_write_device", "vk_generate_blobs", "vk_gaussian_psf"):
         getattr(L, name).restype = st
+    L.vk_richardson_lucy_batch.argtypes = [i, i, _u64p, i, ctypes.POINTER(_vp), i, _u64p, _fp,
+                                           ctypes.POINTER(_Rule), i, ctypes.POINTER(_vp), ctypes.POINTER(_Trace)]
+    L.vk_richardson_lucy_batch.restype = st
+    L.vk_rl_plan_otf_bytes.argtypes = [_vp, i, _u64p]
+    L.vk_rl_plan_otf_bytes.restype = st
+    L.vk_plan_cache_clear.argtypes = []
+    L.vk_plan_cache_clear.restype = st
     L.vk_good_size.argtypes = [ctypes.c_uint64]
     L.vk_good_size.restype = ctypes.c_uint64
     L.vk_last_error.restype = ctypes.c_char_p
     L.vk_abi_version.restype = ctypes.c_int
     _lib = L
     return L
+
+
+def plan_cache_clear() -> None:
+    """Frees the idle plans the one-shot calls (richardson_lucy, rl_step with a
+    PSF, fft_convolve) keep for reuse (vk_plan_cache_clear)."""
+    _check(lib().vk_plan_cache_clear())
 
 
 def _check(rc: int) -> None:
@@ -337,6 +350,13 @@ class _Plan:
         ab = (ctypes.c_uint64 * n)()
         _check(lib().vk_rl_plan_profile_read(self._h, n, ms, cnt, ab, int(bool(reset))))
         return {KERNEL_KINDS[i]: (float(ms[i]), int(cnt[i]), int(ab[i])) for i in range(n)}
+
+    def otf_bytes(self) -> dict:
+        """{kind: OTF bytes one launch reads} (not part of the algorithmic bytes)."""
+        n = len(KERNEL_KINDS)
+        ob = (ctypes.c_uint64 * n)()
+        _check(lib().vk_rl_plan_otf_bytes(self._h, n, ob))
+        return {KERNEL_KINDS[i]: int(ob[i]) for i in range(n)}
 
     def device_bytes(self) -> int:
         v = ctypes.c_uint64(0)
@@ -488,6 +508,33 @@ def richardson_lucy(observed, psf, rule: StoppingRule = StoppingRule(), flat_ini
                                     _shape(k.shape), k.ctypes.data_as(_fp), ctypes.byref(rule._c(sp)),
                                     int(bool(flat_init)), est.ctypes.data, ctypes.byref(tb.c)))
     return RlResult(est, tb.trace(rule.metric, obs.ndim))
+
+
+def richardson_lucy_batch(observed: Sequence[np.ndarray], psf, rule: StoppingRule = StoppingRule(),
+                          flat_init: bool = False, device: int = 0) -> List[RlResult]:
+    """richardson_lucy on each volume (one shape), through one cached plan and
+    its batch lanes (vk_richardson_lucy_batch; reference semantics per volume,
+    src/deconv.cpp:304-431)."""
+    obs = [_f32(o) for o in observed]
+    if not obs:
+        return []
+    for i, o in enumerate(obs):
+        _check_image(o, obs[0].shape, f"observed[{i}]")
+    k = _f32(psf)
+    n = len(obs)
+    outs = [np.empty_like(o) for o in obs]
+    tbs = [_TraceBuf(max(int(rule.max_iters), 1)) for _ in range(n)]
+    traces = (_Trace * n)(*[t.c for t in tbs])
+    ip = (_vp * n)(*[o.ctypes.data for o in obs])
+    op = (_vp * n)(*[o.ctypes.data for o in outs])
+    _check(lib().vk_richardson_lucy_batch(device, obs[0].ndim, _shape(obs[0].shape), n, ip, k.ndim, _shape(k.shape),
+                                          k.ctypes.data_as(_fp), ctypes.byref(rule._c()), int(bool(flat_init)), op,
+                                          traces))
+    res = []
+    for i in range(n):
+        tbs[i].c = traces[i]
+        res.append(RlResult(outs[i], tbs[i].trace(rule.metric, obs[0].ndim)))
+    return res
 
 
 def _shape_str(s) -> str:
@@ -683,7 +730,7 @@ def exported_symbols() -> List[str]:
 __all__ = [
     "Error", "ShapeMismatch", "NegativeInput", "UnnormalizedPsf", "DegenerateReference", "TooSmall",
     "OddExtent", "CudaError", "Unsupported", "KernelTooLarge", "ConvPlan", "fft_convolve", "StopMetric", "StoppingRule", "IterationRecord",
-    "IterationTrace", "RlResult", "RlTransforms", "RlPlan", "richardson_lucy", "rl_step", "good_size",
+    "IterationTrace", "RlResult", "RlTransforms", "RlPlan", "richardson_lucy", "richardson_lucy_batch", "plan_cache_clear", "rl_step", "good_size",
     "to_string", "lib", "exported_symbols", "Volume", "VolumeInfo", "volume_info", "read_volume", "write_volume", "read_volume_device",
     "write_volume_device", "SynthSpec", "generate_blobs_device", "gaussian_psf", "BadMagic", "HeaderMismatch",
     "TruncatedPayload", "PlacementFailure", "EvenExtent",

@@ -435,6 +435,32 @@ __global__ void wrap_kernel_kernel(const float* __restrict__ k, int Kz, int Ky, 
   }
 }
 
+// Periodic extension for circular fft_convolve on extents the device FFT
+// does not plan (not 5-smooth): dst [Ez][Ey][Ex] = src[(i - h) mod A] per axis.
+__global__ void wrap_extend_kernel(const float* __restrict__ src, int Az, int Ay, int Ax, float* __restrict__ dst,
+                                   int Ez, int Ey, int Ex, int hz, int hy, int hx) {
+  const size_t n = (size_t)Ez * Ey * Ex;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % Ex);
+    const size_t t = i / Ex;
+    const int y = (int)(t % Ey), z = (int)(t / Ey);
+    const int sz = ((z - hz) % Az + Az) % Az, sy = ((y - hy) % Ay + Ay) % Ay, sx = ((x - hx) % Ax + Ax) % Ax;
+    dst[i] = src[((size_t)sz * Ay + sy) * Ax + sx];
+  }
+}
+
+// dst [Az][Ay][Ax] = src [Ez][Ey][Ex] at offset (hz, hy, hx).
+__global__ void crop_block_kernel(const float* __restrict__ src, int Ey, int Ex, float* __restrict__ dst, int Az,
+                                  int Ay, int Ax, int hz, int hy, int hx) {
+  const size_t n = (size_t)Az * Ay * Ax;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int x = (int)(i % Ax);
+    const size_t t = i / Ax;
+    const int y = (int)(t % Ay), z = (int)(t / Ay);
+    dst[i] = src[((size_t)(z + hz) * Ey + (y + hy)) * Ex + (x + hx)];
+  }
+}
+
 // P -> I crop (deconv.cpp:239-252) for runs that stop early.
 __global__ void crop_kernel(const float* __restrict__ est, float* __restrict__ out, Geom g) {
   const size_t n = (size_t)g.Iz * g.Iy * g.Ix;

@@ -11,6 +11,11 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
+#include <condition_variable>
+#include <deque>
+#include <functional>
+#include <list>
 #include <cmath>
 #include <cstdio>
 #include <cstdlib>
@@ -172,6 +177,164 @@ size_t x_smem(int Wx, int L) {
 }
 size_t yz_smem(int N, int L) { return 2 * (size_t)N * (L + 1) * sizeof(float2); }
 
+// ---- host staging -----------------------------------------------------------
+// Host-pointer calls (vk_rl_run, vk_rl_step, vk_conv_run, the batch form)
+// take whatever memory the caller has: pinned pointers are DMA'd directly;
+// pageable ones go through a per-plan ring of pinned chunks.  The host copy of
+// chunk c+1 (split over a process-wide worker pool) overlaps the DMA of chunk
+// c, so a pageable call costs about max(PCIe, host memcpy) instead of both.
+
+// Process-wide workers for parallel host memcpy.  run(n, f) calls f(0..n-1)
+// on the pool and the calling thread and returns when all are done; the tasks
+// never block, so concurrent callers (batch lanes) cannot deadlock.
+class HostPool {
+ public:
+  static HostPool& get() {
+    static HostPool* p = new HostPool();  // process lifetime
+    return *p;
+  }
+  int size() const { return (int)th_.size() + 1; }
+  template <class F>
+  void run(int n, F&& f) {
+    if (n <= 1 || th_.empty()) {
+      for (int i = 0; i < n; ++i) f(i);
+      return;
+    }
+    struct Group {
+      std::atomic<int> left;
+      std::mutex m;
+      std::condition_variable cv;
+    } grp;
+    grp.left = n;
+    auto one = [&](int i) {
+      f(i);
+      if (grp.left.fetch_sub(1) == 1) {
+        std::lock_guard<std::mutex> g(grp.m);
+        grp.cv.notify_all();
+      }
+    };
+    {
+      std::lock_guard<std::mutex> g(mu_);
+      for (int i = 1; i < n; ++i) q_.push_back([&one, i] { one(i); });
+    }
+    cv_.notify_all();
+    one(0);
+    std::unique_lock<std::mutex> g(grp.m);
+    grp.cv.wait(g, [&] { return grp.left.load() == 0; });
+  }
+
+ private:
+  HostPool() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    int n = (int)std::min(hw, 8u) - 1;
+    if (const char* e = std::getenv("VK_RL_HOST_THREADS")) n = std::max(0, std::atoi(e) - 1);
+    for (int i = 0; i < n; ++i)
+      th_.emplace_back([this] {
+        for (;;) {
+          std::function<void()> t;
+          {
+            std::unique_lock<std::mutex> g(mu_);
+            cv_.wait(g, [&] { return !q_.empty(); });
+            t = std::move(q_.front());
+            q_.pop_front();
+          }
+          t();
+        }
+      });
+    for (auto& t : th_) t.detach();
+  }
+  std::mutex mu_;
+  std::condition_variable cv_;
+  std::deque<std::function<void()>> q_;
+  std::vector<std::thread> th_;
+};
+
+void parallel_memcpy(void* dst, const void* src, size_t bytes) {
+  constexpr size_t kPiece = 1 << 20;
+  HostPool& pool = HostPool::get();
+  const int n = (int)std::min<size_t>((size_t)pool.size(), (bytes + kPiece - 1) / kPiece);
+  if (n <= 1) {
+    std::memcpy(dst, src, bytes);
+    return;
+  }
+  const size_t per = (bytes / n + 63) / 64 * 64;
+  pool.run(n, [&](int i) {
+    const size_t off = (size_t)i * per;
+    if (off < bytes) std::memcpy((char*)dst + off, (const char*)src + off, std::min(per, bytes - off));
+  });
+}
+
+bool host_pinned(const void* p) {
+  cudaPointerAttributes a{};
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+struct Staging {
+  static constexpr int kSlots = 4;
+  static constexpr size_t kChunk = 16 << 20;
+  void* h[kSlots]{};
+  cudaEvent_t ev[kSlots]{};
+  ~Staging() {
+    for (int i = 0; i < kSlots; ++i) {
+      if (h[i]) cudaFreeHost(h[i]);
+      if (ev[i]) cudaEventDestroy(ev[i]);
+    }
+  }
+  void ensure() {
+    for (int i = 0; i < kSlots; ++i) {
+      if (!h[i]) ck(cudaMallocHost(&h[i], kChunk), "pinned staging");
+      if (!ev[i]) ck(cudaEventCreateWithFlags(&ev[i], cudaEventDisableTiming), "staging event");
+    }
+  }
+  // host -> device, enqueued on s; returns when every host byte has been read
+  void h2d(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    if (host_pinned(src)) {
+      ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "H2D");
+      return;
+    }
+    ensure();
+    size_t off = 0;
+    for (int c = 0; off < bytes; ++c, off += kChunk) {
+      const int k = c % kSlots;
+      const size_t n = std::min(kChunk, bytes - off);
+      if (c >= kSlots) ck(cudaEventSynchronize(ev[k]), "staging");  // slot's previous DMA done
+      parallel_memcpy(h[k], (const char*)src + off, n);
+      ck(cudaMemcpyAsync((char*)dst + off, h[k], n, cudaMemcpyHostToDevice, s), "H2D");
+      ck(cudaEventRecord(ev[k], s), "staging");
+    }
+  }
+  // device -> host after everything enqueued on s; returns when dst is written
+  void d2h(void* dst, const void* src, size_t bytes, cudaStream_t s) {
+    if (bytes == 0) return;
+    if (host_pinned(dst)) {
+      ck(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaStreamSynchronize(s), "D2H");
+      return;
+    }
+    ensure();
+    const int nc = (int)((bytes + kChunk - 1) / kChunk);
+    auto issue = [&](int c) {
+      const int k = c % kSlots;
+      const size_t off = (size_t)c * kChunk, n = std::min(kChunk, bytes - off);
+      ck(cudaMemcpyAsync(h[k], (const char*)src + off, n, cudaMemcpyDeviceToHost, s), "D2H");
+      ck(cudaEventRecord(ev[k], s), "staging");
+    };
+    for (int c = 0; c < std::min(nc, kSlots); ++c) issue(c);
+    for (int c = 0; c < nc; ++c) {
+      const int k = c % kSlots;
+      const size_t off = (size_t)c * kChunk, n = std::min(kChunk, bytes - off);
+      ck(cudaEventSynchronize(ev[k]), "D2H");
+      parallel_memcpy((char*)dst + off, h[k], n);
+      if (c + kSlots < nc) issue(c + kSlots);
+    }
+  }
+};
+
 constexpr size_t kSmemCap = 110 * 1024;  // two CTAs per SM
 constexpr int kThreads = 256;
 constexpr int kFrcBlocks = 148 * 6;  // FRC ring-sum blocks (per-block partials, fixed-order reduce)
@@ -183,6 +346,11 @@ struct vk_rl_plan_s {
   int rank = 3;
   bool pad = true;
   int conv = 0;  // 0: RL plan; 1 / 2: filters::fft_convolve plan, linear / circular
+  // circular fft_convolve on extents that are not 5-smooth: a linear plan on
+  // the periodic extension E = A + K - 1 (offset h = K-1-c), see conv_device
+  vk_rl_plan_s* circ = nullptr;
+  int circ_h[3]{}, circ_e[3]{};
+  DevBuf<float> circ_in, circ_out;
   // slab plans (vk_rl_slab_*): own P rows [own0, own1) of the local domain;
   // halo rows below / above are refreshed by the caller between passes
   bool slab = false;
@@ -264,6 +432,8 @@ struct vk_rl_plan_s {
   std::vector<cudaEvent_t> events;
   double* h_acc = nullptr;  // pinned
   uint64_t launches = 0;
+  Staging staging;  // pinned chunks for pageable host buffers
+  bool cached = false, busy = false;  // plan cache (vk_richardson_lucy & co.)
 
   // Optional per-launch CUDA-event timing, by kernel kind (vk_rl_plan_profile).
   bool prof = false;
@@ -289,6 +459,7 @@ struct vk_rl_plan_s {
     if (ev_join) cudaEventDestroy(ev_join);
     if (h_frc) cudaFreeHost(h_frc);
     delete frc;
+    delete circ;
   }
 };
 
@@ -910,6 +1081,47 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
   for (int i = 0; i < rank; ++i) {
     if (shape[i] == 0) fail(VK_ERR_ARG, "empty image");
     if (psf_shape[i] == 0) fail(VK_ERR_ARG, "empty psf");
+  }
+  if (conv == 2) {
+    // Circular convolution = the 'same' linear convolution of the periodic
+    // extension, cropped (out[n] = sum_j k[j] a[(n + c - j) mod A], filters.cpp:
+    // 184-233): the reference plans any extent with FFTW; the device FFT plans
+    // 5-smooth grids, so any other extent goes through the linear path on
+    // E = A + K - 1 with the image at offset h = K - 1 - c.
+    bool smooth = true;
+    for (int i = 0; i < rank; ++i) smooth = smooth && good_size(shape[i]) == shape[i];
+    if (!smooth) {
+      uint64_t E[VK_MAX_RANK];
+      for (int i = 0; i < rank; ++i) E[i] = shape[i] + psf_shape[i] - 1;
+      vk_rl_plan inner = create_plan(device, rank, E, psf_rank, psf_shape, psf, 0, 1);
+      DeviceGuard dg(device);
+      auto* p = new vk_rl_plan_s();
+      p->device = device;
+      p->rank = rank;
+      p->pad = false;
+      p->conv = 2;
+      p->circ = inner;
+      uint64_t I3[3], K3[3], E3[3];
+      to3(rank, shape, I3);
+      to3(rank, psf_shape, K3);
+      to3(rank, E, E3);
+      p->g = inner->g;
+      p->g.Iz = (int)I3[0];
+      p->g.Iy = (int)I3[1];
+      p->g.Ix = (int)I3[2];
+      for (int a = 0; a < 3; ++a) {
+        p->circ_e[a] = (int)E3[a];
+        p->circ_h[a] = (int)(K3[a] - 1 - (K3[a] - 1) / 2);
+      }
+      for (int i = 0; i < rank; ++i) {
+        p->ishape[i] = shape[i];
+        p->kshape[i] = psf_shape[i];
+        p->dshape[i] = shape[i];
+        p->wshape[i] = inner->wshape[i];
+      }
+      ck(cudaStreamCreateWithFlags(&p->stream, cudaStreamNonBlocking), "cudaStreamCreate");
+      return p;
+    }
   }
   DeviceGuard dg(device);
   auto* p = new vk_rl_plan_s();
@@ -1693,6 +1905,21 @@ void conv_device(vk_rl_plan p, const float* d_img, float* d_out, cudaStream_t s)
   if (!p->conv) fail(VK_ERR_ARG, "plan was not created by vk_conv_plan_create");
   const Geom& g = p->g;
   p->launches = 0;
+  if (p->circ) {  // periodic extension -> linear 'same' convolution -> crop at h
+    const size_t en = (size_t)p->circ_e[0] * p->circ_e[1] * p->circ_e[2];
+    if (p->circ_in.n < en) p->circ_in.alloc(en, "circular extension");
+    if (p->circ_out.n < en) p->circ_out.alloc(en, "circular result");
+    vk::wrap_extend_kernel<<<148 * 4, kThreads, 0, s>>>(d_img, g.Iz, g.Iy, g.Ix, p->circ_in.p, p->circ_e[0],
+                                                         p->circ_e[1], p->circ_e[2], p->circ_h[0], p->circ_h[1],
+                                                         p->circ_h[2]);
+    launch_check(p, "wrap extend");
+    conv_device(p->circ, p->circ_in.p, p->circ_out.p, s);
+    vk::crop_block_kernel<<<148 * 4, kThreads, 0, s>>>(p->circ_out.p, p->circ_e[1], p->circ_e[2], d_out, g.Iz, g.Iy,
+                                                        g.Ix, p->circ_h[0], p->circ_h[1], p->circ_h[2]);
+    launch_check(p, "crop block");
+    p->launches += p->circ->launches;
+    return;
+  }
   x_pass(p, s, vk::XM_FWD, d_img, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr, 0);
   conv_yz(p, s, p->otf.p);
   x_pass(p, s, vk::XM_CONV_OUT, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, nullptr, nullptr, d_out);
@@ -1715,24 +1942,143 @@ void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_
 
 size_t image_count(vk_rl_plan p) { return (size_t)p->g.Iz * p->g.Iy * p->g.Ix; }
 
-// Algorithmic HBM bytes of one launch of each kernel kind: every byte the
-// kernel must move at least once (complex64 spectra in and out, the observed
-// image once, the estimate in and out, the OTF once).  SURVEY.md §8(d).
+// ---- plan cache -----------------------------------------------------------
+// The one-shot entry points (vk_richardson_lucy, vk_rl_step_psf,
+// vk_fft_convolve) replace calls that build their transforms per call
+// (deconv.cpp:332, :196-200; filters.cpp:174-264).  On the CPU that is cheap;
+// on the GPU a plan is ~1.3 GB of cudaMalloc plus two OTF builds at C2.  So
+// plans are kept, keyed on (device, kind, shapes, PSF values), LRU, up to
+// VK_RL_PLAN_CACHE plans (default 2, 0 disables).  A plan in use by another
+// thread is never shared: that caller builds its own.
+struct PlanKey {
+  int device, rank, pad, conv;
+  uint64_t shape[VK_MAX_RANK], kshape[VK_MAX_RANK];
+  std::vector<float> psf;
+  bool operator==(const PlanKey& o) const {
+    return device == o.device && rank == o.rank && pad == o.pad && conv == o.conv &&
+           std::equal(shape, shape + rank, o.shape) && std::equal(kshape, kshape + rank, o.kshape) && psf == o.psf;
+  }
+};
+
+struct PlanCache {
+  std::mutex mu;
+  std::list<std::pair<PlanKey, vk_rl_plan>> lru;  // front = most recent
+  size_t capacity() const {
+    const char* e = std::getenv("VK_RL_PLAN_CACHE");
+    return e ? (size_t)std::max(0, std::atoi(e)) : 2;
+  }
+  static PlanCache& get() {
+    static PlanCache* c = new PlanCache();  // process lifetime: plans die with the context
+    return *c;
+  }
+};
+
+PlanKey make_key(int device, int rank, const uint64_t* shape, const uint64_t* kshape, const float* psf, int pad,
+                 int conv) {
+  PlanKey k{device, rank, pad, conv, {}, {}, {}};
+  size_t kn = 1;
+  for (int i = 0; i < rank; ++i) {
+    k.shape[i] = shape[i];
+    k.kshape[i] = kshape[i];
+    kn *= kshape[i];
+  }
+  k.psf.assign(psf, psf + kn);
+  return k;
+}
+
+// A plan for the key: a cached idle one, else a new one (created outside the lock).
+vk_rl_plan acquire_plan(const PlanKey& k, int psf_rank) {
+  PlanCache& c = PlanCache::get();
+  if (c.capacity() > 0) {
+    std::lock_guard<std::mutex> g(c.mu);
+    for (auto it = c.lru.begin(); it != c.lru.end(); ++it)
+      if (!it->second->busy && it->first == k) {
+        it->second->busy = true;
+        c.lru.splice(c.lru.begin(), c.lru, it);
+        return c.lru.front().second;
+      }
+  }
+  vk_rl_plan p = create_plan(k.device, k.rank, k.shape, psf_rank, k.kshape, k.psf.data(), k.pad, k.conv);
+  p->busy = true;
+  return p;
+}
+
+void release_plan(const PlanKey& k, vk_rl_plan p) {
+  PlanCache& c = PlanCache::get();
+  std::vector<vk_rl_plan> drop;
+  {
+    std::lock_guard<std::mutex> g(c.mu);
+    p->busy = false;
+    if (!p->cached) {
+      if (c.capacity() == 0) {
+        drop.push_back(p);
+      } else {
+        p->cached = true;
+        c.lru.emplace_front(k, p);
+      }
+    }
+    // evict idle plans beyond capacity, least recent first
+    for (auto it = c.lru.end(); c.lru.size() > c.capacity() && it != c.lru.begin();) {
+      --it;
+      if (!it->second->busy) {
+        drop.push_back(it->second);
+        it = c.lru.erase(it);
+      }
+    }
+  }
+  for (vk_rl_plan q : drop) {
+    DeviceGuard dg(q->device);
+    delete q;
+  }
+}
+
+// Runs fn(plan) on a cached plan for the key; the plan returns to the cache.
+template <class F>
+void with_cached_plan(const PlanKey& k, int psf_rank, F&& fn) {
+  vk_rl_plan p = acquire_plan(k, psf_rank);
+  try {
+    fn(p);
+  } catch (...) {
+    release_plan(k, p);
+    throw;
+  }
+  release_plan(k, p);
+}
+
+// Algorithmic HBM bytes of one launch of each kernel kind: every byte of
+// data the kernel must move at least once (complex64 spectra in and out, the
+// observed image once, the estimate in and out).  The OTF is NOT counted
+// (amortisable / regenerable, reported separately:
+// otf_bytes()).
 uint64_t alg_bytes(vk_rl_plan p, int kind) {
   const Geom& g = p->g;
   const uint64_t Sp = (uint64_t)g.Hx * g.Pz * g.Py, Sb = (uint64_t)g.Hx * g.Pz * g.Wy;
-  const uint64_t So = (uint64_t)g.Hx * g.Wz * g.Wy;
   const uint64_t nI = image_count(p), nP = (uint64_t)g.Pz * g.Py * g.Px;
   switch (kind) {
     case VK_KIND_X_FWD: return 4 * nP + 8 * Sp;
     case VK_KIND_X_RATIO: return 16 * Sp + 4 * nI;
     case VK_KIND_X_UPDATE: return 16 * Sp + 8 * nP + 4 * nI;
     case VK_KIND_Y_FWD: return 8 * Sp + 8 * Sb;
-    case VK_KIND_Z_CONV: return 16 * Sb + 8 * So;
+    case VK_KIND_Z_CONV: return 16 * Sb;
     case VK_KIND_Y_INV: return 8 * Sb + 8 * Sp;
-    case VK_KIND_Y_CONV: return 16 * Sp + 8 * So;
-    case VK_KIND_YZ_DATAFLOW: return 16 * Sp + 8 * So;
-    case VK_KIND_YZ_CLUSTER: return 16 * Sp + 8 * So;
+    case VK_KIND_Y_CONV: return 16 * Sp;
+    case VK_KIND_YZ_DATAFLOW: return 16 * Sp;
+    case VK_KIND_YZ_CLUSTER: return 16 * Sp;
+    default: return 0;
+  }
+}
+
+// OTF bytes one launch of `kind` reads from memory (0 when the OTF is
+// rebuilt from its 1D factors, p->ofactored).
+uint64_t otf_bytes(vk_rl_plan p, int kind) {
+  const Geom& g = p->g;
+  if (p->ofactored) return 0;
+  const uint64_t So = (uint64_t)g.Hx * g.Wz * g.Wy;
+  switch (kind) {
+    case VK_KIND_Z_CONV:
+    case VK_KIND_Y_CONV:
+    case VK_KIND_YZ_DATAFLOW:
+    case VK_KIND_YZ_CLUSTER: return 8 * So;
     default: return 0;
   }
 }
@@ -1828,6 +2174,13 @@ vk_status vk_rl_plan_profile(vk_rl_plan p, int enable) {
   });
 }
 
+vk_status vk_rl_plan_otf_bytes(vk_rl_plan p, int n_kinds, uint64_t* otf_bytes_per_launch) {
+  return guarded([&] {
+    if (!p || !otf_bytes_per_launch) fail(VK_ERR_ARG, "NULL argument");
+    for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k) otf_bytes_per_launch[k] = otf_bytes(p, k);
+  });
+}
+
 vk_status vk_rl_plan_profile_read(vk_rl_plan p, int n_kinds, double* ms_total, uint64_t* launches,
                                   uint64_t* alg_bytes_per_launch, int reset) {
   return guarded([&] {
@@ -1884,10 +2237,9 @@ vk_status vk_rl_run(vk_rl_plan p, const float* obs, float* est, const vk_stop_ru
     const size_t n = image_count(p);
     if (p->obs.n < n) p->obs.alloc(n, "observed");
     if (p->out.n < n) p->out.alloc(n, "output");
-    ck(cudaMemcpyAsync(p->obs.p, obs, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "observed H2D");
+    p->staging.h2d(p->obs.p, obs, n * sizeof(float), p->stream);
     run_device(p, p->obs.p, p->out.p, rule, flat_init, trace, p->stream, true);
-    ck(cudaMemcpyAsync(est, p->out.p, n * sizeof(float), cudaMemcpyDeviceToHost, p->stream), "estimate D2H");
-    ck(cudaStreamSynchronize(p->stream), "estimate D2H");
+    p->staging.d2h(est, p->out.p, n * sizeof(float), p->stream);
   });
 }
 
@@ -1936,49 +2288,82 @@ vk_status vk_rl_step(vk_rl_plan p, const float* e, const float* o, float* out) {
     if (!p || !e || !o || !out) fail(VK_ERR_ARG, "NULL argument");
     DeviceGuard dg(p->device);
     const size_t n = image_count(p);
-    DevBuf<float> de, dobs, dout;
+    if (p->obs.n < n) p->obs.alloc(n, "observed");
+    if (p->out.n < n) p->out.alloc(n, "output");
+    DevBuf<float> de;
     de.alloc(n, "estimate");
-    dobs.alloc(n, "observed");
-    dout.alloc(n, "output");
-    ck(cudaMemcpyAsync(de.p, e, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
-    ck(cudaMemcpyAsync(dobs.p, o, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
-    step_device(p, de.p, dobs.p, dout.p, p->stream);
-    ck(cudaMemcpyAsync(out, dout.p, n * sizeof(float), cudaMemcpyDeviceToHost, p->stream), "D2H");
-    ck(cudaStreamSynchronize(p->stream), "rl_step");
+    p->staging.h2d(de.p, e, n * sizeof(float), p->stream);
+    p->staging.h2d(p->obs.p, o, n * sizeof(float), p->stream);
+    step_device(p, de.p, p->obs.p, p->out.p, p->stream);
+    p->staging.d2h(out, p->out.p, n * sizeof(float), p->stream);
   });
 }
 
 vk_status vk_richardson_lucy(int device, int rank, const uint64_t* shape, const float* obs, int psf_rank,
                              const uint64_t* psf_shape, const float* psf, const vk_stop_rule* rule, int flat_init,
                              float* est, vk_trace* trace) {
-  vk_rl_plan p = nullptr;
-  vk_status st = guarded([&] {
+  return guarded([&] {
     check_rule(rule);  // deconv.cpp:306-309
     if (rank != psf_rank) fail(VK_ERR_SHAPE, "ShapeMismatch: psf rank must match the image rank");
     if (!shape || !obs || !psf_shape || !psf || !est) fail(VK_ERR_ARG, "NULL argument");
-    p = create_plan(device, rank, shape, psf_rank, psf_shape, psf, 1);
+    if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
+    with_cached_plan(make_key(device, rank, shape, psf_shape, psf, 1, 0), psf_rank, [&](vk_rl_plan p) {
+      const vk_status st = vk_rl_run(p, obs, est, rule, flat_init, trace);
+      if (st != VK_OK) fail(st, g_last_error);
+    });
   });
-  if (st != VK_OK) return st;
-  st = vk_rl_run(p, obs, est, rule, flat_init, trace);
-  std::string keep = g_last_error;
-  vk_rl_plan_destroy(p);
-  g_last_error = keep;
-  return st;
+}
+
+vk_status vk_richardson_lucy_batch(int device, int rank, const uint64_t* shape, int n, const float* const* obs,
+                                   int psf_rank, const uint64_t* psf_shape, const float* psf, const vk_stop_rule* rule,
+                                   int flat_init, float* const* est, vk_trace* traces) {
+  return guarded([&] {
+    check_rule(rule);
+    if (rank != psf_rank) fail(VK_ERR_SHAPE, "ShapeMismatch: psf rank must match the image rank");
+    if (!shape || !psf_shape || !psf || n < 0 || (n > 0 && (!obs || !est))) fail(VK_ERR_ARG, "NULL argument");
+    if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
+    if (n == 0) return;
+    with_cached_plan(make_key(device, rank, shape, psf_shape, psf, 1, 0), psf_rank, [&](vk_rl_plan p) {
+      const vk_status st = vk_rl_run_batch(p, n, obs, est, rule, flat_init, traces);
+      if (st != VK_OK) fail(st, g_last_error);
+    });
+  });
 }
 
 vk_status vk_rl_step_psf(int device, int rank, const uint64_t* shape, const float* e, const float* o, int psf_rank,
                          const uint64_t* psf_shape, const float* psf, float* out) {
-  vk_rl_plan p = nullptr;
-  vk_status st = guarded([&] {
+  return guarded([&] {
     if (!shape || !e || !o || !psf_shape || !psf || !out) fail(VK_ERR_ARG, "NULL argument");
-    p = create_plan(device, rank, shape, psf_rank, psf_shape, psf, 0);
+    if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
+    if (psf_rank != rank) fail(VK_ERR_SHAPE, "ShapeMismatch: psf rank must match the image rank");
+    with_cached_plan(make_key(device, rank, shape, psf_shape, psf, 0, 0), psf_rank, [&](vk_rl_plan p) {
+      const vk_status st = vk_rl_step(p, e, o, out);
+      if (st != VK_OK) fail(st, g_last_error);
+    });
   });
-  if (st != VK_OK) return st;
-  st = vk_rl_step(p, e, o, out);
-  std::string keep = g_last_error;
-  vk_rl_plan_destroy(p);
-  g_last_error = keep;
-  return st;
+}
+
+vk_status vk_plan_cache_clear(void) {
+  return guarded([&] {
+    PlanCache& c = PlanCache::get();
+    std::vector<vk_rl_plan> drop;
+    {
+      std::lock_guard<std::mutex> g(c.mu);
+      for (auto it = c.lru.begin(); it != c.lru.end();) {
+        if (!it->second->busy) {
+          drop.push_back(it->second);
+          it = c.lru.erase(it);
+        } else {
+          it->second->cached = false;  // freed by its user on release
+          it = c.lru.erase(it);
+        }
+      }
+    }
+    for (vk_rl_plan q : drop) {
+      DeviceGuard dg(q->device);
+      delete q;
+    }
+  });
 }
 
 // ---- single-volume slab decomposition ---------------------
@@ -2031,26 +2416,26 @@ vk_status vk_conv_run(vk_rl_plan p, const float* img, float* out) {
     if (!p || !img || !out) fail(VK_ERR_ARG, "NULL argument");
     DeviceGuard dg(p->device);
     const size_t n = image_count(p);
-    DevBuf<float> di, dout;
-    di.alloc(n, "image");
-    dout.alloc(n, "output");
-    ck(cudaMemcpyAsync(di.p, img, n * sizeof(float), cudaMemcpyHostToDevice, p->stream), "H2D");
-    conv_device(p, di.p, dout.p, p->stream);
-    ck(cudaMemcpyAsync(out, dout.p, n * sizeof(float), cudaMemcpyDeviceToHost, p->stream), "D2H");
-    ck(cudaStreamSynchronize(p->stream), "fft_convolve");
+    if (p->obs.n < n) p->obs.alloc(n, "image");
+    if (p->out.n < n) p->out.alloc(n, "output");
+    p->staging.h2d(p->obs.p, img, n * sizeof(float), p->stream);
+    conv_device(p, p->obs.p, p->out.p, p->stream);
+    p->staging.d2h(out, p->out.p, n * sizeof(float), p->stream);
   });
 }
 
 vk_status vk_fft_convolve(int device, int rank, const uint64_t* shape, const float* img, int kernel_rank,
                           const uint64_t* kernel_shape, const float* kernel, int circular, float* out) {
-  vk_rl_plan p = nullptr;
-  vk_status st = vk_conv_plan_create(device, rank, shape, kernel_rank, kernel_shape, kernel, circular, &p);
-  if (st != VK_OK) return st;
-  st = vk_conv_run(p, img, out);
-  std::string keep = g_last_error;
-  vk_rl_plan_destroy(p);
-  g_last_error = keep;
-  return st;
+  return guarded([&] {
+    if (!shape || !kernel_shape || !kernel || !img || !out) fail(VK_ERR_ARG, "NULL argument");
+    if (rank < 1 || rank > VK_MAX_RANK) fail(VK_ERR_ARG, "rank must be 1, 2 or 3");
+    if (kernel_rank != rank) fail(VK_ERR_SHAPE, "ShapeMismatch: fft_convolve: rank mismatch");
+    with_cached_plan(make_key(device, rank, shape, kernel_shape, kernel, 0, circular ? 2 : 1), kernel_rank,
+                     [&](vk_rl_plan p) {
+                       const vk_status st = vk_conv_run(p, img, out);
+                       if (st != VK_OK) fail(st, g_last_error);
+                     });
+  });
 }
 
 vk_status vk_rl_slab_plan_create(int device, const uint64_t* shape, const uint64_t* psf_shape, const float* psf,

@@ -30,6 +30,7 @@
 #include "voxelkit/errors.hpp"
 #include "voxelkit/image.hpp"
 #include "voxelkit/registry.hpp"
+#include "voxelkit_b200/deconv_batch.hpp"
 #include "vk_rl.h"
 
 namespace voxelkit::deconv {
@@ -67,6 +68,41 @@ void check(vk_status st) {
 }
 
 std::vector<std::uint64_t> u64(const Shape& s) { return {s.begin(), s.end()}; }
+
+// Caller-side buffers of one vk_trace.
+struct TraceBuf {
+  std::vector<double> metric, wall, ll;
+  vk_trace tr{};
+  explicit TraceBuf(int max_iters) {
+    const int cap = max_iters > 0 ? max_iters : 1;
+    metric.resize(cap);
+    wall.resize(cap);
+    ll.resize(cap);
+    tr.capacity = cap;
+    tr.metric = metric.data();
+    tr.wall_s = wall.data();
+    tr.log_likelihood = ll.data();
+  }
+};
+
+// The C ABI's stopping rule; FRC uses the x spacing of the observed image
+// (deconv.cpp:286-287).
+vk_stop_rule c_rule(const StoppingRule& rule, const NdImage& obs) {
+  const double spacing = obs.spacing() ? obs.spacing()->back() : 0.0;
+  return vk_stop_rule{static_cast<int>(rule.metric), rule.rel_tol, rule.patience, rule.max_iters, spacing};
+}
+
+RlResult assemble(const NdImage& obs, const StoppingRule& rule, std::vector<float> est, const TraceBuf& t) {
+  RlResult res;
+  res.estimate = NdImage::f32_like(obs, std::move(est));
+  for (int i = 0; i < t.tr.iters_run; ++i) {
+    res.trace.records.push_back({i + 1, to_string(rule.metric), t.metric[i], t.wall[i]});
+    res.trace.log_likelihood.push_back(t.ll[i]);
+  }
+  res.trace.fft_shape.assign(t.tr.fft_shape, t.tr.fft_shape + obs.rank());
+  res.trace.stop_reason = t.tr.stop_reason == 1 ? "converged" : "max_iters";
+  return res;
+}
 
 }  // namespace
 
@@ -140,36 +176,74 @@ RlResult richardson_lucy(const NdImage& observed, const NdImage& psf, const Stop
   const NdImage k = psf.as_f32();
   const auto sh = u64(obs.shape());
   const auto ks = u64(k.shape());
-  const int cap = rule.max_iters > 0 ? rule.max_iters : 1;
-  std::vector<double> metric(cap), wall(cap), ll(cap);
-  vk_trace tr{};
-  tr.capacity = cap;
-  tr.metric = metric.data();
-  tr.wall_s = wall.data();
-  tr.log_likelihood = ll.data();
-  // FRC uses the x spacing of the observed image (deconv.cpp:286-287)
-  const double spacing = obs.spacing() ? obs.spacing()->back() : 0.0;
-  const vk_stop_rule r{static_cast<int>(rule.metric), rule.rel_tol, rule.patience, rule.max_iters, spacing};
+  TraceBuf t(rule.max_iters);
+  const vk_stop_rule r = c_rule(rule, obs);
   std::vector<float> est(obs.size());
+  // one-shot call: the C ABI keeps the plan (OTFs, work buffers) cached for
+  // the next call on the same shape and PSF
   check(vk_richardson_lucy(device(), static_cast<int>(sh.size()), sh.data(), obs.f32_values().data(),
                            static_cast<int>(ks.size()), ks.data(), k.f32_values().data(), &r, flat_init ? 1 : 0,
-                           est.data(), &tr));
-  RlResult res;
-  res.estimate = NdImage::f32_like(obs, std::move(est));
-  for (int i = 0; i < tr.iters_run; ++i) {
-    res.trace.records.push_back({i + 1, to_string(rule.metric), metric[i], wall[i]});
-    res.trace.log_likelihood.push_back(ll[i]);
+                           est.data(), &t.tr));
+  return assemble(obs, rule, std::move(est), t);
+}
+
+std::vector<RlResult> richardson_lucy_batch(const std::vector<NdImage>& observed, const NdImage& psf,
+                                            const StoppingRule& rule, bool flat_init) {
+  std::vector<RlResult> out;
+  const auto sequential = [&] {
+    out.clear();
+    for (const NdImage& o : observed) out.push_back(richardson_lucy(o, psf, rule, flat_init));
+    return out;
+  };
+  if (observed.size() < 2) return sequential();
+  const NdImage k = psf.as_f32();
+  std::vector<NdImage> obs;
+  obs.reserve(observed.size());
+  for (const NdImage& o : observed) obs.push_back(o.as_f32());
+  const vk_stop_rule r = c_rule(rule, obs[0]);
+  for (const NdImage& o : obs)  // one plan serves volumes of one shape (and one FRC spacing)
+    if (o.shape() != obs[0].shape() || c_rule(rule, o).spacing != r.spacing || k.rank() != o.rank())
+      return sequential();
+  const auto sh = u64(obs[0].shape());
+  const auto ks = u64(k.shape());
+  const int n = static_cast<int>(obs.size());
+  std::vector<std::vector<float>> est(n, std::vector<float>(obs[0].size()));
+  std::vector<TraceBuf> tb;
+  tb.reserve(n);
+  std::vector<vk_trace> trs(n);
+  std::vector<const float*> ip(n);
+  std::vector<float*> op(n);
+  for (int i = 0; i < n; ++i) {
+    tb.emplace_back(rule.max_iters);
+    trs[i] = tb[i].tr;
+    ip[i] = obs[i].f32_values().data();
+    op[i] = est[i].data();
   }
-  res.trace.fft_shape.assign(tr.fft_shape, tr.fft_shape + obs.rank());
-  res.trace.stop_reason = tr.stop_reason == 1 ? "converged" : "max_iters";
-  return res;
+  // one cached plan, volumes on its concurrent batch lanes
+  const vk_status st =
+      vk_richardson_lucy_batch(device(), static_cast<int>(sh.size()), sh.data(), n, ip.data(),
+                               static_cast<int>(ks.size()), ks.data(), k.f32_values().data(), &r, flat_init ? 1 : 0,
+                               op.data(), trs.data());
+  // any failure: the per-volume loop throws exactly what the reference would
+  if (st != VK_OK) return sequential();
+  for (int i = 0; i < n; ++i) {
+    tb[i].tr = trs[i];
+    out.push_back(assemble(obs[i], rule, std::move(est[i]), tb[i]));
+  }
+  return out;
 }
 
 }  // namespace voxelkit::deconv
 
 namespace voxelkit::detail {
 
+void register_filter_ops_b200(ExecutionRegistry& reg);  // host/filters_b200.cpp
+
 void register_deconv_ops(ExecutionRegistry& reg) {
+  // The registry is filled register_filter_ops first, register_deconv_ops
+  // last (registry.cpp:87-93) and add() replaces an entry, so this puts
+  // "fft_convolve" on the GPU for both tags too (filters.cpp:316-323).
+  register_filter_ops_b200(reg);
   using StepSig = NdImage(const NdImage&, const NdImage&, const NdImage&);
   auto step = [](const NdImage& estimate, const NdImage& observed, const NdImage& psf) {
     deconv::RlTransforms transforms(estimate.shape(), psf.as_f32(), 1);

@@ -16,7 +16,11 @@
 #include "voxelkit/errors.hpp"
 #include "voxelkit/filters.hpp"
 #include "voxelkit/image.hpp"
+#include "voxelkit/io.hpp"
 #include "voxelkit/synth.hpp"
+#include "voxelkit_b200/deconv_batch.hpp"
+#include <fstream>
+#include <iterator>
 
 extern "C" {
 int vkref_richardson_lucy(int rank, const std::uint64_t* shape, const float* observed, int psf_rank,
@@ -27,6 +31,10 @@ int vkref_richardson_lucy(int rank, const std::uint64_t* shape, const float* obs
 int vkref_rl_step(int rank, const std::uint64_t* shape, const float* estimate, const float* observed,
                   const std::uint64_t* psf_shape, const float* psf, int accelerated, float* out, char* err,
                   int errlen);
+int vkref_fft_convolve(int rank, const std::uint64_t* shape, const float* img, const std::uint64_t* kshape,
+                       const float* kernel, int circular, float* out, char* err, int errlen);
+int vkref_write_volume(const char* path, int elem, int rank, const std::uint64_t* shape, const void* data,
+                       const double* spacing, char* err, int errlen) __attribute__((weak));
 }
 
 using namespace voxelkit;
@@ -226,6 +234,108 @@ int main() {
     } catch (const ShapeMismatch& ex) {
       report(std::string(ex.what()) == "ShapeMismatch: rl_step: transforms were prepared for [6,14,18]",
              "rl_step transforms shape error", ex.what());
+    }
+  }
+  // richardson_lucy_batch: element-wise identical to richardson_lucy
+  {
+    const NdImage k = synth::gaussian_psf({5, 5, 5}, {1.0});
+    std::vector<NdImage> vols;
+    for (int i = 0; i < 3; ++i) vols.push_back(blurred_blobs({12, 40, 36}, 3, 40 + i, k));
+    deconv::StoppingRule rule{deconv::StopMetric::si_psnr_vs_input, 1e-300, 4, 4};
+    const auto batch = deconv::richardson_lucy_batch(vols, k, rule, false);
+    bool ok = batch.size() == vols.size();
+    double worst = 0;
+    for (std::size_t i = 0; ok && i < vols.size(); ++i) {
+      const deconv::RlResult one = deconv::richardson_lucy(vols[i], k, rule, false);
+      const auto a = batch[i].estimate.f32_values(), b = one.estimate.f32_values();
+      ok = std::equal(a.begin(), a.end(), b.begin()) && batch[i].trace.records.size() == one.trace.records.size() &&
+           batch[i].trace.stop_reason == one.trace.stop_reason && batch[i].trace.fft_shape == one.trace.fft_shape;
+      for (std::size_t r = 0; ok && r < one.trace.records.size(); ++r)
+        ok = batch[i].trace.records[r].value == one.trace.records[r].value &&
+             batch[i].trace.log_likelihood[r] == one.trace.log_likelihood[r];
+      const RefRun ref = ref_rl(vols[i], k, rule, false);
+      worst = std::max(worst, rel_l2(a, ref.est));
+    }
+    char buf[96];
+    std::snprintf(buf, sizeof buf, "worst relL2 vs reference %.2e", worst);
+    report(ok && worst <= 1e-3, "richardson_lucy_batch == per-volume richardson_lucy", buf);
+    // the first failing volume's exception, as the per-volume loop throws it
+    std::vector<float> bad(vols[1].f32_values().begin(), vols[1].f32_values().end());
+    bad[5] = -1.f;
+    vols[1] = NdImage::f32({12, 40, 36}, bad);
+    try {
+      deconv::richardson_lucy_batch(vols, k, rule, false);
+      report(false, "richardson_lucy_batch error", "no exception");
+    } catch (const NegativeInput& e) {
+      report(std::string(e.what()) == "NegativeInput: observed image must be nonnegative",
+             "richardson_lucy_batch error", e.what());
+    }
+  }
+  // filters::fft_convolve through the registry (both tags) on the GPU vs the reference
+  {
+    struct Case {
+      Shape a, k;
+      bool circ;
+    };
+    const Case cases[] = {{{20, 33, 40}, {5, 4, 7}, false}, {{16, 18, 20}, {3, 3, 5}, true},
+                          {{7, 11, 13}, {3, 4, 5}, true}, {{50, 61}, {9, 8}, false}};
+    for (const Case& c : cases) {
+      std::size_t n = 1, kn = 1;
+      for (auto v : c.a) n *= v;
+      for (auto v : c.k) kn *= v;
+      std::vector<float> a(n), k(kn), ref(n);
+      for (std::size_t i = 0; i < n; ++i) a[i] = std::sin(0.37f * (float)i) + 0.1f * (float)(i % 7);
+      for (std::size_t i = 0; i < kn; ++i) k[i] = 0.5f + std::cos(0.9f * (float)i);
+      std::vector<std::uint64_t> s(c.a.begin(), c.a.end()), ks(c.k.begin(), c.k.end());
+      char err[256];
+      vkref_fft_convolve((int)s.size(), s.data(), a.data(), ks.data(), k.data(), c.circ, ref.data(), err, 256);
+      for (BackendId b : {BackendId::reference, BackendId::accelerated}) {
+        const NdImage out = filters::fft_convolve(NdImage::f32(c.a, a).with_backend(b), NdImage::f32(c.k, k), c.circ);
+        char buf[96];
+        std::snprintf(buf, sizeof buf, "relL2 %.2e", rel_l2(out.f32_values(), ref));
+        report(rel_l2(out.f32_values(), ref) <= 1e-5 && out.backend() == b,
+               std::string("fft_convolve registry ") + to_string(b) + (c.circ ? " circular " : " linear ") +
+                   shape_to_string(c.a),
+               buf);
+      }
+    }
+    try {
+      filters::fft_convolve(NdImage::f32({4, 4}, std::vector<float>(16, 1.f)),
+                            NdImage::f32({5, 3}, std::vector<float>(15, 1.f)), true);
+      report(false, "fft_convolve KernelTooLarge", "no exception");
+    } catch (const KernelTooLarge& e) {
+      report(std::string(e.what()) == "KernelTooLarge: circular convolution needs kernel <= image",
+             "fft_convolve KernelTooLarge", e.what());
+    }
+  }
+  // io::write_volume / read_volume (io_b200.cpp over vk_io.h): round trip, and
+  // byte-identical to the reference writer when it is linked in
+  {
+    std::vector<float> v(3 * 4 * 5);
+    for (std::size_t i = 0; i < v.size(); ++i) v[i] = 0.25f * (float)i - 3.f;
+    const NdImage img = NdImage::f32({3, 4, 5}, v).with_spacing({2.0, 0.5, 0.125});
+    const std::string ours = "/tmp/vk_dropin_io_ours.ndiv", theirs = "/tmp/vk_dropin_io_ref.ndiv";
+    io::write_volume(ours, img);
+    const NdImage back = io::read_volume(ours);
+    const auto bv = back.f32_values();
+    bool ok = back.shape() == img.shape() && back.spacing() && *back.spacing() == *img.spacing() &&
+              std::equal(bv.begin(), bv.end(), v.begin());
+    if (vkref_write_volume) {
+      const std::uint64_t sh[3] = {3, 4, 5};
+      const double sp[3] = {2.0, 0.5, 0.125};
+      char err[256];
+      vkref_write_volume(theirs.c_str(), 0, 3, sh, v.data(), sp, err, 256);
+      std::ifstream fa(ours, std::ios::binary), fb(theirs, std::ios::binary);
+      const std::string A((std::istreambuf_iterator<char>(fa)), {}), B((std::istreambuf_iterator<char>(fb)), {});
+      ok = ok && A == B;
+    }
+    report(ok, "io write/read round trip (byte-identical to the reference writer)");
+    try {
+      io::read_volume("/tmp/vk_dropin_io_missing.ndiv");
+      report(false, "io read missing file");
+    } catch (const Error& e) {
+      report(std::string(e.what()) == "cannot open '/tmp/vk_dropin_io_missing.ndiv'", "io read missing file",
+             e.what());
     }
   }
   // trace CSV (deconv.cpp:85-96)

@@ -15,7 +15,7 @@ def test_header_symbols_exported():
     L = vk.lib()
     missing = [n for n in names if not hasattr(L, n)]
     assert not missing, missing
-    assert L.vk_abi_version() == 3
+    assert L.vk_abi_version() == 4
 
 
 def test_good_size_matches_oracle():
@@ -73,3 +73,22 @@ def test_trace_csv_format():
     t = vk.IterationTrace([vk.IterationRecord(1, "si_psnr_vs_input", 12.5, 0.25),
                            vk.IterationRecord(2, "frc_resolution", float("inf"), 0.5)])
     assert t.to_csv() == "iter,metric,value,wall_time_s\n1,si_psnr_vs_input,12.5,0.25\n2,frc_resolution,inf,0.5\n"
+
+
+def test_bench_roofline_groups_kinds_by_kernel():
+    """bench.py's §8(d) roofline: kinds of one kernel are summed, OTF bytes are
+    reported beside the algorithmic bytes and never inside them."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    prof = {"x_ratio": (10.0, 10, 500), "x_update": (20.0, 10, 900), "z_conv": (25.0, 20, 400),
+            "y_fwd": (1.0, 0, 0)}
+    k = bench.roofline(prof, {"z_conv": 256}, peak=1.0, steps=10)
+    assert set(k) == {"xpass", "zpass"}
+    assert k["xpass"]["bytes"] == 10 * 500 + 10 * 900 and k["xpass"]["ms"] == 30.0
+    assert abs(k["xpass"]["gbs"] - (14000 / 0.030) / 1e9) < 1e-12
+    assert k["zpass"]["otf_bytes"] == 20 * 256 and k["zpass"]["bytes"] == 20 * 400

@@ -68,8 +68,23 @@ def test_errors_match_reference_types():
         vk.fft_convolve(np.ones((4, 4), np.float32), np.ones((3,), np.float32))
     with pytest.raises(vk.KernelTooLarge, match="KernelTooLarge: circular convolution needs kernel <= image"):
         vk.fft_convolve(np.ones((4, 4), np.float32), np.ones((5, 3), np.float32), circular=True)
-    with pytest.raises(vk.Unsupported):  # 7 is not 5-smooth: no Bluestein on this path yet
-        vk.fft_convolve(np.ones((7, 8), np.float32), np.ones((3, 3), np.float32), circular=True)
+
+
+@pytest.mark.parametrize("shape,kshape", [((7, 8), (3, 3)), ((7,), (7,)), ((11, 13, 14), (4, 5, 3)),
+                                          ((31, 37), (31, 6)), ((9, 49, 7), (2, 1, 7))])
+def test_circular_any_extent(shape, kshape):
+    """Circular mode on extents the device FFT does not plan (filters.cpp:184-233:
+    FFTW plans any length): periodic extension + linear convolution + crop."""
+    rng = np.random.default_rng(sum(shape) * 3 + sum(kshape))
+    a = rng.standard_normal(shape).astype(np.float32)
+    k = rng.standard_normal(kshape).astype(np.float32)
+    want = O.fft_convolve(a, k, True)
+    got = vk.fft_convolve(a, k, circular=True)
+    assert got.shape == a.shape
+    assert rel_l2(got, want) <= TOL
+    plan = vk.ConvPlan(shape, k, circular=True)
+    assert np.array_equal(plan.run(a), got)
+    plan.close()
 
 
 def test_blur_matches_cli_synthesis():
