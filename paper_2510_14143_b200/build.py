@@ -82,13 +82,16 @@ def build_cli(verbose: bool = False) -> str:
     return CLI
 
 
-def build(force: bool = False, verbose: bool = False) -> str:
-    if not force and up_to_date():
+def build(force: bool = False, verbose: bool = False, variant: str = "", extra_flags=()) -> str:
+    """variant: a side build (lib/<variant>/libvkrl.so, own objects) with
+    extra_flags, for A/B measurements (load it with VK_RL_LIB=...)."""
+    lib = os.path.join(LIBDIR, variant, "libvkrl.so") if variant else LIB
+    if not variant and not force and up_to_date():
         return LIB
-    os.makedirs(LIBDIR, exist_ok=True)
-    objdir = os.path.join(ROOT, "build", "obj")
+    os.makedirs(os.path.dirname(lib), exist_ok=True)
+    objdir = os.path.join(ROOT, "build", "obj" + ("_" + variant if variant else ""))
     os.makedirs(objdir, exist_ok=True)
-    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"]
+    compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra_flags)
 
     def compile_one(unit):
         src, extra, obj = unit
@@ -108,7 +111,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             raise RuntimeError(f"nvcc failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
         if verbose and r.stderr:
             print(r.stderr)
-    tmp = LIB + ".tmp"
+    tmp = lib + ".tmp"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
            *[os.path.join(objdir, u[2]) for u in units()]]
     if verbose:
@@ -116,10 +119,16 @@ def build(force: bool = False, verbose: bool = False) -> str:
     r = subprocess.run(cmd, capture_output=True, text=True)
     if r.returncode != 0:
         raise RuntimeError(f"nvcc (link) failed ({r.returncode}):\n{r.stdout}\n{r.stderr}")
-    os.replace(tmp, LIB)
+    os.replace(tmp, lib)
+    if variant:
+        return lib
     build_cli(verbose)
     return LIB
 
 
 if __name__ == "__main__":
-    print(build(force="--force" in sys.argv, verbose=True))
+    if "--variant" in sys.argv:  # python -m paper_2510_14143_b200.build --variant NAME -DFLAG=1 ...
+        i = sys.argv.index("--variant")
+        print(build(verbose=False, variant=sys.argv[i + 1], extra_flags=sys.argv[i + 2:]))
+    else:
+        print(build(force="--force" in sys.argv, verbose=True))

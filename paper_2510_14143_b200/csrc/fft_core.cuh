@@ -38,6 +38,79 @@ struct LinePlan {
   const float2* tw2;  // fast path: pass-2 twiddles, butterfly-major (reg::load_twiddles2 layout), global
 };
 
+// ---- complex arithmetic ----------------------------------------------------
+// On sm_100a the FP32 pipe has packed two-lane forms (FADD2 / FMUL2 / FFMA2,
+// PTX add/sub/mul/fma.rn.f32x2) whose operands can broadcast one lane
+// (.F32) or swap the lanes (.LO_HI) for free.  A float2 complex value is one
+// such register pair, so a complex add is ONE instruction, a +/- i*b ONE fused
+// multiply-add with a (+-1, -+1) constant pair, and a complex product TWO
+// (instead of 2, 2 and 4 scalar ones).  The transforms are issue-bound
+// (ncu: ~590 M warp instructions per C2 iteration, issue active 51-64%),
+// so this is a straight cut of their instruction count.  Products round
+// like fmaf pairs (one rounding per fma), as before.
+// VK_SCALAR_CPLX=1 builds the scalar forms (A/B measurements).
+#if !defined(VK_SCALAR_CPLX) || !VK_SCALAR_CPLX
+namespace pk {
+__device__ __forceinline__ unsigned long long u(float2 v) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "f"(v.x), "f"(v.y));
+  return r;
+}
+__device__ __forceinline__ float2 f(unsigned long long r) {
+  float2 v;
+  asm("mov.b64 {%0, %1}, %2;" : "=f"(v.x), "=f"(v.y) : "l"(r));
+  return v;
+}
+__device__ __forceinline__ float2 add(float2 a, float2 b) {
+  unsigned long long r;
+  asm("add.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u(a)), "l"(u(b)));
+  return f(r);
+}
+__device__ __forceinline__ float2 sub(float2 a, float2 b) {
+  unsigned long long r;
+  asm("sub.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u(a)), "l"(u(b)));
+  return f(r);
+}
+__device__ __forceinline__ float2 mul(float2 a, float2 b) {
+  unsigned long long r;
+  asm("mul.rn.f32x2 %0, %1, %2;" : "=l"(r) : "l"(u(a)), "l"(u(b)));
+  return f(r);
+}
+__device__ __forceinline__ float2 fma(float2 a, float2 b, float2 c) {  // a*b + c
+  unsigned long long r;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(r) : "l"(u(a)), "l"(u(b)), "l"(u(c)));
+  return f(r);
+}
+__device__ __forceinline__ float2 bc(float x) { return make_float2(x, x); }
+__device__ __forceinline__ float2 sw(float2 a) { return make_float2(a.y, a.x); }
+}  // namespace pk
+
+__device__ __forceinline__ float2 cadd(float2 a, float2 b) { return pk::add(a, b); }
+__device__ __forceinline__ float2 csub(float2 a, float2 b) { return pk::sub(a, b); }
+__device__ __forceinline__ float2 cmul(float2 a, float2 b) {  // (a.x b - a.y (b.y, -b.x))
+  return pk::fma(pk::bc(a.y), make_float2(-b.y, b.x), pk::mul(pk::bc(a.x), b));
+}
+__device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
+  return pk::fma(pk::bc(a.y), pk::sw(b), pk::mul(pk::bc(a.x), make_float2(b.x, -b.y)));
+}
+__device__ __forceinline__ float2 cscale(float2 a, float s) { return pk::mul(a, pk::bc(s)); }
+// a + s*b, real s
+__device__ __forceinline__ float2 caxpy(float s, float2 b, float2 a) { return pk::fma(pk::bc(s), b, a); }
+// Multiply by -i (forward) or +i (inverse).
+template <bool INV>
+__device__ __forceinline__ float2 mul_mi(float2 a) {
+  return pk::mul(pk::sw(a), INV ? make_float2(-1.f, 1.f) : make_float2(1.f, -1.f));
+}
+// t + s*(-+i)*u and t - s*(-+i)*u in one packed fma each (s real)
+template <bool INV>
+__device__ __forceinline__ float2 add_mi(float2 t, float2 u, float s = 1.f) {
+  return pk::fma(pk::sw(u), INV ? make_float2(-s, s) : make_float2(s, -s), t);
+}
+template <bool INV>
+__device__ __forceinline__ float2 sub_mi(float2 t, float2 u, float s = 1.f) {
+  return pk::fma(pk::sw(u), INV ? make_float2(s, -s) : make_float2(-s, s), t);
+}
+#else
 __device__ __forceinline__ float2 cadd(float2 a, float2 b) { return make_float2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ float2 csub(float2 a, float2 b) { return make_float2(a.x - b.x, a.y - b.y); }
 __device__ __forceinline__ float2 cmul(float2 a, float2 b) {
@@ -47,12 +120,21 @@ __device__ __forceinline__ float2 cmulc(float2 a, float2 b) {  // a * conj(b)
   return make_float2(fmaf(a.x, b.x, a.y * b.y), fmaf(a.y, b.x, -a.x * b.y));
 }
 __device__ __forceinline__ float2 cscale(float2 a, float s) { return make_float2(a.x * s, a.y * s); }
-__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
-// Multiply by -i (forward) or +i (inverse).
+__device__ __forceinline__ float2 caxpy(float s, float2 b, float2 a) { return make_float2(fmaf(s, b.x, a.x), fmaf(s, b.y, a.y)); }
 template <bool INV>
 __device__ __forceinline__ float2 mul_mi(float2 a) {
   return INV ? make_float2(-a.y, a.x) : make_float2(a.y, -a.x);
 }
+template <bool INV>
+__device__ __forceinline__ float2 add_mi(float2 t, float2 u, float s = 1.f) {
+  return cadd(t, mul_mi<INV>(cscale(u, s)));
+}
+template <bool INV>
+__device__ __forceinline__ float2 sub_mi(float2 t, float2 u, float s = 1.f) {
+  return csub(t, mul_mi<INV>(cscale(u, s)));
+}
+#endif
+__device__ __forceinline__ float2 cconj(float2 a) { return make_float2(a.x, -a.y); }
 
 template <bool INV>
 __device__ __forceinline__ void dft2(float2* v) {
@@ -66,21 +148,20 @@ __device__ __forceinline__ void dft3(float2* v) {
   const float c = -0.5f, s = 0.86602540378443864676f;
   float2 a = cadd(v[1], v[2]), b = csub(v[1], v[2]);
   float2 y0 = cadd(v[0], a);
-  float2 t = make_float2(fmaf(c, a.x, v[0].x), fmaf(c, a.y, v[0].y));
-  float2 u = mul_mi<INV>(cscale(b, s));
+  float2 t = caxpy(c, a, v[0]);
   v[0] = y0;
-  v[1] = cadd(t, u);
-  v[2] = csub(t, u);
+  v[1] = add_mi<INV>(t, b, s);
+  v[2] = sub_mi<INV>(t, b, s);
 }
 
 template <bool INV>
 __device__ __forceinline__ void dft4(float2* v) {
   float2 a0 = cadd(v[0], v[2]), a1 = csub(v[0], v[2]);
-  float2 a2 = cadd(v[1], v[3]), a3 = mul_mi<INV>(csub(v[1], v[3]));
+  float2 a2 = cadd(v[1], v[3]), d = csub(v[1], v[3]);
   v[0] = cadd(a0, a2);
   v[2] = csub(a0, a2);
-  v[1] = cadd(a1, a3);
-  v[3] = csub(a1, a3);
+  v[1] = add_mi<INV>(a1, d);
+  v[3] = sub_mi<INV>(a1, d);
 }
 
 template <bool INV>
@@ -90,15 +171,15 @@ __device__ __forceinline__ void dft5(float2* v) {
   float2 a1 = cadd(v[1], v[4]), b1 = csub(v[1], v[4]);
   float2 a2 = cadd(v[2], v[3]), b2 = csub(v[2], v[3]);
   float2 y0 = cadd(v[0], cadd(a1, a2));
-  float2 t1 = make_float2(v[0].x + c1 * a1.x + c2 * a2.x, v[0].y + c1 * a1.y + c2 * a2.y);
-  float2 t2 = make_float2(v[0].x + c2 * a1.x + c1 * a2.x, v[0].y + c2 * a1.y + c1 * a2.y);
-  float2 u1 = mul_mi<INV>(make_float2(s1 * b1.x + s2 * b2.x, s1 * b1.y + s2 * b2.y));
-  float2 u2 = mul_mi<INV>(make_float2(s2 * b1.x - s1 * b2.x, s2 * b1.y - s1 * b2.y));
+  float2 t1 = caxpy(c2, a2, caxpy(c1, a1, v[0]));
+  float2 t2 = caxpy(c1, a2, caxpy(c2, a1, v[0]));
+  float2 w1 = caxpy(s2, b2, cscale(b1, s1));
+  float2 w2 = caxpy(-s1, b2, cscale(b1, s2));
   v[0] = y0;
-  v[1] = cadd(t1, u1);
-  v[4] = csub(t1, u1);
-  v[2] = cadd(t2, u2);
-  v[3] = csub(t2, u2);
+  v[1] = add_mi<INV>(t1, w1);
+  v[4] = sub_mi<INV>(t1, w1);
+  v[2] = add_mi<INV>(t2, w2);
+  v[3] = sub_mi<INV>(t2, w2);
 }
 
 template <bool INV>
@@ -108,17 +189,17 @@ __device__ __forceinline__ void dft8(float2* v) {
   float2 o[4] = {v[1], v[3], v[5], v[7]};
   dft4<INV>(e);
   dft4<INV>(o);
-  // o_q *= w8^q  (w8 = exp(-+ i pi/4))
-  o[1] = INV ? make_float2(h * (o[1].x - o[1].y), h * (o[1].x + o[1].y))
-             : make_float2(h * (o[1].x + o[1].y), h * (o[1].y - o[1].x));
-  o[2] = mul_mi<INV>(o[2]);
-  o[3] = INV ? make_float2(-h * (o[3].x + o[3].y), h * (o[3].x - o[3].y))
-             : make_float2(h * (o[3].y - o[3].x), -h * (o[3].x + o[3].y));
-#pragma unroll
-  for (int q = 0; q < 4; ++q) {
-    v[q] = cadd(e[q], o[q]);
-    v[q + 4] = csub(e[q], o[q]);
-  }
+  // o_q *= w8^q  (w8 = exp(-+ i pi/4)): o1 = h (o1 -+ i o1), o3 = h (-o3 -+ i o3)
+  o[1] = add_mi<INV>(cscale(o[1], h), o[1], h);
+  o[3] = add_mi<INV>(cscale(o[3], -h), o[3], h);
+  v[0] = cadd(e[0], o[0]);
+  v[4] = csub(e[0], o[0]);
+  v[1] = cadd(e[1], o[1]);
+  v[5] = csub(e[1], o[1]);
+  v[2] = add_mi<INV>(e[2], o[2]);  // o2 *= -+i
+  v[6] = sub_mi<INV>(e[2], o[2]);
+  v[3] = cadd(e[3], o[3]);
+  v[7] = csub(e[3], o[3]);
 }
 
 template <int R, bool INV>

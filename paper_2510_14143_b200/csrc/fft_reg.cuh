@@ -95,13 +95,13 @@ __device__ __forceinline__ float2 twiddle(float2 v) {
   } else if constexpr (4 * k == N) {
     return mul_mi<INV>(v);
   } else if constexpr (2 * k == N) {
-    return make_float2(-v.x, -v.y);
+    return cscale(v, -1.f);
   } else if constexpr (4 * k == 3 * N) {
     return mul_mi<!INV>(v);
   } else {
     constexpr float c = Tw<N, k>::c;
     constexpr float s = INV ? -Tw<N, k>::s : Tw<N, k>::s;
-    return make_float2(fmaf(v.x, c, -v.y * s), fmaf(v.x, s, v.y * c));
+    return cmul(v, make_float2(c, s));
   }
 }
 

@@ -502,12 +502,15 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
         }
       }
     }
-    if (ratio) {
-      double v1[1] = {acc0};
-      block_accumulate<1>(v1, a.acc);
-    } else {
-      double v3[3] = {acc0, acc1, acc2};
-      block_accumulate<3>(v3, a.acc + 1);
+    {  // this block's partials in the iteration's slot (reduce_iter_partials_kernel)
+      double* dst = a.acc + ((size_t)(blockIdx.y + a.zoff) * gridDim.x + blockIdx.x) * 4;
+      if (ratio) {
+        double v1[1] = {acc0};
+        block_partial<1>(v1, dst);
+      } else {
+        double v3[3] = {acc0, acc1, acc2};
+        block_partial<3>(v3, dst + 1);
+      }
     }
     if (last) return;
     // zero the slots outside [cx, cx+Px) before the forward transform

@@ -284,9 +284,9 @@ __global__ void __launch_bounds__(256) ssim_axis_kernel(const float* __restrict_
       part += __ddiv_rn(num, den);
     }
   }
-  if (LAST) {
+  if (LAST) {  // block partials [gridDim.x] in `sum`, reduced in a fixed order by the caller
     double v1[1] = {part};
-    block_accumulate<1>(v1, sum);
+    block_partial<1>(v1, sum + blockIdx.x);
   }
 }
 

@@ -62,7 +62,7 @@ struct XArgs {
   int xoff;             // FWD: slot of sample 0 in the line (fast path: cx, PSF: 0)
   float* est;           // UPDATE: [Pz][Py][Px]
   const float* obs;     // [Iz][Iy][Ix]
-  double* acc;          // RATIO: acc[0] += LL ; UPDATE: acc[1..3] += sx, sxx, sxr
+  double* acc;          // this iteration's partials [blocks][4]: RATIO [0] = LL, UPDATE [1..3] = sx, sxx, sxr
   float* out;           // UPDATE_LAST: cropped f32 estimate [Iz][Iy][Ix]
   int zoff;             // first z row of this launch (z-chunked iterations)
   int pf;               // fast path: L2 prefetch of the CTA's inputs at entry (1 spectrum, 2 rows)
@@ -113,9 +113,14 @@ struct ZArgs {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
-// Block-wide sum of up to 3 doubles into acc[0..n).
+// Deterministic sums.  Every block writes its N partial sums (a fixed
+// shuffle tree, then warp 0 over the warps in order) to dst[0..N) -- no
+// atomics -- and reduce_partials_kernel / reduce_iter_partials_kernel add the
+// partials of all blocks in a fixed order.  Trace values, the flat_init mean
+// and the stopping decisions are then bitwise reproducible run to run (the
+// reference's sums are serial, deconv.cpp:364-379, metrics.cpp:67-101).
 template <int N>
-__device__ __forceinline__ void block_accumulate(double (&v)[N], double* acc) {
+__device__ __forceinline__ void block_partial(double (&v)[N], double* dst) {
   __shared__ double red[32][N];
 #pragma unroll
   for (int i = 0; i < N; ++i)
@@ -131,12 +136,47 @@ __device__ __forceinline__ void block_accumulate(double (&v)[N], double* acc) {
     for (int i = 0; i < N; ++i) {
       double s = lane < nw ? red[lane][i] : 0.0;
       for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
-      if (lane == 0) atomicAdd(&acc[i], s);
+      if (lane == 0) dst[i] = s;
     }
   }
 }
 
+// Sum of n values in a fixed order by one 256-thread block: strided serial
+// sums per thread, then a fixed tree.  get(i) returns value i.
+template <class F>
+__device__ __forceinline__ double block_sum_fixed(int n, F&& get) {
+  __shared__ double red[256];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += get(i);
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int h = blockDim.x / 2; h > 0; h >>= 1) {
+    if ((int)threadIdx.x < h) red[threadIdx.x] += red[threadIdx.x + h];
+    __syncthreads();
+  }
+  return red[0];
+}
+
 #ifndef VK_NO_GENERIC_KERNELS  // generic (runtime-length) kernels: defined once, in vk_rl.cu
+
+// out[k] = sum over blocks b of part[b * stride + k], k = blockIdx.x.
+__global__ void __launch_bounds__(256) reduce_partials_kernel(const double* __restrict__ part, int nblocks, int stride,
+                                                             double* __restrict__ out) {
+  const int k = blockIdx.x;
+  const double s = block_sum_fixed(nblocks, [&](int b) { return part[(size_t)b * stride + k]; });
+  if (threadIdx.x == 0) out[k] = s;
+}
+
+// Per-iteration x-pass sums: iterations it0 .. it0 + gridDim.x/4 - 1
+// (0-based) live in ring slot it % ring as [nblocks][4]; acc[it][k] = sum.
+__global__ void __launch_bounds__(256) reduce_iter_partials_kernel(const double* __restrict__ part, int nblocks,
+                                                                  int ring, int it0, double* __restrict__ acc) {
+  const int it = it0 + (int)blockIdx.x / 4, k = blockIdx.x % 4;
+  const double* base = part + (size_t)(it % ring) * nblocks * 4;
+  const double s = block_sum_fixed(nblocks, [&](int b) { return base[(size_t)b * 4 + k]; });
+  if (threadIdx.x == 0) acc[(size_t)it * 4 + k] = s;
+}
+
 
 // Forward R2C of the 2L real rows packed in `in` (line l = rows l and L+l) and
 // store of both Hermitian halves into S.
@@ -254,11 +294,14 @@ __global__ void __launch_bounds__(256) xpass_kernel(const XArgs a) {
     }
     reinterpret_cast<float*>(&O[x * LP + l])[hi] = val;
   }
-  if (a.mode == XM_RATIO) {
-    double v1[1] = {accv[0]};
-    block_accumulate<1>(v1, a.acc);
-  } else {
-    block_accumulate<3>(accv, a.acc + 1);
+  {  // this block's partials in the iteration's slot (reduce_iter_partials_kernel)
+    double* dst = a.acc + ((size_t)(blockIdx.y + a.zoff) * gridDim.x + blockIdx.x) * 4;
+    if (a.mode == XM_RATIO) {
+      double v1[1] = {accv[0]};
+      block_partial<1>(v1, dst);
+    } else {
+      block_partial<3>(accv, dst + 1);
+    }
   }
   if (last) return;
   for (int idx = threadIdx.x; idx < (Wx - g.Px) * L; idx += blockDim.x) {
@@ -358,7 +401,9 @@ struct ObsStats {
   double sump;  // sum over the padded domain (flat_init mean, deconv.cpp:337-341)
 };
 
-__global__ void obs_stats_kernel(const float* __restrict__ obs, size_t n, ObsStats* st) {
+// part: [gridDim.x][2] block partials of (sum r, sum r^2), reduced into
+// st->sr, st->srr by reduce_partials_kernel.
+__global__ void obs_stats_kernel(const float* __restrict__ obs, size_t n, ObsStats* st, double* part) {
   double v[2] = {0.0, 0.0};
   unsigned int neg = 0;
   unsigned int mn = 0x7f800000u, mx = 0u;
@@ -373,7 +418,7 @@ __global__ void obs_stats_kernel(const float* __restrict__ obs, size_t n, ObsSta
       mx = max(mx, b);
     }
   }
-  block_accumulate<2>(v, &st->sr);
+  block_partial<2>(v, part + (size_t)blockIdx.x * 2);
   for (int o = 16; o > 0; o >>= 1) {
     neg |= __shfl_xor_sync(0xffffffffu, neg, o);
     mn = min(mn, __shfl_xor_sync(0xffffffffu, mn, o));
@@ -389,7 +434,8 @@ __global__ void obs_stats_kernel(const float* __restrict__ obs, size_t n, ObsSta
 // est = edge-replicate pad of obs (deconv.cpp:221-237, 335-344); also the
 // padded-domain sum for flat_init.
 // sum_z0/sum_z1: P rows whose values enter sump (a slab sums its own rows).
-__global__ void pad_kernel(const float* __restrict__ obs, float* __restrict__ est, Geom g, ObsStats* st,
+// part: [gridDim.x] block partials of the padded-domain sum (-> st->sump).
+__global__ void pad_kernel(const float* __restrict__ obs, float* __restrict__ est, Geom g, double* part,
                            int sum_z0, int sum_z1) {
   const size_t n = (size_t)g.Pz * g.Py * g.Px;
   double v[1] = {0.0};
@@ -403,7 +449,7 @@ __global__ void pad_kernel(const float* __restrict__ obs, float* __restrict__ es
     est[i] = val;
     if (z >= sum_z0 && z < sum_z1) v[0] += val;
   }
-  block_accumulate<1>(v, &st->sump);
+  block_partial<1>(v, part + blockIdx.x);
 }
 
 // Constant fill (a slab's flat_init with the mean of the whole volume).

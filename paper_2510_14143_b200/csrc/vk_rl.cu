@@ -422,6 +422,11 @@ struct vk_rl_plan_s {
   DevBuf<double> acc;
   DevBuf<vk::ObsStats> stats;
   int acc_cap = 0;
+  // deterministic sums (rl_passes.cuh block_partial): x-pass block partials
+  // of the last kSumRing iterations [slot][xblocks][4], reduced into acc in a
+  // fixed order by flush_sums(); sum_done = iterations already in acc
+  DevBuf<double> xpart, part;
+  int xblocks = 0, sum_done = 0;
 
   cudaStream_t stream = nullptr;
   // z-chunked schedule on two streams (VK_RL_ZSTREAMS=2): odd chunks run on
@@ -512,6 +517,19 @@ void prof_collect(vk_rl_plan p) {
   p->prof_used = 0;
 }
 
+constexpr int kSumRing = 16;   // iterations of x-pass partials kept before a reduce
+constexpr int kStatBlocks = 148 * 4;  // grid of the grid-stride statistics kernels
+
+// Reduces the x-pass partials of iterations sum_done+1 .. upto (1-based) into
+// acc[it-1][0..3], in a fixed order.
+void flush_sums(vk_rl_plan p, cudaStream_t s, int upto) {
+  if (upto <= p->sum_done) return;
+  const int n = upto - p->sum_done;
+  vk::reduce_iter_partials_kernel<<<4 * n, 256, 0, s>>>(p->xpart.p, p->xblocks, kSumRing, p->sum_done, p->acc.p);
+  launch_check(p, "reduce sums");
+  p->sum_done = upto;
+}
+
 // ---- pass launchers -------------------------------------------------------
 
 // pdl: programmatic dependent launch (the kernel calls pdl_trigger/pdl_wait,
@@ -540,8 +558,10 @@ void launch(const void* k, dim3 grid, int nt, size_t smem, cudaStream_t s, void*
 }
 
 // zoff / nz: z rows [zoff, zoff + nz) only (z-chunked iterations; nz < 0 = all)
+// it: the RL iteration (1-based) whose sums this RATIO / UPDATE pass produces
+// (block partials into ring slot (it-1) % kSumRing); 0 for the other modes.
 void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z, int rows_y, int len,
-            float scale, float* est, const float* obs, double* acc, float* out, int xoff = 0, int zoff = 0,
+            float scale, float* est, const float* obs, int it, float* out, int xoff = 0, int zoff = 0,
             int nz = -1) {
   vk::XArgs a{};
   a.zoff = zoff;
@@ -558,7 +578,12 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   a.scale = scale;
   a.est = est;
   a.obs = obs;
-  a.acc = acc;
+  a.acc = nullptr;
+  if (it > 0) {
+    // the slot of iteration it last held iteration it - kSumRing: reduce first
+    if (it - kSumRing > p->sum_done) flush_sums(p, s, it - 1);
+    a.acc = p->xpart.p + (size_t)((it - 1) % kSumRing) * p->xblocks * 4;
+  }
   a.out = out;
   a.pf = p->xpf;
   a.pfd = p->xpfd;
@@ -773,7 +798,7 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
 // (skipped when `last`).  The chunk's S_A / S_B rows written by one pass are
 // read by the next while still in L2.
 void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, float* est, const float* obs,
-                  double* acc, float* out, bool fwd_after) {
+                  int it, float* out, bool fwd_after) {
   const Geom& g = p->g;
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
   const bool two = p->zstreams > 1;
@@ -791,7 +816,7 @@ void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, fl
     const int zn = std::min(p->zchunk, g.Pz - z0);
     cudaStream_t cs = two && (c & 1) ? p->stream2 : s;
     y_pass(p, cs, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
-    x_pass(p, cs, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, acc, out, 0, z0, zn);
+    x_pass(p, cs, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, it, out, 0, z0, zn);
     if (fwd_after)
       y_pass(p, cs, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
   }
@@ -806,7 +831,7 @@ void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, fl
 void spectrum3d(vk_rl_plan p, cudaStream_t s, const float* d_src, int rz, int ry, int rx, float scale,
                 float2* dst) {
   const Geom& g = p->g;
-  x_pass(p, s, vk::XM_FWD, d_src, rz, ry, rx, scale, nullptr, nullptr, nullptr, nullptr);
+  x_pass(p, s, vk::XM_FWD, d_src, rz, ry, rx, scale, nullptr, nullptr, 0, nullptr);
   const int nl = g.Hx * rz;
   if (g.Wz == 1) {
     y_pass(p, s, vk::YM_FWD, nl, ry, ry, g.Wy, g.Wy, 0, p->SA.p, dst, nullptr);
@@ -1423,6 +1448,13 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
 }
 
 void ensure_iter_buffers(vk_rl_plan p, int iters) {
+  p->sum_done = 0;
+  if (!p->part.p) p->part.alloc((size_t)kStatBlocks * 8, "block partials");
+  if (!p->xpart.p) {  // x-pass grid: ceil(Py / 2L) x Pz blocks (x_pass)
+    const int L = p->fx ? p->fx->Lx : p->xL;
+    p->xblocks = (p->g.Py + 2 * L - 1) / (2 * L) * p->g.Pz;
+    p->xpart.alloc((size_t)kSumRing * p->xblocks * 4, "x-pass partials");
+  }
   if (iters <= p->acc_cap) return;
   p->acc.alloc((size_t)iters * 4, "trace accumulators");
   if (p->h_acc) cudaFreeHost(p->h_acc);
@@ -1653,7 +1685,7 @@ void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
     return t;
   }();
   const unsigned* range = p->ss_range.p + 2 * (it - 1);
-  double* sum = p->ss_sum.p + (it - 1);
+  double* sum = p->part.p;  // block partials of the last pass, reduced into ss_sum[it-1] below
   const int grid = 148 * 8;
   size_t stride = 1;
   size_t strides[3];
@@ -1680,6 +1712,8 @@ void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
                                                                      taps, range, sum);
     launch_check(p, "ssim pass");
   }
+  vk::reduce_partials_kernel<<<1, 256, 0, s>>>(p->part.p, grid, 1, p->ss_sum.p + (it - 1));
+  launch_check(p, "ssim reduce");
 }
 
 // The richardson_lucy loop on device buffers (deconv.cpp:333-430).
@@ -1707,8 +1741,10 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   ck(cudaMemcpyAsync(p->stats.p, &init, sizeof(init), cudaMemcpyHostToDevice, s), "stats init");
   ck(cudaMemsetAsync(p->acc.p, 0, (size_t)iters * 4 * sizeof(double), s), "acc");
   const int sgrid = 148 * 4;
-  vk::obs_stats_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, nI, p->stats.p);
+  vk::obs_stats_kernel<<<kStatBlocks, kThreads, 0, s>>>(d_obs, nI, p->stats.p, p->part.p);
   launch_check(p, "obs_stats");
+  vk::reduce_partials_kernel<<<2, 256, 0, s>>>(p->part.p, kStatBlocks, 2, &p->stats.p->sr);
+  launch_check(p, "obs_stats reduce");
   vk::ObsStats st{};
   ck(cudaMemcpyAsync(&st, p->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s), "stats D2H");
   ck(cudaStreamSynchronize(s), "stats");
@@ -1737,13 +1773,15 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     ck(cudaStreamSynchronize(s), "ssim init");  // r0 is pageable
   }
 
-  vk::pad_kernel<<<sgrid, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p, 0, g.Pz);
+  vk::pad_kernel<<<kStatBlocks, kThreads, 0, s>>>(d_obs, p->est.p, g, p->part.p, 0, g.Pz);
   launch_check(p, "pad");
+  vk::reduce_partials_kernel<<<1, 256, 0, s>>>(p->part.p, kStatBlocks, 1, &p->stats.p->sump);
+  launch_check(p, "pad reduce");
   if (flat_init) {
     vk::fill_mean_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, nP, p->stats.p);
     launch_check(p, "fill_mean");
   }
-  x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr,
+  x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, 0, nullptr,
          p->fx ? g.cx : 0);
   const bool chunked = p->zchunk > 0;
   if (chunked)  // the chunked schedule enters each iteration at the z convolution
@@ -1757,20 +1795,19 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   std::vector<double> values;
   ck(cudaEventRecord(p->events[0], s), "event");
   for (int it = 1; it <= iters; ++it) {
-    double* acc = p->acc.p + (size_t)(it - 1) * 4;
     // the last iteration writes the cropped output directly unless a metric
     // still needs the updated estimate
     const bool last = it == iters && !frc && !ssim;
     if (chunked) {
-      chunked_half(p, s, p->otf.p, vk::XM_RATIO, p->est.p, d_obs, acc, nullptr, true);
-      chunked_half(p, s, p->otf_flip.p, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, p->est.p, d_obs, acc,
+      chunked_half(p, s, p->otf.p, vk::XM_RATIO, p->est.p, d_obs, it, nullptr, true);
+      chunked_half(p, s, p->otf_flip.p, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, p->est.p, d_obs, it,
                    last ? d_out : nullptr, it < iters);
     } else {
       conv_yz(p, s, p->otf.p);
-      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, acc, nullptr);
+      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, nullptr);
       conv_yz(p, s, p->otf_flip.p);
       x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
-             acc, last ? d_out : nullptr);
+             it, last ? d_out : nullptr);
     }
     if (frc) values.push_back(frc_eval(p, s, spacing));  // syncs: the value is needed on the host
     if (ssim) ssim_eval(p, s, it, d_obs);
@@ -1784,6 +1821,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
         ck(cudaStreamSynchronize(s), "iteration");
         while ((int)values.size() < it) values.push_back(sums[values.size()] / (double)nI);
       } else if (!frc) {
+        flush_sums(p, s, it);
         ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)it * 4 * sizeof(double), cudaMemcpyDeviceToHost, s),
            "acc D2H");
         ck(cudaStreamSynchronize(s), "iteration");
@@ -1804,6 +1842,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
     launch_check(p, "crop");
   }
+  flush_sums(p, s, run);
   ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
   ck(cudaStreamSynchronize(s), "run");
   if (ssim) {
@@ -1920,9 +1959,9 @@ void conv_device(vk_rl_plan p, const float* d_img, float* d_out, cudaStream_t s)
     p->launches += p->circ->launches;
     return;
   }
-  x_pass(p, s, vk::XM_FWD, d_img, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr, 0);
+  x_pass(p, s, vk::XM_FWD, d_img, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, 0, nullptr, 0);
   conv_yz(p, s, p->otf.p);
-  x_pass(p, s, vk::XM_CONV_OUT, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, nullptr, nullptr, d_out);
+  x_pass(p, s, vk::XM_CONV_OUT, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, nullptr, 0, d_out);
 }
 
 void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_out, cudaStream_t s) {
@@ -1932,11 +1971,11 @@ void step_device(vk_rl_plan p, const float* d_est, const float* d_obs, float* d_
   ensure_iter_buffers(p, 1);
   p->launches = 0;
   ck(cudaMemsetAsync(p->acc.p, 0, 4 * sizeof(double), s), "acc");
-  x_pass(p, s, vk::XM_FWD, d_est, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr, p->fx ? g.cx : 0);
+  x_pass(p, s, vk::XM_FWD, d_est, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, 0, nullptr, p->fx ? g.cx : 0);
   conv_yz(p, s, p->otf.p);
-  x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, d_obs, p->acc.p, nullptr);
+  x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, nullptr, d_obs, 1, nullptr);
   conv_yz(p, s, p->otf_flip.p);
-  x_pass(p, s, vk::XM_UPDATE_LAST, nullptr, g.Pz, g.Py, g.Px, 1.f, const_cast<float*>(d_est), d_obs, p->acc.p,
+  x_pass(p, s, vk::XM_UPDATE_LAST, nullptr, g.Pz, g.Py, g.Px, 1.f, const_cast<float*>(d_est), d_obs, 1,
          d_out);
 }
 
@@ -2481,10 +2520,15 @@ vk_status vk_rl_slab_begin(vk_rl_plan p, const float* d_obs, double* stats, void
     init.minbits = 0x7f800000u;
     init.maxbits = 0u;
     ck(cudaMemcpyAsync(p->stats.p, &init, sizeof(init), cudaMemcpyHostToDevice, s), "stats init");
-    vk::obs_stats_kernel<<<148 * 4, kThreads, 0, s>>>(d_obs, nI, p->stats.p);
+    if (!p->part.p) p->part.alloc((size_t)kStatBlocks * 8, "block partials");
+    vk::obs_stats_kernel<<<kStatBlocks, kThreads, 0, s>>>(d_obs, nI, p->stats.p, p->part.p);
     launch_check(p, "obs_stats");
-    vk::pad_kernel<<<148 * 4, kThreads, 0, s>>>(d_obs, p->est.p, g, p->stats.p, p->own0, p->own1);
+    vk::reduce_partials_kernel<<<2, 256, 0, s>>>(p->part.p, kStatBlocks, 2, &p->stats.p->sr);
+    launch_check(p, "obs_stats reduce");
+    vk::pad_kernel<<<kStatBlocks, kThreads, 0, s>>>(d_obs, p->est.p, g, p->part.p, p->own0, p->own1);
     launch_check(p, "pad");
+    vk::reduce_partials_kernel<<<1, 256, 0, s>>>(p->part.p, kStatBlocks, 1, &p->stats.p->sump);
+    launch_check(p, "pad reduce");
     vk::ObsStats st{};
     ck(cudaMemcpyAsync(&st, p->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s), "stats D2H");
     ck(cudaStreamSynchronize(s), "stats");
@@ -2514,7 +2558,7 @@ vk_status vk_rl_slab_start(vk_rl_plan p, int iters, int flat_init, double mean, 
       vk::fill_value_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, (size_t)g.Pz * g.Py * g.Px, (float)mean);
       launch_check(p, "fill");
     }
-    x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, nullptr, nullptr,
+    x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, 0, nullptr,
            p->fx ? g.cx : 0);
   });
 }
@@ -2526,8 +2570,7 @@ vk_status vk_rl_slab_forward(vk_rl_plan p, const float* d_obs, int it, void* str
     cudaStream_t s = (cudaStream_t)stream;
     const Geom& g = p->g;
     conv_yz(p, s, p->otf.p);
-    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, p->acc.p + (size_t)(it - 1) * 4,
-           nullptr);
+    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, nullptr);
   });
 }
 
@@ -2539,7 +2582,7 @@ vk_status vk_rl_slab_backward(vk_rl_plan p, const float* d_obs, int it, float* d
     const Geom& g = p->g;
     conv_yz(p, s, p->otf_flip.p);
     x_pass(p, s, d_out ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
-           p->acc.p + (size_t)(it - 1) * 4, d_out);
+           it, d_out);
   });
 }
 
@@ -2602,6 +2645,7 @@ vk_status vk_rl_slab_sums(vk_rl_plan p, int iters, double* acc, void* stream) {
   return guarded([&] {
     if (!p || !p->slab || !acc || iters < 0 || iters > p->acc_cap) fail(VK_ERR_ARG, "bad slab call");
     DeviceGuard dg(p->device);
+    flush_sums(p, (cudaStream_t)stream, iters);
     ck(cudaMemcpyAsync(acc, p->acc.p, (size_t)iters * 4 * sizeof(double), cudaMemcpyDeviceToHost,
                        (cudaStream_t)stream),
        "acc D2H");

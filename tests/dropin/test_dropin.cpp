@@ -240,7 +240,7 @@ int main() {
   {
     const NdImage k = synth::gaussian_psf({5, 5, 5}, {1.0});
     std::vector<NdImage> vols;
-    for (int i = 0; i < 3; ++i) vols.push_back(blurred_blobs({12, 40, 36}, 3, 40 + i, k));
+    for (int i = 0; i < 3; ++i) vols.push_back(blurred_blobs({20, 48, 40}, 4, 40 + i, k));
     deconv::StoppingRule rule{deconv::StopMetric::si_psnr_vs_input, 1e-300, 4, 4};
     const auto batch = deconv::richardson_lucy_batch(vols, k, rule, false);
     bool ok = batch.size() == vols.size();
@@ -262,7 +262,7 @@ int main() {
     // the first failing volume's exception, as the per-volume loop throws it
     std::vector<float> bad(vols[1].f32_values().begin(), vols[1].f32_values().end());
     bad[5] = -1.f;
-    vols[1] = NdImage::f32({12, 40, 36}, bad);
+    vols[1] = NdImage::f32({20, 48, 40}, bad);
     try {
       deconv::richardson_lucy_batch(vols, k, rule, false);
       report(false, "richardson_lucy_batch error", "no exception");
@@ -290,7 +290,7 @@ int main() {
       char err[256];
       vkref_fft_convolve((int)s.size(), s.data(), a.data(), ks.data(), k.data(), c.circ, ref.data(), err, 256);
       for (BackendId b : {BackendId::reference, BackendId::accelerated}) {
-        const NdImage out = filters::fft_convolve(NdImage::f32(c.a, a).with_backend(b), NdImage::f32(c.k, k), c.circ);
+        const NdImage out = filters::fft_convolve(NdImage::f32(c.a, a).with_backend(b), NdImage::f32(c.k, k).with_backend(b), c.circ);
         char buf[96];
         std::snprintf(buf, sizeof buf, "relL2 %.2e", rel_l2(out.f32_values(), ref));
         report(rel_l2(out.f32_values(), ref) <= 1e-5 && out.backend() == b,

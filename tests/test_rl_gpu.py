@@ -448,9 +448,9 @@ def test_batch_device_lanes_match_single_runs(lanes):
         torch.cuda.synchronize()
         for sgl, o, tr in zip(single, d_out, trs):
             assert np.array_equal(o.cpu().numpy(), sgl.estimate)
-            # the metric sums use FP64 atomics: order-dependent in the last bits
-            np.testing.assert_allclose([r.value for r in tr.records], [r.value for r in sgl.trace.records],
-                                       rtol=1e-12)
+            # block partials reduced in a fixed order: bitwise identical traces
+            assert [r.value for r in tr.records] == [r.value for r in sgl.trace.records]
+            assert list(tr.log_likelihood) == list(sgl.trace.log_likelihood)
         assert plan.lanes() == (int(lanes) if lanes else 3)  # 2D default
         assert plan.launches() > 7 * 5 * 4  # every lane's launches are counted
         host = plan.run_batch(vols, rule)  # the host batch uses the lanes too
@@ -465,6 +465,21 @@ def test_batch_device_lanes_match_single_runs(lanes):
         os.environ.pop("VK_RL_LANES", None)
         if old is not None:
             os.environ["VK_RL_LANES"] = old
+
+
+@pytest.mark.parametrize("metric", ["si_psnr_vs_input", "ssim_vs_prev"])
+def test_sums_are_deterministic(metric):
+    """Trace sums and the flat_init mean use block partials reduced in a fixed
+    order (no FP64 atomics): repeated runs agree bitwise, so a stop decision
+    can never flip between runs (VERDICT r1 weak #10)."""
+    psf = O.gaussian_psf((7, 7, 7), 1.2)
+    obs = synth.blurred(synth.blobs((30, 96, 80), 12, 4, 7, seed=13), psf)
+    rule = vk.StoppingRule(metric, 1e-300, 20, 20)
+    runs = [vk.richardson_lucy(obs, psf, rule, flat_init=True) for _ in range(3)]
+    for r in runs[1:]:
+        assert np.array_equal(r.estimate, runs[0].estimate)
+        assert [x.value for x in r.trace.records] == [x.value for x in runs[0].trace.records]
+        assert list(r.trace.log_likelihood) == list(runs[0].trace.log_likelihood)
 
 
 def test_plan_reuse_batch_and_device_api():
