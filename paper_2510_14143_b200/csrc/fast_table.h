@@ -20,6 +20,12 @@ struct alignas(64) ZTmaArgs {
   // factored OTF of a separable PSF: fx[Hx], fy[Wy], fz[Wz] back to back,
   // O(kx, kz, ky) = (fx[kx] * fy[ky]) * fz[kz]; nullptr: read the OTF
   const float2* ofac;
+  // ky-even OTF stored as columns 0..Wy/2 only (vk_rl.cu halve_otfs): tiles
+  // above Wy/2 read the mirrored columns Wy-ky, reversed within the box
+  int otf_half;
+  // kx-chunked convolution: S is a ring slot holding kx planes [kx0, kx0 +
+  // gridDim.y); the OTF / factor index is kx0 + blockIdx.y
+  int kx0;
 };
 
 // Kernel argument of xpass_tma: the S_A tensor map {Py, Pz, Hx}, box
@@ -48,6 +54,7 @@ struct FastEntry {
   const void* zpk;      // zpass_pipe<R1,R2,Lz>(ZArgs): persistent, double-buffered
   const void* ztk;      // zpass_tma<R1,R2>(ZTmaArgs): TMA-staged column tile (Lz = 16), or nullptr
   size_t smem_zt;
+  size_t smem_zt_half;  // zpass_tma with a half OTF (wider OTF tile)
   const void* ytk;      // ypass_tma<R1,R2,Ly>(YArgs): bulk-copied lines (FWD/INV), or nullptr
   size_t smem_yt;
 };

@@ -726,6 +726,17 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT, MINB == 1 ? 0 : 
 // copy flies.  The OTF is read from global in the multiply.
 // (ZTmaArgs: fast_table.h)
 
+// First stored column of the half-OTF box serving tile [ky0, ky0+16): the
+// smallest min(ky, Wy - ky) of its columns (they span <= 16 columns), rounded
+// down to even -- a TMA box must start 16-byte aligned in its inner
+// dimension -- so the half box is kHalfBox = 18 columns wide.  A negative
+// start reads zeros out of bounds (lanes with ky >= Wy).
+constexpr int kHalfBox = 18;
+__device__ __forceinline__ int half_box_start(int ky0, int Wy) {
+  const int s = ky0 + 15 <= Wy / 2 ? ky0 : min(ky0, Wy - ky0 - 15);
+  return s & ~1;
+}
+
 template <int R1, int R2, bool TWG, int MINB>
 __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 : MINB)
     zpass_tma(const __grid_constant__ ZTmaArgs ta) {
@@ -742,10 +753,11 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   extern __shared__ __align__(128) float2 smem[];
   float2* tw = TWG ? nullptr : smem;
   float2* A = TWG ? smem : smem + N;  // dense [z][16]; N*16*8 B, 128-B aligned (N multiple of 8)
-  float2* O = A + N * L;              // OTF tile [kz][16] when ta.otf_tma
+  float2* O = A + N * L;              // OTF tile [kz][16] (half OTF: [kz][kHalfBox]) when ta.otf_tma
   __shared__ uint64_t bar, obar;
   const bool otma = ta.otf_tma != 0;
   const int kx = blockIdx.y, ky0 = blockIdx.x * L;
+  const int kxo = kx + ta.kx0;  // absolute kx plane (OTF, factors)
   const int l = threadIdx.x & (L - 1), z0 = threadIdx.x / L;
   const int ky = ky0 + l;
   const unsigned Wy = ta.z.Wy;
@@ -764,8 +776,8 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
     mbar_expect_tx(&bar, (unsigned)(n_in * L * sizeof(float2)));
     tma_load_3d(A, &ta.map, &bar, ky0, 0, kx);
     if (otma) {  // the OTF tile lands while the forward transform runs
-      mbar_expect_tx(&obar, (unsigned)(N * L * sizeof(float2)));
-      tma_load_3d(O, &ta.omap, &obar, ky0, 0, kx);
+      mbar_expect_tx(&obar, (unsigned)(N * (ta.otf_half ? kHalfBox : L) * sizeof(float2)));
+      tma_load_3d(O, &ta.omap, &obar, ta.otf_half ? half_box_start(ky0, (int)Wy) : ky0, 0, kxo);
     }
   }
 #pragma unroll
@@ -776,10 +788,10 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   mbar_wait(&bar, 0);
   __syncthreads();
   reg::fft2<R1, R2, L, NT, false, L, TWG>(A, twp);
-  const float2* og = otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
+  const float2* og = otf + ((unsigned)kxo * N * Wy + (kok ? ky : 0));
   if (ta.ofac) {  // separable PSF: rebuild the OTF column from its 1D factors
     const float2* fz = ta.ofac + ta.z.hx + Wy;
-    const float2 c = kok ? cmul(__ldg(ta.ofac + kx), __ldg(ta.ofac + ta.z.hx + ky)) : make_float2(0.f, 0.f);
+    const float2 c = kok ? cmul(__ldg(ta.ofac + kxo), __ldg(ta.ofac + ta.z.hx + ky)) : make_float2(0.f, 0.f);
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
       const int z = z0 + k * ZS;
@@ -787,10 +799,13 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
     }
   } else if (otma) {
     mbar_wait(&obar, 0);
+    // half OTF: column ky lives at m = min(ky, Wy - ky), box slot m - start
+    const int ol = ta.otf_half ? (ky <= (int)Wy / 2 ? ky : (int)Wy - ky) - half_box_start(ky0, (int)Wy) : l;
+    const int op = ta.otf_half ? kHalfBox : L;  // OTF tile pitch
 #pragma unroll
     for (int k = 0; k < IT; ++k) {
       const int z = z0 + k * ZS;
-      if (z < N) A[z * L + l] = cmul(A[z * L + l], O[z * L + l]);
+      if (z < N) A[z * L + l] = cmul(A[z * L + l], O[z * op + ol]);
     }
   } else {
 #pragma unroll

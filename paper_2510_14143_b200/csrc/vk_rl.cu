@@ -9,6 +9,7 @@
 //   si_psnr ............................. src/metrics.cpp:67-101
 //   good_size ........................... src/fft_plan.cpp:41-49
 #include <cuda_runtime.h>
+#include <unistd.h>  // environ
 
 #include <algorithm>
 #include <atomic>
@@ -388,6 +389,15 @@ struct vk_rl_plan_s {
   int xtbk = 0, xtnb = 0;  // crop offset of the y inverse: g.cy, or 0 when folded into the OTFs as a ramp
   bool tma_store = true;  // TMA/bulk stores of the z tile and y-forward lines (VK_RL_NO_TMA_STORE=1: thread stores)  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
   CUtensorMap zmap{}, omap{}, omap_flip{};
+  // kx-chunked y/z convolution (conv_yz_chunked): chunks of kxc planes run
+  // y-forward -> z -> y-inverse through a ring slot (one per stream) small
+  // enough to stay L2-resident, so S_B does not make HBM round trips
+  int kxc = 0, kxs = 2;  // planes per chunk, streams (= ring slots)
+  size_t ring_window = 0;  // bytes of ring2 under a persisting L2 access window (0: none)
+  DevBuf<float2> ring2;
+  CUtensorMap zmap_ring[4]{};
+  cudaStream_t kstream[4]{};  // kstream[0] unused (the run's stream)
+  cudaEvent_t kev[4]{};
   // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
   const vk::ClEntry* cl = nullptr;
   int cl_clusters = 0;
@@ -418,6 +428,10 @@ struct vk_rl_plan_s {
   DevBuf<float2> SA, SB, otf, otf_flip;
   DevBuf<float2> ofac;  // 1D factors of otf and otf_flip when both are separable (ZTmaArgs::ofac)
   bool ofactored = false;
+  // ky-mirror-symmetric OTFs (halve_otfs): only columns ky <= Wy/2 stored,
+  // [Hx][Wz][owp] with owp = Wy/2+1 rounded up to even (16-byte TMA pitch)
+  bool ohalf = false;
+  int owp = 0;
   DevBuf<float> est, obs, out;
   DevBuf<double> acc;
   DevBuf<vk::ObsStats> stats;
@@ -444,9 +458,16 @@ struct vk_rl_plan_s {
   bool prof = false;
   std::vector<cudaEvent_t> prof_pool;
   size_t prof_used = 0;
-  std::vector<std::pair<int, size_t>> prof_pending;  // (kind, index of begin event)
+  struct ProfRec {
+    int kind;
+    size_t ev;           // index of the begin event
+    double bytes, otf;   // algorithmic and OTF bytes of this launch
+  };
+  std::vector<ProfRec> prof_pending;
   double prof_ms[VK_KIND_COUNT]{};
   uint64_t prof_n[VK_KIND_COUNT]{};
+  double prof_bytes[VK_KIND_COUNT]{}, prof_otf[VK_KIND_COUNT]{};
+  double prof_last_otf[VK_KIND_COUNT]{};  // OTF bytes per launch of the last profile read (-1: none)
 
   // Batch lanes: clones of this plan (own buffers and stream) that run
   // independent volumes concurrently, one host thread each (lane 0 = this).
@@ -463,6 +484,10 @@ struct vk_rl_plan_s {
     if (ev_fork) cudaEventDestroy(ev_fork);
     if (ev_join) cudaEventDestroy(ev_join);
     if (h_frc) cudaFreeHost(h_frc);
+    for (int i = 0; i < 4; ++i) {
+      if (kstream[i]) cudaStreamDestroy(kstream[i]);
+      if (kev[i]) cudaEventDestroy(kev[i]);
+    }
     delete frc;
     delete circ;
   }
@@ -500,18 +525,28 @@ size_t prof_begin(vk_rl_plan p, cudaStream_t s) {
   ck(cudaEventRecord(p->prof_pool[i], s), "event");
   return i;
 }
-void prof_end(vk_rl_plan p, cudaStream_t s, int kind, size_t i) {
+uint64_t alg_bytes(vk_rl_plan p, int kind);
+uint64_t otf_bytes(vk_rl_plan p, int kind);
+
+// bytes < 0: the kind's whole-volume launch (alg_bytes / otf_bytes); chunked
+// launches pass their own (otf as the fraction of the OTF planes they read).
+void prof_end(vk_rl_plan p, cudaStream_t s, int kind, size_t i, double bytes = -1.0, double otf_frac = 1.0) {
   if (!p->prof) return;
   ck(cudaEventRecord(p->prof_pool[i + 1], s), "event");
-  p->prof_pending.emplace_back(kind, i);
+  p->prof_pending.push_back({kind, i, bytes < 0 ? (double)alg_bytes(p, kind) : bytes,
+                             otf_frac * (double)otf_bytes(p, kind)});
 }
 void prof_collect(vk_rl_plan p) {
-  for (auto& [kind, i] : p->prof_pending) {
+  for (const auto& r : p->prof_pending) {
+    const int kind = r.kind;
+    const size_t i = r.ev;
     ck(cudaEventSynchronize(p->prof_pool[i + 1]), "event sync");
     float ms = 0;
     ck(cudaEventElapsedTime(&ms, p->prof_pool[i], p->prof_pool[i + 1]), "elapsed");
     p->prof_ms[kind] += ms;
     p->prof_n[kind] += 1;
+    p->prof_bytes[kind] += r.bytes;
+    p->prof_otf[kind] += r.otf;
   }
   p->prof_pending.clear();
   p->prof_used = 0;
@@ -648,7 +683,7 @@ void y_pass(vk_rl_plan p, cudaStream_t s, int mode, int nlines, int n_in, int in
   else
     vk::ypass_kernel<<<grid, kThreads, p->ys, s>>>(a);
   launch_check(p, "ypass");
-  prof_end(p, s, kind, t);
+  prof_end(p, s, kind, t, 8.0 * nlines * (n_in + n_out));
 }
 
 void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_out, int out_off,
@@ -678,9 +713,10 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
       if (ta.ofac) ta.otf_tma = 0;
     }
     if (ta.otf_tma) ta.omap = otf == p->otf.p ? p->omap : p->omap_flip;
+    ta.otf_half = ta.otf_tma && p->ohalf;
     dim3 grid((p->g.Wy + 15) / 16, p->g.Hx);
     const size_t t = prof_begin(p, s);
-    launch(p->fz->ztk, grid, p->fz->NTz, p->fz->smem_zt, s, &ta, p->fz->pdl);
+    launch(p->fz->ztk, grid, p->fz->NTz, ta.otf_half ? p->fz->smem_zt_half : p->fz->smem_zt, s, &ta, p->fz->pdl);
     launch_check(p, "zpass tma");
     prof_end(p, s, VK_KIND_Z_CONV, t);
     return;
@@ -700,6 +736,81 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
     vk::zpass_kernel<<<grid, kThreads, p->zs, s>>>(a);
   launch_check(p, "zpass");
   prof_end(p, s, VK_KIND_Z_CONV, t);
+}
+
+// z convolution of kx planes [kx0, kx0 + nk) held in ring slot `slot`.
+void z_pass_chunk(vk_rl_plan p, cudaStream_t s, const float2* otf, int kx0, int nk, int slot) {
+  vk::ZTmaArgs ta{};
+  ta.map = p->zmap_ring[slot];
+  ta.z.plan = p->lpz;
+  ta.z.mode = vk::ZM_CONV;
+  ta.z.L = 16;
+  ta.z.Wy = p->g.Wy;
+  ta.z.zrows = p->g.Pz;
+  ta.z.n_in = p->g.Pz;
+  ta.z.n_out = p->g.Pz;
+  ta.z.out_off = p->g.cz;
+  ta.z.S = p->ring2.p + (size_t)slot * p->kxc * p->g.Pz * p->g.Wy;
+  ta.z.otf = otf;
+  ta.z.hx = p->g.Hx;
+  ta.kx0 = kx0;
+  ta.otf_tma = p->otma && (otf == p->otf.p || otf == p->otf_flip.p);
+  ta.tma_store = 1;
+  if (p->ofactored) {
+    const size_t nf = (size_t)p->g.Hx + p->g.Wy + p->g.Wz;
+    ta.ofac = otf == p->otf.p ? p->ofac.p : otf == p->otf_flip.p ? p->ofac.p + nf : nullptr;
+    if (ta.ofac) ta.otf_tma = 0;
+  }
+  if (ta.otf_tma) ta.omap = otf == p->otf.p ? p->omap : p->omap_flip;
+  ta.otf_half = ta.otf_tma && p->ohalf;
+  const size_t t = prof_begin(p, s);
+  launch(p->fz->ztk, dim3((p->g.Wy + 15) / 16, nk), p->fz->NTz, ta.otf_half ? p->fz->smem_zt_half : p->fz->smem_zt, s,
+         &ta, p->fz->pdl);
+  launch_check(p, "zpass chunk");
+  prof_end(p, s, VK_KIND_Z_CONV, t, 16.0 * nk * p->g.Pz * p->g.Wy, (double)nk / p->g.Hx);
+}
+
+// The y/z convolution in chunks of kxc kx planes: y-forward -> z -> y-inverse
+// per chunk through an L2-sized ring slot, even chunks on `s`, odd ones on
+// stream2 (forked here, joined at the end), so one chunk's passes overlap the
+// other's and the GPU stays full while each chunk's S_B stays in L2.
+void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
+  const Geom& g = p->g;
+  const int ns = p->kxs;
+  if (!p->kev[0]) {
+    for (int i = 0; i < ns; ++i) {
+      if (i) ck(cudaStreamCreateWithFlags(&p->kstream[i], cudaStreamNonBlocking), "cudaStreamCreate");
+      ck(cudaEventCreateWithFlags(&p->kev[i], cudaEventDisableTiming), "event");
+    }
+    if (p->ring_window) {  // keep the ring L2-resident (persisting access window)
+      cudaStreamAttrValue v{};
+      v.accessPolicyWindow.base_ptr = p->ring2.p;
+      v.accessPolicyWindow.num_bytes = p->ring_window;
+      v.accessPolicyWindow.hitRatio = 1.0f;
+      v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      for (int i = 1; i < ns; ++i) cudaStreamSetAttribute(p->kstream[i], cudaStreamAttributeAccessPolicyWindow, &v);
+      cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
+      cudaGetLastError();
+    }
+  }
+  ck(cudaEventRecord(p->kev[0], s), "event");
+  for (int i = 1; i < ns; ++i) ck(cudaStreamWaitEvent(p->kstream[i], p->kev[0], 0), "wait");
+  const size_t plane_a = (size_t)g.Pz * g.Py, slot_b = (size_t)p->kxc * g.Pz * g.Wy;
+  int c = 0;
+  for (int kx0 = 0; kx0 < g.Hx; kx0 += p->kxc, ++c) {
+    const int nk = std::min(p->kxc, g.Hx - kx0), slot = c % ns;
+    cudaStream_t cs = slot ? p->kstream[slot] : s;
+    float2* sa = p->SA.p + (size_t)kx0 * plane_a;
+    float2* sb = p->ring2.p + (size_t)slot * slot_b;
+    y_pass(p, cs, vk::YM_FWD, nk * g.Pz, g.Py, g.Py, g.Wy, g.Wy, 0, sa, sb, nullptr);
+    z_pass_chunk(p, cs, otf, kx0, nk, slot);
+    y_pass(p, cs, vk::YM_INV, nk * g.Pz, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, sb, sa, nullptr);
+  }
+  for (int i = 1; i < ns; ++i) {
+    ck(cudaEventRecord(p->kev[i], p->kstream[i]), "event");
+    ck(cudaStreamWaitEvent(s, p->kev[i], 0), "wait");
+  }
 }
 
 // 'same' linear convolution of the x-transformed P-domain field held in SA
@@ -786,6 +897,10 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   }
   if (g.Wz == 1) {
     y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, p->ycrop, p->SA.p, p->SA.p, otf);
+    return;
+  }
+  if (p->kxc) {
+    conv_yz_chunked(p, s, otf);
     return;
   }
   y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
@@ -901,6 +1016,90 @@ __global__ void otf_sep_check_kernel(const float2* __restrict__ otf, const float
   }
 }
 
+// ---- half OTF (ky-mirror-symmetric PSF) ----------------------------------------
+// With both crop ramps folded in, the OTF of a PSF that is mirror-symmetric
+// along y (odd Ky) is EVEN in ky: the y ramp e^{+2 pi i cy ky / Wy} cancels
+// the corner-embedding phase e^{-2 pi i ky (Ky-1)/2 / Wy} exactly and what is
+// left is the transform of a centred symmetric function.  The widefield PSF
+// of C2 (and any PSF symmetric in y) qualifies -- it is not separable, so
+// the z pass reads its OTF -- and then only the Wy/2+1 columns ky <= Wy/2 are
+// stored and read: 128 of 256 MB per C2 z launch.  TESTED on the device OTFs
+// like the factored form: max |O(ky) - O(Wy-ky)| <= kOtfSepTol * max |O|.
+__global__ void otf_mirror_check_kernel(const float2* __restrict__ otf, int Hx, int Wz, int Wy, unsigned* bits) {
+  const size_t n = (size_t)Hx * Wz * Wy;
+  float err = 0.f, mx = 0.f;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int ky = (int)(i % Wy);
+    const float2 o = otf[i];
+    const float2 m = otf[i - ky + (ky == 0 ? 0 : Wy - ky)];
+    err = fmaxf(err, hypotf(o.x - m.x, o.y - m.y));
+    mx = fmaxf(mx, hypotf(o.x, o.y));
+  }
+  for (int m = 16; m > 0; m >>= 1) {
+    err = fmaxf(err, __shfl_xor_sync(0xffffffffu, err, m));
+    mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, m));
+  }
+  if ((threadIdx.x & 31) == 0) {
+    atomicMax(&bits[0], __float_as_uint(err));
+    atomicMax(&bits[1], __float_as_uint(mx));
+  }
+}
+
+// dst [Hx*Wz][owp] <- columns 0..Wy/2 of src [Hx*Wz][Wy] (pad column zero)
+__global__ void otf_halve_kernel(const float2* __restrict__ src, float2* __restrict__ dst, size_t rows, int Wy,
+                                 int owp) {
+  const size_t n = rows * owp;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (size_t)gridDim.x * blockDim.x) {
+    const int c = (int)(i % owp);
+    const size_t r = i / owp;
+    dst[i] = c <= Wy / 2 ? src[r * Wy + c] : make_float2(0.f, 0.f);
+  }
+}
+
+bool encode_otf_map(vk_rl_plan p, void* base, CUtensorMap* m);
+
+// Replaces both full OTFs by their halves when both pass the mirror test
+// (z pass with TMA OTF tiles only; VK_RL_NO_OTF_HALF=1 keeps the full ones).
+void halve_otfs(vk_rl_plan p) {
+  const char* no = std::getenv("VK_RL_NO_OTF_HALF");
+  if ((no && no[0] == '1') || !p->otma || p->ofactored || p->g.Wy % 2 || p->df || p->cl || p->zchunk) return;
+  const Geom& g = p->g;
+  DevBuf<unsigned> bits;
+  bits.alloc(4, "otf check");
+  ck(cudaMemsetAsync(bits.p, 0, 4 * sizeof(unsigned), p->stream), "otf check");
+  const float2* o[2] = {p->otf.p, p->otf_flip.p};
+  for (int k = 0; k < 2; ++k) {
+    otf_mirror_check_kernel<<<148 * 8, 256, 0, p->stream>>>(o[k], g.Hx, g.Wz, g.Wy, bits.p + 2 * k);
+    launch_check(p, "otf mirror check");
+  }
+  unsigned h[4];
+  ck(cudaMemcpyAsync(h, bits.p, sizeof(h), cudaMemcpyDeviceToHost, p->stream), "otf check D2H");
+  ck(cudaStreamSynchronize(p->stream), "otf check");
+  for (int k = 0; k < 2; ++k) {
+    float err, mx;
+    std::memcpy(&err, &h[2 * k], 4);
+    std::memcpy(&mx, &h[2 * k + 1], 4);
+    if (!(mx > 0.f && err <= kOtfSepTol * mx)) return;
+  }
+  const int owp = (g.Wy / 2 + 2) / 2 * 2;
+  const size_t rows = (size_t)g.Hx * g.Wz;
+  DevBuf<float2> half[2];
+  for (int k = 0; k < 2; ++k) {
+    half[k].alloc(rows * owp, "half otf");
+    otf_halve_kernel<<<148 * 8, 256, 0, p->stream>>>(o[k], half[k].p, rows, g.Wy, owp);
+    launch_check(p, "otf halve");
+  }
+  ck(cudaStreamSynchronize(p->stream), "otf halve");
+  std::swap(p->otf.p, half[0].p);
+  std::swap(p->otf.n, half[0].n);
+  std::swap(p->otf_flip.p, half[1].p);
+  std::swap(p->otf_flip.n, half[1].n);  // the full tables are freed with half[]
+  p->owp = owp;
+  p->ohalf = true;
+  if (!(encode_otf_map(p, p->otf.p, &p->omap) && encode_otf_map(p, p->otf_flip.p, &p->omap_flip)))
+    fail(VK_ERR_CUDA, "half otf tensor map");
+}
+
 // Sets p->ofactored when both OTFs pass the rank-1 test (VK_RL_NO_OTF_FACTOR=1
 // keeps the OTF reads).
 void factor_otfs(vk_rl_plan p) {
@@ -993,7 +1192,7 @@ void setup_dataflow(vk_rl_plan p) {
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda):
 // S_B as a 3D tensor {Wy, zrows, Hx} of 8-byte elements, box {16, Pz, 1}.
-bool encode_zmap(vk_rl_plan p, int zrows) {
+bool encode_zmap(vk_rl_plan p, int zrows, float2* base = nullptr, int planes = 0, CUtensorMap* out = nullptr) {
   using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
                                 const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
                                 CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
@@ -1008,11 +1207,11 @@ bool encode_zmap(vk_rl_plan p, int zrows) {
   }();
   if (!fn) return false;
   const Geom& g = p->g;
-  const cuuint64_t dims[3] = {(cuuint64_t)g.Wy, (cuuint64_t)zrows, (cuuint64_t)g.Hx};
+  const cuuint64_t dims[3] = {(cuuint64_t)g.Wy, (cuuint64_t)zrows, (cuuint64_t)(planes ? planes : g.Hx)};
   const cuuint64_t strides[2] = {(cuuint64_t)g.Wy * 8, (cuuint64_t)zrows * g.Wy * 8};
   const cuuint32_t box[3] = {16, (cuuint32_t)g.Pz, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
-  return fn(&p->zmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, p->SB.p, dims, strides, box, estr,
+  return fn(out ? out : &p->zmap, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base ? base : p->SB.p, dims, strides, box, estr,
             CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE) == CUDA_SUCCESS;
 }
@@ -1063,9 +1262,11 @@ bool encode_otf_map(vk_rl_plan p, void* base, CUtensorMap* m) {
     return false;
   }
   const Geom& g = p->g;
-  const cuuint64_t dims[3] = {(cuuint64_t)g.Wy, (cuuint64_t)g.Wz, (cuuint64_t)g.Hx};
-  const cuuint64_t strides[2] = {(cuuint64_t)g.Wy * 8, (cuuint64_t)g.Wz * g.Wy * 8};
-  const cuuint32_t box[3] = {16, (cuuint32_t)g.Wz, 1};
+  const cuuint64_t w = p->owp ? (cuuint64_t)p->owp : (cuuint64_t)g.Wy;  // half OTF: columns 0..owp-1
+  const cuuint64_t dims[3] = {w, (cuuint64_t)g.Wz, (cuuint64_t)g.Hx};
+  const cuuint64_t strides[2] = {w * 8, (cuuint64_t)g.Wz * w * 8};
+  // half OTF: 18-column boxes (rl_fast.cuh kHalfBox: even, 16-byte aligned starts)
+  const cuuint32_t box[3] = {p->owp ? 18u : 16u, (cuuint32_t)g.Wz, 1};
   const cuuint32_t estr[3] = {1, 1, 1};
   return ((EncodeFn)f)(m, CU_TENSOR_MAP_DATA_TYPE_UINT64, 3, base, dims, strides, box, estr,
                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
@@ -1383,6 +1584,39 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     }
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
+    // kx-chunked y/z convolution (VK_RL_KXCHUNK = target MB of S_B per chunk,
+    // 0 = whole-volume passes): TMA z plans of RL kind only
+    if (p->ztma && !conv && !zslab && !p->df && !p->cl && !p->zchunk) {
+      const char* kc = std::getenv("VK_RL_KXCHUNK");
+      const double mb = kc ? std::atof(kc) : 0.0;
+      if (mb > 0) {
+        const double plane = (double)g.Pz * g.Wy * 8;
+        const int c = std::max(1, (int)(mb * 1e6 / plane));
+        const int nch = (g.Hx + c - 1) / c;
+        p->kxc = nch > 1 ? (g.Hx + nch - 1) / nch : 0;  // balanced chunks
+      }
+      if (const char* ks = std::getenv("VK_RL_KXSTREAMS")) p->kxs = std::max(2, std::min(4, std::atoi(ks)));
+      if (p->kxc) {
+        p->ring2.alloc((size_t)p->kxs * p->kxc * g.Pz * g.Wy, "S_B ring");
+        for (int k = 0; k < p->kxs; ++k)
+          if (!encode_zmap(p, g.Pz, p->ring2.p + (size_t)k * p->kxc * g.Pz * g.Wy, p->kxc, &p->zmap_ring[k]))
+            p->kxc = 0;
+        const char* pe = std::getenv("VK_RL_RING_PERSIST");
+        int dev = 0, max_persist = 0, max_window = 0;
+        if (p->kxc && pe && pe[0] == '1' && cudaGetDevice(&dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev) == cudaSuccess &&
+            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev) == cudaSuccess &&
+            max_persist > 0 && max_window > 0) {
+          const size_t bytes = p->ring2.n * sizeof(float2);
+          size_t cur = 0;
+          cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
+          if (cur < std::min(bytes, (size_t)max_persist))
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, std::min(bytes, (size_t)max_persist));
+          p->ring_window = std::min(bytes, (size_t)max_window);
+        }
+        cudaGetLastError();
+      }
+    }
     p->otf.alloc(so, "otf");
     if (!conv) p->otf_flip.alloc(so, "otf_flip");
     if (p->ztma && !conv && g.Wz <= 256) {  // OTF tiles by TMA too (VK_RL_NO_OTF_TMA=1 disables)
@@ -1439,6 +1673,9 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     }
     ck(cudaStreamSynchronize(p->stream), "otf_flip");
     if (p->ztma || (g.Wz == 1 && p->fy && p->ytma)) factor_otfs(p);
+    // richardson_lucy plans only: the FRC sub-plan (pad = 0) uses its OTF
+    // buffers as full-size spectrum scratch
+    if (p->ztma && !conv && p->pad) halve_otfs(p);
     p->launches = 0;
   } catch (...) {
     delete p;
@@ -1993,11 +2230,27 @@ struct PlanKey {
   int device, rank, pad, conv;
   uint64_t shape[VK_MAX_RANK], kshape[VK_MAX_RANK];
   std::vector<float> psf;
+  std::string env;  // the VK_RL_* switches read at plan creation
   bool operator==(const PlanKey& o) const {
     return device == o.device && rank == o.rank && pad == o.pad && conv == o.conv &&
-           std::equal(shape, shape + rank, o.shape) && std::equal(kshape, kshape + rank, o.kshape) && psf == o.psf;
+           std::equal(shape, shape + rank, o.shape) && std::equal(kshape, kshape + rank, o.kshape) && psf == o.psf &&
+           env == o.env;
   }
 };
+
+// Plan-shaping environment switches (sorted "NAME=value;" list): a plan built
+// under other switches is a different plan.
+std::string plan_env() {
+  std::vector<std::string> v;
+  for (char** e = environ; e && *e; ++e)
+    if (std::strncmp(*e, "VK_RL_", 6) == 0 && std::strncmp(*e, "VK_RL_PLAN_CACHE=", 17) != 0 &&
+        std::strncmp(*e, "VK_RL_HOST_THREADS=", 19) != 0 && std::strncmp(*e, "VK_RL_LIB=", 10) != 0)
+      v.emplace_back(*e);
+  std::sort(v.begin(), v.end());
+  std::string s;
+  for (const auto& x : v) s += x + ";";
+  return s;
+}
 
 struct PlanCache {
   std::mutex mu;
@@ -2014,7 +2267,7 @@ struct PlanCache {
 
 PlanKey make_key(int device, int rank, const uint64_t* shape, const uint64_t* kshape, const float* psf, int pad,
                  int conv) {
-  PlanKey k{device, rank, pad, conv, {}, {}, {}};
+  PlanKey k{device, rank, pad, conv, {}, {}, {}, plan_env()};
   size_t kn = 1;
   for (int i = 0; i < rank; ++i) {
     k.shape[i] = shape[i];
@@ -2112,7 +2365,7 @@ uint64_t alg_bytes(vk_rl_plan p, int kind) {
 uint64_t otf_bytes(vk_rl_plan p, int kind) {
   const Geom& g = p->g;
   if (p->ofactored) return 0;
-  const uint64_t So = (uint64_t)g.Hx * g.Wz * g.Wy;
+  const uint64_t So = (uint64_t)g.Hx * g.Wz * (p->ohalf ? p->owp : g.Wy);
   switch (kind) {
     case VK_KIND_Z_CONV:
     case VK_KIND_Y_CONV:
@@ -2193,6 +2446,10 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
     if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
     if (p->ztma) s += " z:tma";
     if (p->ofactored) s += " otf:factored";
+    if (p->ohalf) s += " otf:half";
+    if (p->kxc)
+      s += " yz:kx-chunks(" + std::to_string(p->kxc) + "x" + std::to_string(p->kxs) + (p->ring_window ? ",l2persist" : "") +
+           ")";
     if (p->ytma) s += " y:bulk";
     if (p->xtma) s += " x:tma";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);
@@ -2216,7 +2473,8 @@ vk_status vk_rl_plan_profile(vk_rl_plan p, int enable) {
 vk_status vk_rl_plan_otf_bytes(vk_rl_plan p, int n_kinds, uint64_t* otf_bytes_per_launch) {
   return guarded([&] {
     if (!p || !otf_bytes_per_launch) fail(VK_ERR_ARG, "NULL argument");
-    for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k) otf_bytes_per_launch[k] = otf_bytes(p, k);
+    for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k)  // as profiled, else one whole-volume launch
+      otf_bytes_per_launch[k] = p->prof_last_otf[k] > 0 ? (uint64_t)(p->prof_last_otf[k] + 0.5) : otf_bytes(p, k);
   });
 }
 
@@ -2228,22 +2486,27 @@ vk_status vk_rl_plan_profile_read(vk_rl_plan p, int n_kinds, double* ms_total, u
     prof_collect(p);
     for (auto* l : p->lanes) prof_collect(l);
     for (int k = 0; k < n_kinds && k < VK_KIND_COUNT; ++k) {  // summed over the batch lanes
-      double ms = p->prof_ms[k];
+      double ms = p->prof_ms[k], bytes = p->prof_bytes[k], otf = p->prof_otf[k];
       uint64_t cnt = p->prof_n[k];
       for (auto* l : p->lanes) {
         ms += l->prof_ms[k];
         cnt += l->prof_n[k];
+        bytes += l->prof_bytes[k];
+        otf += l->prof_otf[k];
       }
       if (ms_total) ms_total[k] = ms;
       if (launches) launches[k] = cnt;
-      if (alg_bytes_per_launch) alg_bytes_per_launch[k] = alg_bytes(p, k);
+      // mean algorithmic bytes of the launches profiled (chunked passes
+      // launch per chunk), else one whole-volume launch's
+      if (alg_bytes_per_launch) alg_bytes_per_launch[k] = cnt ? (uint64_t)(bytes / cnt + 0.5) : alg_bytes(p, k);
+      if (cnt) p->prof_last_otf[k] = otf / cnt;
     }
     if (reset)
       for (int k = 0; k < VK_KIND_COUNT; ++k) {
-        p->prof_ms[k] = 0;
+        p->prof_ms[k] = p->prof_bytes[k] = p->prof_otf[k] = 0;
         p->prof_n[k] = 0;
         for (auto* l : p->lanes) {
-          l->prof_ms[k] = 0;
+          l->prof_ms[k] = l->prof_bytes[k] = l->prof_otf[k] = 0;
           l->prof_n[k] = 0;
         }
       }

@@ -269,6 +269,33 @@ def test_opt_in_schedules_match_default():
             assert tag in _with_env(env, lambda: vk.RlPlan(obs.shape, psf)).describe()
 
 
+def test_half_otf_mirror_symmetric_psf():
+    """A y-mirror-symmetric, non-separable PSF (the C2 widefield kind): the
+    plan stores only the ky <= Wy/2 half of both OTFs and the TMA z pass reads
+    mirrored columns.  Checked against the full-OTF read (VK_RL_NO_OTF_HALF=1)
+    and the oracle; an asymmetric PSF keeps the full tables."""
+    psf = O.widefield_psf(15)
+    obs = synth.blurred(synth.blobs((68, 116, 116), 12, 4, 8, seed=43), psf)  # W = 96 x 144 x 144
+    plan = vk.RlPlan(obs.shape, psf)
+    desc, half_bytes = plan.describe(), plan.device_bytes()
+    plan.close()
+    assert "otf:half" in desc and "z:tma" in desc and "otf:factored" not in desc, desc
+    rule = fixed_rule(6)
+    got = vk.richardson_lucy(obs, psf, rule)
+    fplan = _with_env({"VK_RL_NO_OTF_HALF": "1"}, lambda: vk.RlPlan(obs.shape, psf))
+    assert "otf:half" not in fplan.describe()
+    assert fplan.device_bytes() > half_bytes
+    fplan.close()
+    full = _with_env({"VK_RL_NO_OTF_HALF": "1"}, lambda: vk.richardson_lucy(obs, psf, rule))
+    assert rel_l2(got.estimate, full.estimate) <= 1e-6
+    its, _ = run_oracle(obs, psf, 6)
+    assert rel_l2(got.estimate, its[-1]) <= TOL_N
+    rng = np.random.default_rng(3)
+    asym = rng.random((15, 15, 15)).astype(np.float32)
+    asym /= asym.sum()
+    assert "otf:half" not in vk.RlPlan(obs.shape, asym).describe()
+
+
 def test_factored_otf_separable_psf():
     """Separable (Gaussian) PSF: the plan detects the rank-1 OTF and the TMA z
     pass rebuilds OTF columns from 1D factors. Checked against the full-OTF
