@@ -1584,11 +1584,15 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     }
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
-    // kx-chunked y/z convolution (VK_RL_KXCHUNK = target MB of S_B per chunk,
-    // 0 = whole-volume passes): TMA z plans of RL kind only
+    // kx-chunked y/z convolution (VK_RL_KXCHUNK = target MB of S_B per
+    // chunk, 0 = whole-volume passes), TMA z plans of RL kind.  Default 20 MB
+    // on 2 streams where S_B does not fit L2 anyway (> 64 MB): C2 +6.5%, C4
+    // +1.5%, chunk/stream sweep in profiles/r02/kxchunk.md; small volumes
+    // (C1/C3, S_B 26 MB) keep the whole-volume passes.
     if (p->ztma && !conv && !zslab && !p->df && !p->cl && !p->zchunk) {
       const char* kc = std::getenv("VK_RL_KXCHUNK");
-      const double mb = kc ? std::atof(kc) : 0.0;
+      const double sb_mb = (double)g.Hx * g.Pz * g.Wy * 8 / 1e6;
+      const double mb = kc ? std::atof(kc) : (sb_mb > 64.0 ? 20.0 : 0.0);
       if (mb > 0) {
         const double plane = (double)g.Pz * g.Wy * 8;
         const int c = std::max(1, (int)(mb * 1e6 / plane));
