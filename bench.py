@@ -87,6 +87,33 @@ def make_psf(kind, k, sigma, rank):
     return (v / v.sum()).astype(np.float32)
 
 
+def good_size(n: int) -> int:
+    """fftx::good_size (reference src/fft_plan.cpp:41-49): smallest 2^a 3^b 5^c >= n."""
+    if n <= 1:
+        return 1
+    c = n
+    while True:
+        m = c
+        for p in (2, 3, 5):
+            while m % p == 0:
+                m //= p
+        if m == 1:
+            return c
+        c += 1
+
+
+def config_dict(cfg, ws, n_batch):
+    """The workload record both arms print (identical keys and values)."""
+    shape, k = cfg["image"], cfg["psf"][1]
+    padded = [s + 2 * (k // 2) for s in shape]
+    return {"workload": cfg["label"] + (" per GPU" if ws > 1 and not n_batch else ""), "image": list(shape),
+            "psf": [k] * len(shape), "iters_per_step": cfg["iters"], "volumes": n_batch or ws,
+            "fft_shape": [good_size(p + k - 1) for p in padded], "padded_domain": padded,
+            "parallelism": (f"volume blocks over {ws} ranks" if n_batch else f"independent volumes x{ws}"),
+            "l2": "inputs larger than L2" if int(np.prod(shape)) * 4 > 126e6 or n_batch else
+                  "single volume partly L2-resident (126 MB L2)"}
+
+
 def load_peaks():
     p = os.path.join(ROOT, "MEASURED_PEAKS.json")
     if os.path.exists(p):
@@ -244,9 +271,9 @@ def run_reference_arm(args, cfg, ws, rank):
         line = {
             "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": per_it * 1e3,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
-            "data": "synthetic", "config": {"workload": cfg["label"], "image": list(shape),
-                                            "psf": list(psf.shape)},
+            "higher_is_better": True, "scaling": "strong" if cfg.get("volumes") else "weak", "vs_baseline": None,
+            "dtype": "f64",
+            "data": "synthetic", "config": config_dict(cfg, ws, cfg.get("volumes", 0)),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": reference_threads(), "kind": "reference",
                              "sample": (f"one step = one RL iteration of the full {shape} volume "
                                         f"(reference richardson_lucy, accelerated backend, {total} iterations in "
@@ -451,13 +478,9 @@ def main():
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": ws, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": elapsed_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if n_batch else "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-        "config": {"workload": cfg["label"] + (" per GPU" if ws > 1 and not n_batch else ""),
-                   "image": list(shape), "psf": list(psf.shape), "iters_per_step": iters,
-                   "volumes": n_batch or ws, "fft_shape": list(g), "padded_domain": list(P),
-                   "parallelism": (f"volume blocks over {ws} ranks" if n_batch else f"independent volumes x{ws}"),
-                   "plan": plan.describe(),
-                   "l2": "inputs larger than L2 (spectrum %.0f MB, observed %.0f MB > 126 MB)"
-                         % (s_p * 8 / 1e6, n_img * 4 / 1e6)},
+        "config": config_dict(cfg, ws, n_batch),
+        "plan": {"describe": plan.describe(), "fft_shape": list(g), "padded_domain": list(P),
+                 "spectrum_mb": round(s_p * 8 / 1e6, 1), "observed_mb": round(n_img * 4 / 1e6, 1)},
         "roofline": {"bound": "hbm", "kernel": dom, "achieved": kd["gbs"], "peak": peak, "unit": "GB/s",
                      "frac": kd["frac"], "traffic": traffic, "peak_source": peak_src,
                      "alg_bytes_per_launch": kd["bytes"] / kd["launches"],

@@ -262,8 +262,8 @@ typedef enum vk_kernel_kind {
   VK_KIND_Z_CONV = 4,   /* z-pass forward * OTF * inverse               */
   VK_KIND_Y_INV = 5,    /* y-pass inverse                               */
   VK_KIND_Y_CONV = 6,   /* y-pass forward * OTF * inverse (rank <= 2)   */
-  VK_KIND_YZ_DATAFLOW = 7, /* one-launch y fwd -> z*OTF*z -> y inv (3D) */
-  VK_KIND_YZ_CLUSTER = 8,  /* same, fused on thread-block clusters (DSMEM) */
+  VK_KIND_YZ_DATAFLOW = 7, /* reserved (retired one-launch y/z schedule)   */
+  VK_KIND_YZ_CLUSTER = 8,  /* reserved (retired cluster y/z schedule)       */
   VK_KIND_COUNT = 9
 } vk_kernel_kind;
 

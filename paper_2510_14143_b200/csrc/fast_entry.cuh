@@ -14,7 +14,7 @@ namespace vk {
 // TWG / YPREF / XMINB / XPB: x and y pass variants (rl_fast.cuh); ZTWG /
 // ZPREF / ZMINB: the z pass's.  Chosen per length from B200 measurements.
 template <int R1, int R2, int LX, int LZ, bool TWG = false, bool YPREF = true, int XMINB = 1, bool XPB = false,
-          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int ZPMINB = 2, int LY0 = 0,
+          bool ZTWG = false, bool ZPREF = true, int ZMINB = 1, bool PDL = true, int /*retired: pipelined-z floor*/ = 2, int LY0 = 0,
           int ZTMA = 0,  // ZTMA: resident-CTA floor of the TMA z kernel (0 = no TMA variant)
           bool YTMA = false,
           bool XTMA = false>  // XTMA: TMA-staged RATIO/UPDATE x pass (xpass_tma)
@@ -43,8 +43,6 @@ FastEntry make_entry() {
   e.smem_z = (size_t)(FastCfg<R1, R2, LZ, true>::DATA + (ZTWG ? 0 : R1 * R2) + (ZPREF ? R1 * R2 * LZ : 0)) *
              sizeof(float2);
   e.zk = (const void*)zpass_fast<R1, R2, LZ, ZTWG, ZPREF, ZMINB>;
-  e.smem_zp = ZPipeCfg<R1, R2, LZ, ZTWG, ZPREF>::smem;
-  e.zpk = (const void*)zpass_pipe<R1, R2, LZ, ZTWG, ZPREF, ZPMINB>;
   if constexpr (YTMA) {
     e.ytk = (const void*)ypass_tma<R1, R2, LY, TWG>;
     e.smem_yt = (size_t)(LY * YTma<R1 * R2, LY>::NP + (TWG ? 0 : ((R1 * R2 + 1) / 2) * 2)) * sizeof(float2);

@@ -50,8 +50,6 @@ struct FastEntry {
   int Lz, NTz;          // z-pass
   size_t smem_z;
   const void* zk;       // zpass_fast<R1,R2,Lz>(ZArgs)
-  size_t smem_zp;
-  const void* zpk;      // zpass_pipe<R1,R2,Lz>(ZArgs): persistent, double-buffered
   const void* ztk;      // zpass_tma<R1,R2>(ZTmaArgs): TMA-staged column tile (Lz = 16), or nullptr
   size_t smem_zt;
   size_t smem_zt_half;  // zpass_tma with a half OTF (wider OTF tile)
@@ -67,55 +65,3 @@ cudaError_t launch_otf_ramp(float2* otf, int Hx, size_t plane, int Wx, int cx, i
 
 }  // namespace vk
 
-namespace vk {
-
-// One-launch 3D y/z convolution (rl_dataflow.cuh): task codes and arguments.
-enum DfTask : unsigned { DF_YF = 0, DF_Z = 1, DF_YI = 2 };
-
-__host__ __device__ inline unsigned df_encode(unsigned type, unsigned plane, unsigned chunk) {
-  return (type << 30) | (plane << 14) | chunk;
-}
-
-struct DfArgs {
-  const float2* twy;
-  const float2* twz;
-  Geom g;
-  float2* SA;         // [Hx][Pz][Py]
-  float2* ring;       // [R][Pz][Wy]
-  const float2* otf;  // [Hx][Wz][Wy]
-  int R;
-  const unsigned* tasks;
-  int ntasks;
-  int* ctr;           // [0] next task, then done counters [3][Hx] (Yf, Z, Yi)
-  int nYf, nZ, nYi;
-};
-
-// One-launch 3D y/z convolution kernels by (Wy, Wz).
-struct DfEntry {
-  int Ny, Nz;
-  int Ly, Lz;
-  int NT;
-  size_t smem;
-  const void* k;  // yzconv_dataflow<...>(DfArgs)
-};
-const DfEntry* df_lookup(int ny, int nz);
-
-// Cluster-fused 3D y/z convolution kernels (rl_cluster.cuh) by (Wy, Wz).
-struct ClArgs {
-  const float2* twy;
-  const float2* twz;
-  Geom g;
-  float2* SA;         // [Hx][Pz][Py], read and written in place
-  const float2* otf;  // [Hx][Wz][Wy]
-};
-struct ClEntry {
-  int Ny, Nz;
-  int C;     // cluster size (CTAs, one per SM)
-  int RZ;    // max z rows per CTA: requires ceil(Pz / C) <= RZ
-  int NT;
-  size_t smem;
-  const void* k;  // yzconv_cluster<...>(ClArgs)
-};
-const ClEntry* cl_lookup(int ny, int nz, int pz);
-
-}  // namespace vk

@@ -223,13 +223,6 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
       }
     };
     prefetch_tile(z, y0, a.pf & 3);
-    // look-ahead (bits 4, 8): the tile of the CTA about one resident wave
-    // later in launch order (a.pfd blocks on), so its loads hit L2 as well
-    if ((a.pf & 12) && a.pfd > 0) {
-      const unsigned id = blockIdx.y * gridDim.x + blockIdx.x + (unsigned)a.pfd;
-      if (id < gridDim.x * gridDim.y)
-        prefetch_tile((int)(id / gridDim.x) + a.zoff, (int)(id % gridDim.x) * 2 * L, (a.pf >> 2) & 3);
-    }
     // the prefetches are hints (L2 is coherent): issued before the wait, they
     // overlap the previous pass's tail
     pdl_wait();
@@ -922,95 +915,6 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
     float2* out = a.out + (size_t)y_line(a, line0 + l) * a.out_pitch;
     for (int j = threadIdx.x; j < a.n_out; j += NT) out[j] = A[l * NP + j + a.out_off];
   }
-}
-
-// Persistent, double-buffered z convolution: each CTA walks tiles
-// (kx, ky-chunk) with stride gridDim.x and keeps the NEXT tile's column block
-// (and, with PREF, its OTF block) in flight (cp.async group) while it
-// transforms the current one, so HBM latency hides behind the FFT.  TWG /
-// PREF / MINB as for zpass_fast.
-template <int R1, int R2, int L, bool TWG, bool PREF>
-struct ZPipeCfg {
-  static constexpr int N = R1 * R2;
-  static constexpr int NT = FastCfg<R1, R2, L, true>::NT;
-  static constexpr int STAGE = N * (L + 1) + (PREF ? N * L : 0);  // padded data block (+ OTF tile)
-  static constexpr size_t smem = (size_t)((TWG ? 0 : N) + 2 * STAGE) * sizeof(float2);
-};
-
-template <int R1, int R2, int L, bool TWG, bool PREF, int MINB>
-__global__ void __launch_bounds__(ZPipeCfg<R1, R2, L, TWG, PREF>::NT, MINB == 1 ? 0 : MINB)
-    zpass_pipe(const ZArgs a) {
-  using C = ZPipeCfg<R1, R2, L, TWG, PREF>;
-  constexpr int N = C::N, NT = C::NT;
-  constexpr int ZS = NT / L;
-  constexpr int IT = (N + ZS - 1) / ZS;
-  extern __shared__ float2 smem[];
-  float2* tw = TWG ? nullptr : smem;
-  float2* buf = TWG ? smem : smem + N;  // stage s: padded data at buf + s*STAGE (OTF tile right after)
-  const unsigned Wy = a.Wy;
-  const int nchunks = (a.Wy + L - 1) / L;
-  const int ntiles = nchunks * a.hx;
-  pdl_trigger();
-  if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
-  const float2* twp = TWG ? a.plan.tw2 : tw;
-  pdl_wait();
-  // thread-derived offsets come from reg::fresh_tid() in every use, so the
-  // compiler cannot hoist IT unrolled addresses out of the tile loop
-  auto issue = [&](int tile, int stage) {
-    const int t = reg::fresh_tid();
-    const int l = t & (L - 1), z0 = t / L;
-    float2* A = buf + stage * C::STAGE;
-    float2* O = A + N * (L + 1);
-    const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
-    const bool kok = ky < a.Wy;
-    const float2* col = a.S + ((unsigned)kx * a.zrows * Wy + (kok ? ky : 0));
-    const float2* o = a.otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      const int z = z0 + k * ZS;
-      if (z < N) {
-        if (kok && z < a.n_in)
-          cp_async8(&A[sw<L>(z, l)], &col[(unsigned)z * Wy]);
-        else
-          A[sw<L>(z, l)] = make_float2(0.f, 0.f);
-        if (PREF && kok) cp_async8(&O[z * L + l], &o[(unsigned)z * Wy]);
-      }
-    }
-  };
-  int tile = blockIdx.x;
-  if (tile < ntiles) issue(tile, 0);
-  cp_async_commit();
-  for (int it = 0; tile < ntiles; ++it, tile += gridDim.x) {
-    const int stage = it & 1;
-    const int next = tile + gridDim.x;
-    if (next < ntiles) issue(next, stage ^ 1);
-    cp_async_commit();
-    cp_async_wait_1();  // the current tile's group has landed
-    __syncthreads();
-    float2* A = buf + stage * C::STAGE;
-    const float2* O = A + N * (L + 1);
-    reg::fft2<R1, R2, L, NT, false, L + 1, TWG>(A, twp);
-    const int t = reg::fresh_tid();
-    const int l = t & (L - 1), z0 = t / L;
-    const int kx = tile / nchunks, ky = (tile - kx * nchunks) * L + l;
-    const bool kok = ky < a.Wy;
-    const float2* og = a.otf + ((unsigned)kx * N * Wy + (kok ? ky : 0));
-#pragma unroll
-    for (int k = 0; k < IT; ++k) {
-      const int z = z0 + k * ZS;
-      if (z < N)
-        A[sw<L>(z, l)] = cmul(A[sw<L>(z, l)], PREF ? O[z * L + l]
-                                                   : (kok ? __ldg(&og[(unsigned)z * Wy]) : make_float2(0.f, 0.f)));
-    }
-    __syncthreads();
-    reg::fft2<R1, R2, L, NT, true, L + 1, TWG>(A, twp);
-    if (kok) {
-      float2* col = a.S + ((unsigned)kx * a.zrows * Wy + ky);
-      for (int z = z0; z < a.n_out; z += ZS) col[(unsigned)z * Wy] = A[sw<L>(z + a.out_off, l)];
-    }
-    __syncthreads();  // stage is refilled two tiles later
-  }
-  cp_async_wait_all();
 }
 
 #ifdef VK_FAST_TABLE_MAIN  // defined once, in rl_fast_table.cu

@@ -6,8 +6,6 @@
 #define VK_FAST_TABLE_MAIN  // otf_ramp_kernel lives in this TU
 #include "fast_table.h"
 #include "rl_fast.cuh"
-#include "rl_cluster.cuh"
-#include "rl_dataflow.cuh"
 
 namespace vk {
 
@@ -44,52 +42,7 @@ const FastEntry* fast_lookup(int n) {
   return nullptr;
 }
 
-template <int YR1, int YR2, int YL, int ZR1, int ZR2, int ZL>
-DfEntry make_df() {
-  using C = DfCfg<YR1, YR2, YL, ZR1, ZR2, ZL>;
-  return DfEntry{C::NY, C::NZ, YL, ZL, C::NT, C::smem, (const void*)yzconv_dataflow<YR1, YR2, YL, ZR1, ZR2, ZL>};
-}
-
-const DfEntry kDfTable[] = {
-    make_df<16, 18, 8, 8, 12, 16>(),    // C1/C3 grid: Wy 288, Wz 96
-    make_df<24, 24, 8, 12, 16, 8>(),    // C2 grid: Wy 576, Wz 192
-    make_df<30, 36, 4, 12, 12, 8>(),    // C4 grid: Wy 1080, Wz 144
-};
-
-template <int YR1, int YR2, int ZR1, int ZR2, int C, int RZ, int ZG, int NT>
-ClEntry make_cl() {
-  using K = ClCfg<YR1, YR2, ZR1, ZR2, C, RZ, ZG, NT>;
-  return ClEntry{K::NY, K::NZ, C, RZ, NT, K::smem, (const void*)yzconv_cluster<YR1, YR2, ZR1, ZR2, C, RZ, ZG, NT>};
-}
-
-const ClEntry kClTable[] = {
-    make_cl<16, 18, 8, 12, 4, 20, 24, 384>(),    // C1/C3 grid: Wy 288, Wz 96, Pz <= 80
-    make_cl<24, 24, 12, 16, 12, 14, 24, 384>(),  // C2 grid: Wy 576, Wz 192, Pz <= 168
-    make_cl<30, 36, 12, 12, 12, 10, 30, 384>(),  // C4 grid: Wy 1080, Wz 144, Pz <= 120
-};
-
-const ClEntry* cl_lookup(int ny, int nz, int pz) {
-  for (const auto& e : kClTable)
-    if (e.Ny == ny && e.Nz == nz && (pz + e.C - 1) / e.C <= e.RZ) return &e;
-  return nullptr;
-}
-
-const DfEntry* df_lookup(int ny, int nz) {
-  for (const auto& e : kDfTable)
-    if (e.Ny == ny && e.Nz == nz) return &e;
-  return nullptr;
-}
-
 cudaError_t fast_init_attributes() {
-  for (const auto& e : kClTable) {
-    cudaError_t r = cudaFuncSetAttribute(e.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
-    if (r) return r;
-    if (e.C > 8 && (r = cudaFuncSetAttribute(e.k, cudaFuncAttributeNonPortableClusterSizeAllowed, 1))) return r;
-  }
-  for (const auto& e : kDfTable) {
-    cudaError_t r = cudaFuncSetAttribute(e.k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem);
-    if (r) return r;
-  }
   for (const auto& e : kTable) {
     cudaError_t r;
     if ((r = cudaFuncSetAttribute(e.xk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_xp))) return r;
@@ -97,13 +50,12 @@ cudaError_t fast_init_attributes() {
       return r;
     if ((r = cudaFuncSetAttribute(e.yk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yconv))) return r;
     if ((r = cudaFuncSetAttribute(e.zk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_z))) return r;
-    if ((r = cudaFuncSetAttribute(e.zpk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zp))) return r;
     if (e.ztk && (r = cudaFuncSetAttribute(e.ztk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_zt_half)))
       return r;
     if (e.ytk && (r = cudaFuncSetAttribute(e.ytk, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)e.smem_yt)))
       return r;
     // prefer the full shared-memory carveout: occupancy is smem-limited
-    for (const void* k : {e.xk, e.xtk, e.yk, e.zk, e.zpk})
+    for (const void* k : {e.xk, e.xtk, e.yk, e.zk})
       if (k && (r = cudaFuncSetAttribute(k, cudaFuncAttributePreferredSharedMemoryCarveout, 100))) return r;
   }
   return cudaSuccess;

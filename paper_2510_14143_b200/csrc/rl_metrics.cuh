@@ -18,6 +18,7 @@
 // ring sums are block-reduced in shared memory then added with FP64 atomics.
 // Only the final curve walk (a few hundred bins) runs on the host.
 #pragma once
+#include <math_constants.h>
 #include "rl_passes.cuh"
 
 namespace vk {
@@ -288,6 +289,126 @@ __global__ void __launch_bounds__(256) ssim_axis_kernel(const float* __restrict_
     double v1[1] = {part};
     block_partial<1>(v1, sum + blockIdx.x);
   }
+}
+
+}  // namespace vk
+
+namespace vk {
+
+// ---- device-side stopping rule (CUDA-graph while loop, vk_rl.cu run_graph) ----
+// The iteration body is one graph; this kernel, its last node, evaluates the
+// stopping rule of deconv.cpp:401-423 on the device and sets the while
+// node's condition, so a run that may stop early never syncs the host per
+// iteration.
+struct StopState {
+  int it;       // iterations completed
+  int fails;    // consecutive changes below rel_tol
+  int stopped;  // the rule fired ("converged")
+  int pad;
+  double prev;  // metric of the previous iteration
+};
+
+struct RuleArgs {
+  StopState* st;
+  double* values;         // [iters] metric per iteration
+  unsigned long long* ts; // [iters + 1] %globaltimer at iteration ends (ts[0] = start)
+  const double* xpart;    // x-pass block partials of this iteration [nblocks][4] (si_psnr)
+  int nblocks;
+  double* acc;            // [iters][4]: LL, sum x, sum x^2, sum x r
+  const ObsStats* obs;    // reference statistics of the observed image
+  double n_img;
+  const double* metric_in;  // ssim: SSIM-map sum (divided by n_img); frc: the resolution
+  int metric;             // vk_stop_metric
+  double rel_tol;
+  int patience, iters;
+  cudaGraphConditionalHandle handle;
+};
+
+__device__ __forceinline__ double rel_change_dev(double prev, double cur) {  // deconv.cpp:296-300
+  if (isinf(prev) && isinf(cur) && prev == cur) return 0.0;
+  if (isinf(prev) || isinf(cur)) return CUDART_INF;
+  return fabs(cur - prev) / fmax(fabs(prev), 1e-30);
+}
+
+// si_psnr from the fused sums (metrics.cpp:67-101; host twin si_psnr_from_sums)
+__device__ __forceinline__ double si_psnr_dev(const ObsStats& o, double n, double sx, double sxx, double sxr) {
+  const double var_r = o.srr / n - (o.sr / n) * (o.sr / n);
+  const double var_x = sxx / n - (sx / n) * (sx / n);
+  const double cov = sxr / n - (sx / n) * (o.sr / n);
+  const double a = var_x > 0.0 ? cov / var_x : 0.0;
+  const double err = var_r - a * cov;
+  if (err <= 0.0) return CUDART_INF;
+  const double range = (double)__uint_as_float(o.maxbits) - (double)__uint_as_float(o.minbits);
+  return 10.0 * log10(range * range / err);
+}
+
+__global__ void __launch_bounds__(256) rule_step_kernel(RuleArgs a) {
+  const int k = a.st->it;  // 0-based index of the iteration just completed
+  for (int v = 0; v < 4; ++v) {  // this iteration's x-pass sums (LL; si_psnr sums), fixed order
+    const double s = block_sum_fixed(a.nblocks, [&](int b) { return a.xpart[(size_t)b * 4 + v]; });
+    if (threadIdx.x == 0) a.acc[(size_t)k * 4 + v] = s;
+    __syncthreads();
+  }
+  if (threadIdx.x != 0) return;
+  double value;
+  if (a.metric == 0) {
+    const double* s = a.acc + (size_t)k * 4;
+    value = si_psnr_dev(*a.obs, a.n_img, s[1], s[2], s[3]);
+  } else if (a.metric == 1) {  // VK_METRIC_SSIM_VS_PREV
+    value = a.metric_in[0] / a.n_img;
+  } else {  // VK_METRIC_FRC_RESOLUTION
+    value = a.metric_in[0];
+  }
+  a.values[k] = value;
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  a.ts[k + 1] = t;
+  StopState st = *a.st;
+  if (k > 0) {
+    st.fails = rel_change_dev(st.prev, value) < a.rel_tol ? st.fails + 1 : 0;
+    if (st.fails >= a.patience) st.stopped = 1;
+  }
+  st.prev = value;
+  st.it = k + 1;
+  *a.st = st;
+  cudaGraphSetConditional(a.handle, (!st.stopped && st.it < a.iters) ? 1u : 0u);
+}
+
+__global__ void timestamp_kernel(unsigned long long* ts) {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  *ts = t;
+}
+
+// frc_resolution of the ring sums (metrics.cpp:146-239; host twin frc_eval):
+// first ring below 1/7 (DC excluded), linear interpolation, 2*spacing / nu.
+__global__ void frc_value_kernel(const double* __restrict__ bins, int nb, double binf, double spacing,
+                                 double* __restrict__ out) {
+  if (threadIdx.x != 0 || blockIdx.x != 0) return;
+  const double* num = bins;
+  const double* da = bins + nb;
+  const double* db = bins + 2 * nb;
+  auto corr = [&](int j) {
+    const double den = sqrt(da[j] * db[j]);
+    return den > 0 ? num[j] / den : 0.0;
+  };
+  const double threshold = 1.0 / 7.0, sp = spacing * 2.0;
+  double res = CUDART_INF;  // kUnresolved
+  for (int j = 1; j < nb; ++j) {
+    if (corr(j) < threshold) {
+      double nu;
+      if (j == 1 || corr(j - 1) < threshold) {
+        nu = j * binf;
+      } else {
+        const double c0 = corr(j - 1), c1 = corr(j);
+        const double f0 = (j - 1) * binf, f1 = j * binf;
+        nu = f0 + (f1 - f0) * (c0 - threshold) / (c0 - c1);
+      }
+      res = nu <= 0 ? CUDART_INF : sp / nu;
+      break;
+    }
+  }
+  *out = res;
 }
 
 }  // namespace vk

@@ -67,7 +67,6 @@ struct XArgs {
   int zoff;             // first z row of this launch (z-chunked iterations)
   int pf;               // fast path: L2 prefetch of the CTA's inputs at entry (1 spectrum, 2 rows)
   int tbk, tnb;         // xpass_tma: kx per TMA box, boxes per CTA
-  int pfd;              // fast path: look-ahead distance in blocks (pf bits 4, 8)
 };
 
 struct YArgs {

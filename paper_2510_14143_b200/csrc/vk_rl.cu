@@ -227,7 +227,7 @@ class HostPool {
  private:
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    int n = (int)std::min(hw, 8u) - 1;
+    int n = (int)std::min(hw, 16u) - 1;
     if (const char* e = std::getenv("VK_RL_HOST_THREADS")) n = std::max(0, std::atoi(e) - 1);
     for (int i = 0; i < n; ++i)
       th_.emplace_back([this] {
@@ -368,21 +368,9 @@ struct vk_rl_plan_s {
   const vk::FastEntry* fx = nullptr;
   const vk::FastEntry* fy = nullptr;
   const vk::FastEntry* fz = nullptr;
-  // one-launch y/z convolution (3D fast grids), see rl_dataflow.cuh
-  const vk::DfEntry* df = nullptr;
-  int df_blocks = 0, df_R = 0, df_D = 0, df_ntasks = 0, df_nyf = 0, df_nz = 0;
-  DevBuf<float2> ring;
-  DevBuf<unsigned> df_tasks;
-  DevBuf<int> df_ctr;
-  size_t df_window = 0;
-  int zpipe_blocks = 0;  // > 0: persistent double-buffered z convolution
-  // z-chunked iterations (3D fast plans): y_inv -> x pass -> y_fwd per chunk
-  // of zchunk rows, so the chunk's spectrum rows stay in L2 between passes
-  int zchunk = 0;
   // TMA descriptor of S_B for the z convolution (zpass_tma), when available
   bool ztma = false, otma = false, ytma = false;
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
-  int xpfd = 0;  // x-pass look-ahead distance in blocks (XArgs::pfd)
   int ycrop = 0;
   bool xtma = false;  // xpass_tma for the RATIO/UPDATE x passes (S_A rows staged by TMA)
   CUtensorMap xmap{};
@@ -397,10 +385,25 @@ struct vk_rl_plan_s {
   DevBuf<float2> ring2;
   CUtensorMap zmap_ring[4]{};
   cudaStream_t kstream[4]{};  // kstream[0] unused (the run's stream)
+  // device-side stopping: the iteration body as a CUDA graph under a WHILE
+  // conditional node whose condition the rule kernel sets (run_graph_loop)
+  cudaGraph_t gr = nullptr;
+  cudaGraphExec_t grx = nullptr;
+  struct GraphKey {
+    const float* obs = nullptr;
+    int metric = -1, iters = 0, patience = 0;
+    double rel_tol = 0, spacing = 0;
+    bool operator==(const GraphKey& o) const {
+      return obs == o.obs && metric == o.metric && iters == o.iters && patience == o.patience &&
+             (rel_tol == o.rel_tol || (rel_tol != rel_tol && o.rel_tol != o.rel_tol)) && spacing == o.spacing;
+    }
+  } grkey;
+  uint64_t gr_body_launches = 0;
+  DevBuf<vk::StopState> gstate;
+  DevBuf<double> gvalues, gmetric;
+  DevBuf<unsigned long long> gts;
+  DevBuf<unsigned> grange_init;
   cudaEvent_t kev[4]{};
-  // cluster-fused y/z convolution (3D fast grids), see rl_cluster.cuh
-  const vk::ClEntry* cl = nullptr;
-  int cl_clusters = 0;
   // frc_resolution stopping metric (rl_metrics.cuh): a sub-plan supplies the
   // r2c transforms of the two half-size checkerboard images
   vk_rl_plan_s* frc = nullptr;
@@ -443,11 +446,6 @@ struct vk_rl_plan_s {
   int xblocks = 0, sum_done = 0;
 
   cudaStream_t stream = nullptr;
-  // z-chunked schedule on two streams (VK_RL_ZSTREAMS=2): odd chunks run on
-  // stream2, forked after the z pass and joined before the next one
-  int zstreams = 1;
-  cudaStream_t stream2 = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   std::vector<cudaEvent_t> events;
   double* h_acc = nullptr;  // pinned
   uint64_t launches = 0;
@@ -480,10 +478,9 @@ struct vk_rl_plan_s {
     for (auto e : prof_pool) cudaEventDestroy(e);
     if (h_acc) cudaFreeHost(h_acc);
     if (stream) cudaStreamDestroy(stream);
-    if (stream2) cudaStreamDestroy(stream2);
-    if (ev_fork) cudaEventDestroy(ev_fork);
-    if (ev_join) cudaEventDestroy(ev_join);
     if (h_frc) cudaFreeHost(h_frc);
+    if (grx) cudaGraphExecDestroy(grx);
+    if (gr) cudaGraphDestroy(gr);
     for (int i = 0; i < 4; ++i) {
       if (kstream[i]) cudaStreamDestroy(kstream[i]);
       if (kev[i]) cudaEventDestroy(kev[i]);
@@ -569,13 +566,15 @@ void flush_sums(vk_rl_plan p, cudaStream_t s, int upto) {
 
 // pdl: programmatic dependent launch (the kernel calls pdl_trigger/pdl_wait,
 // rl_fast.cuh); VK_RL_NO_PDL=1 turns it off.
+thread_local bool t_capturing = false;  // inside run_graph_loop's stream capture
+
 void launch(const void* k, dim3 grid, int nt, size_t smem, cudaStream_t s, void* arg, bool pdl = false) {
   void* args[] = {arg};
   static const bool no_pdl = [] {
     const char* e = std::getenv("VK_RL_NO_PDL");
     return e && e[0] == '1';
   }();
-  if (!pdl || no_pdl) {
+  if (!pdl || no_pdl || t_capturing) {  // graph body: plain kernel nodes
     ck(cudaLaunchKernel(k, grid, dim3(nt), args, smem, s), "launch");
     return;
   }
@@ -621,7 +620,6 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   }
   a.out = out;
   a.pf = p->xpf;
-  a.pfd = p->xpfd;
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
@@ -721,13 +719,6 @@ void z_pass(vk_rl_plan p, cudaStream_t s, int mode, int zrows, int n_in, int n_o
     prof_end(p, s, VK_KIND_Z_CONV, t);
     return;
   }
-  if (p->fz && p->zpipe_blocks && mode == vk::ZM_CONV) {
-    const size_t t = prof_begin(p, s);
-    launch(p->fz->zpk, dim3(p->zpipe_blocks), p->fz->NTz, p->fz->smem_zp, s, &a, p->fz->pdl);
-    launch_check(p, "zpass pipe");
-    prof_end(p, s, VK_KIND_Z_CONV, t);
-    return;
-  }
   dim3 grid((p->g.Wy + a.L - 1) / a.L, p->g.Hx);
   const size_t t = prof_begin(p, s);
   if (p->fz)
@@ -771,14 +762,18 @@ void z_pass_chunk(vk_rl_plan p, cudaStream_t s, const float2* otf, int kx0, int 
 }
 
 // The y/z convolution in chunks of kxc kx planes: y-forward -> z -> y-inverse
-// per chunk through an L2-sized ring slot, even chunks on `s`, odd ones on
-// stream2 (forked here, joined at the end), so one chunk's passes overlap the
-// other's and the GPU stays full while each chunk's S_B stays in L2.
+// per chunk through an L2-sized ring slot, chunk c on stream c % kxs (the
+// run's stream and kxs-1 forked ones, joined at the end), so the chunks'
+// passes overlap and fill the GPU while each chunk's S_B stays in L2
+// (C2: 11 chunks of 27 planes, 21 MB each, instead of 210 MB of S_B making
+// two HBM round trips per convolution; profiles/r02/kxchunk.md).
 void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   const Geom& g = p->g;
-  const int ns = p->kxs;
+  // per-launch profiling times each kernel with events on its stream: the
+  // profiled runs keep the chunks on one stream so kernels do not overlap
+  const int ns = p->prof ? 1 : p->kxs;
   if (!p->kev[0]) {
-    for (int i = 0; i < ns; ++i) {
+    for (int i = 0; i < p->kxs; ++i) {
       if (i) ck(cudaStreamCreateWithFlags(&p->kstream[i], cudaStreamNonBlocking), "cudaStreamCreate");
       ck(cudaEventCreateWithFlags(&p->kev[i], cudaEventDisableTiming), "event");
     }
@@ -789,7 +784,7 @@ void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
       v.accessPolicyWindow.hitRatio = 1.0f;
       v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
       v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-      for (int i = 1; i < ns; ++i) cudaStreamSetAttribute(p->kstream[i], cudaStreamAttributeAccessPolicyWindow, &v);
+      for (int i = 1; i < p->kxs; ++i) cudaStreamSetAttribute(p->kstream[i], cudaStreamAttributeAccessPolicyWindow, &v);
       cudaStreamSetAttribute(s, cudaStreamAttributeAccessPolicyWindow, &v);
       cudaGetLastError();
     }
@@ -816,85 +811,9 @@ void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
 // 'same' linear convolution of the x-transformed P-domain field held in SA
 // with `otf` (deconv.cpp:135-147 minus the x transforms, which live in the
 // fused X-pass).  Result back in SA.
-void conv_dataflow(vk_rl_plan p, cudaStream_t s, const float2* otf) {
-  const Geom& g = p->g;
-  vk::DfArgs a{};
-  a.twy = p->twy.p;
-  a.twz = p->twz.p;
-  a.g = g;
-  a.SA = p->SA.p;
-  a.ring = p->ring.p;
-  a.otf = otf;
-  a.R = p->df_R;
-  a.tasks = p->df_tasks.p;
-  a.ntasks = p->df_ntasks;
-  a.ctr = p->df_ctr.p;
-  a.nYf = p->df_nyf;
-  a.nZ = p->df_nz;
-  a.nYi = p->df_nyf;
-  ck(cudaMemsetAsync(p->df_ctr.p, 0, p->df_ctr.n * sizeof(int), s), "dataflow counters");
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p->df_ntasks);  // one CTA per task, ticket-ordered (rl_dataflow.cuh)
-  cfg.blockDim = dim3(p->df->NT);
-  cfg.dynamicSmemBytes = p->df->smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  int nat = 0;
-  if (p->df_window) {
-    at[0].id = cudaLaunchAttributeAccessPolicyWindow;
-    at[0].val.accessPolicyWindow.base_ptr = p->ring.p;
-    at[0].val.accessPolicyWindow.num_bytes = p->df_window;
-    at[0].val.accessPolicyWindow.hitRatio = 1.0f;
-    at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
-    at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
-    nat = 1;
-  }
-  cfg.attrs = at;
-  cfg.numAttrs = nat;
-  void* args[] = {&a};
-  const size_t t = prof_begin(p, s);
-  ck(cudaLaunchKernelExC(&cfg, p->df->k, args), "dataflow launch");
-  launch_check(p, "yz dataflow");
-  prof_end(p, s, VK_KIND_YZ_DATAFLOW, t);
-}
-
-void conv_cluster(vk_rl_plan p, cudaStream_t s, const float2* otf) {
-  vk::ClArgs a{};
-  a.twy = p->twy.p;
-  a.twz = p->twz.p;
-  a.g = p->g;
-  a.SA = p->SA.p;
-  a.otf = otf;
-  cudaLaunchConfig_t cfg{};
-  cfg.gridDim = dim3(p->cl_clusters * p->cl->C);
-  cfg.blockDim = dim3(p->cl->NT);
-  cfg.dynamicSmemBytes = p->cl->smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeClusterDimension;
-  at[0].val.clusterDim.x = p->cl->C;
-  at[0].val.clusterDim.y = 1;
-  at[0].val.clusterDim.z = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  void* args[] = {&a};
-  const size_t t = prof_begin(p, s);
-  ck(cudaLaunchKernelExC(&cfg, p->cl->k, args), "cluster launch");
-  launch_check(p, "yz cluster");
-  prof_end(p, s, VK_KIND_YZ_CLUSTER, t);
-}
-
 void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   const Geom& g = p->g;
   const int nl = g.Hx * g.Pz;
-  if (p->cl) {
-    conv_cluster(p, s, otf);
-    return;
-  }
-  if (p->df) {
-    conv_dataflow(p, s, otf);
-    return;
-  }
   if (g.Wz == 1) {
     y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, p->ycrop, p->SA.p, p->SA.p, otf);
     return;
@@ -906,39 +825,6 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
   y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr);
-}
-
-// One half-iteration of the z-chunked schedule: z convolution of the whole
-// volume, then per chunk of z rows: y inverse -> x pass (mode) -> y forward
-// (skipped when `last`).  The chunk's S_A / S_B rows written by one pass are
-// read by the next while still in L2.
-void chunked_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, float* est, const float* obs,
-                  int it, float* out, bool fwd_after) {
-  const Geom& g = p->g;
-  z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
-  const bool two = p->zstreams > 1;
-  if (two) {
-    if (!p->stream2) {
-      ck(cudaStreamCreateWithFlags(&p->stream2, cudaStreamNonBlocking), "cudaStreamCreate");
-      ck(cudaEventCreateWithFlags(&p->ev_fork, cudaEventDisableTiming), "event");
-      ck(cudaEventCreateWithFlags(&p->ev_join, cudaEventDisableTiming), "event");
-    }
-    ck(cudaEventRecord(p->ev_fork, s), "event");
-    ck(cudaStreamWaitEvent(p->stream2, p->ev_fork, 0), "wait");
-  }
-  int c = 0;
-  for (int z0 = 0; z0 < g.Pz; z0 += p->zchunk, ++c) {
-    const int zn = std::min(p->zchunk, g.Pz - z0);
-    cudaStream_t cs = two && (c & 1) ? p->stream2 : s;
-    y_pass(p, cs, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
-    x_pass(p, cs, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, est, obs, it, out, 0, z0, zn);
-    if (fwd_after)
-      y_pass(p, cs, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
-  }
-  if (two) {
-    ck(cudaEventRecord(p->ev_join, p->stream2), "event");
-    ck(cudaStreamWaitEvent(s, p->ev_join, 0), "wait");
-  }
 }
 
 // Full r2c spectrum [Hx][Wz][Wy] of a real block [rz][ry][rx] corner-embedded
@@ -1062,7 +948,7 @@ bool encode_otf_map(vk_rl_plan p, void* base, CUtensorMap* m);
 // (z pass with TMA OTF tiles only; VK_RL_NO_OTF_HALF=1 keeps the full ones).
 void halve_otfs(vk_rl_plan p) {
   const char* no = std::getenv("VK_RL_NO_OTF_HALF");
-  if ((no && no[0] == '1') || !p->otma || p->ofactored || p->g.Wy % 2 || p->df || p->cl || p->zchunk) return;
+  if ((no && no[0] == '1') || !p->otma || p->ofactored || p->g.Wy % 2) return;
   const Geom& g = p->g;
   DevBuf<unsigned> bits;
   bits.alloc(4, "otf check");
@@ -1130,64 +1016,6 @@ void factor_otfs(vk_rl_plan p) {
   }
   p->ofactored = ok;
   if (!ok) p->ofac.free();
-}
-
-// Task list, ring and counters of the one-launch y/z convolution.  Lag D (in
-// planes) ~ the number of planes whose tasks the resident CTAs hold at once;
-// ring R = 2D + 2 slots (task-order invariant R > 2D, see rl_dataflow.cuh).
-void setup_dataflow(vk_rl_plan p) {
-  const Geom& g = p->g;
-  const vk::DfEntry* d = p->df;
-  int dev = 0, nsm = 0, per_sm = 0;
-  ck(cudaGetDevice(&dev), "device");
-  ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
-  ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, d->k, d->NT, d->smem), "occupancy");
-  if (per_sm < 1) {
-    p->df = nullptr;
-    return;
-  }
-  p->df_blocks = per_sm * nsm;
-  p->df_nyf = (g.Pz + d->Ly - 1) / d->Ly;
-  p->df_nz = (g.Wy + d->Lz - 1) / d->Lz;
-  const int per_plane = 2 * p->df_nyf + p->df_nz;
-  const char* lag_env = std::getenv("VK_RL_DF_LAG");
-  int D = lag_env ? std::atoi(lag_env) : (p->df_blocks + per_plane - 1) / per_plane + 1;
-  D = std::max(1, std::min(D, g.Hx));
-  p->df_D = D;
-  // Yf(p) reuses the slot of Yi(p-R), which sits R-2D steps earlier in the list;
-  // keep that distance >= D so the slot is normally free when Yf starts.
-  const char* ring_env = std::getenv("VK_RL_DF_RING");
-  p->df_R = std::min(ring_env ? std::max(std::atoi(ring_env), 2 * D + 1) : 3 * D + 2, g.Hx);
-  std::vector<unsigned> tasks;
-  tasks.reserve((size_t)g.Hx * per_plane);
-  for (int step = 0; step < g.Hx + 2 * D; ++step) {
-    if (step < g.Hx)
-      for (int c = 0; c < p->df_nyf; ++c) tasks.push_back(vk::df_encode(vk::DF_YF, step, c));
-    if (step - D >= 0 && step - D < g.Hx)
-      for (int c = 0; c < p->df_nz; ++c) tasks.push_back(vk::df_encode(vk::DF_Z, step - D, c));
-    if (step - 2 * D >= 0 && step - 2 * D < g.Hx)
-      for (int c = 0; c < p->df_nyf; ++c) tasks.push_back(vk::df_encode(vk::DF_YI, step - 2 * D, c));
-  }
-  p->df_ntasks = (int)tasks.size();
-  p->df_tasks.alloc(tasks.size(), "dataflow tasks");
-  ck(cudaMemcpy(p->df_tasks.p, tasks.data(), tasks.size() * sizeof(unsigned), cudaMemcpyHostToDevice), "tasks");
-  p->df_ctr.alloc(1 + 3 * (size_t)g.Hx, "dataflow counters");
-  const size_t slot = (size_t)g.Pz * g.Wy;
-  p->ring.alloc((size_t)p->df_R * slot, "dataflow ring");
-  // keep the ring L2-resident (persisting window), within the device limits
-  int max_persist = 0, max_window = 0;
-  cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
-  cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
-  const char* nopersist = std::getenv("VK_RL_NO_L2_PERSIST");
-  if (max_persist > 0 && max_window > 0 && !(nopersist && nopersist[0] == '1')) {
-    const size_t bytes = p->ring.n * sizeof(float2);
-    size_t cur = 0;
-    cudaDeviceGetLimit(&cur, cudaLimitPersistingL2CacheSize);
-    const size_t want = std::min<size_t>(bytes, (size_t)max_persist);
-    if (cur < want) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
-    p->df_window = std::min<size_t>(bytes, (size_t)max_window);
-    cudaGetLastError();
-  }
 }
 
 // cuTensorMapEncodeTiled through the runtime's driver entry point (no -lcuda):
@@ -1444,50 +1272,6 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->fx = vk::fast_lookup(g.Wx);
       p->fy = vk::fast_lookup(g.Wy);
       p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
-      // Cluster/DSMEM fusion of the y/z convolution: opt-in.  Measured slower
-      // than the 3-launch path (C2: 2.07 vs 0.41 ms per convolution, C1: 0.15
-      // vs 0.06; profiles/r01/sweep_c2e.log) -- one CTA per SM with
-      // serialized load/transform/exchange phases cannot hide latency.
-      const char* cl_env = std::getenv("VK_RL_CLUSTER");
-      if (p->fy && p->fz && g.Wz > 1 && cl_env && cl_env[0] == '1') {
-        p->cl = vk::cl_lookup(g.Wy, g.Wz, g.Pz);
-        if (p->cl) {
-          cudaLaunchConfig_t cfg{};
-          cfg.blockDim = dim3(p->cl->NT);
-          cfg.dynamicSmemBytes = p->cl->smem;
-          cudaLaunchAttribute at[1];
-          at[0].id = cudaLaunchAttributeClusterDimension;
-          at[0].val.clusterDim.x = p->cl->C;
-          at[0].val.clusterDim.y = 1;
-          at[0].val.clusterDim.z = 1;
-          cfg.attrs = at;
-          cfg.numAttrs = 1;
-          cfg.gridDim = dim3(p->cl->C);
-          int ncl = 0;
-          if (cudaOccupancyMaxActiveClusters(&ncl, p->cl->k, &cfg) != cudaSuccess || ncl < 1) {
-            cudaGetLastError();
-            p->cl = nullptr;  // cluster shape not schedulable here: 3-launch path
-          } else {
-            p->cl_clusters = ncl;
-          }
-        }
-      }
-      const char* zp = std::getenv("VK_RL_ZPIPE");
-      if (p->fz && zp && zp[0] == '1') {
-        int nsm = 0, per = 0, dev = 0;
-        ck(cudaGetDevice(&dev), "device");
-        ck(cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev), "sm count");
-        ck(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, p->fz->zpk, p->fz->NTz, p->fz->smem_zp), "occ");
-        p->zpipe_blocks = per * nsm;
-      }
-      // The one-launch dataflow convolution halves HBM traffic but measured
-      // slower than the 3-launch path at C2 (0.55 vs 0.41 ms per convolution,
-      // profiles/r01/sweep_c2.log): the passes are latency/issue-bound, not
-      // HBM-bound, yet.  Opt-in until that flips.
-      const char* df_env = std::getenv("VK_RL_DATAFLOW");
-      const char* nodf = std::getenv("VK_RL_NO_DATAFLOW");
-      if (p->fy && p->fz && df_env && df_env[0] == '1' && !(nodf && nodf[0] == '1'))
-        p->df = vk::df_lookup(g.Wy, g.Wz);
       if (conv) p->fx = nullptr;  // XM_CONV_OUT lives in the generic x kernel
       if (p->fx) {  // butterfly-major pass-2 twiddles of the fast x pass (reg::load_twiddles2 layout)
         const int R1 = p->fx->R1, R2 = g.Wx / R1;
@@ -1516,16 +1300,6 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
         ck(cudaMemcpy(p->twy2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
         p->lpy.tw2 = p->twy2.p;
       }
-    }
-    // z-chunked schedule: opt-in (VK_RL_ZCHUNK=rows).  Measured slower at C2
-    // (rows 8/16/24/40: 2.49/1.80/1.76/1.48 vs 1.25 ms per iteration,
-    // profiles/r01/final/zchunk.log): the L2 reuse does not pay for
-    // launches that no longer fill the GPU.
-    const char* zc = std::getenv("VK_RL_ZCHUNK");
-    if (zc && p->fx && p->fy && p->fz && g.Wz > 1 && !p->df && !p->cl && !conv && !zslab) {
-      const int rows = std::atoi(zc);
-      p->zchunk = rows > 0 && rows < g.Pz ? rows : 0;
-      if (const char* zs2 = std::getenv("VK_RL_ZSTREAMS")) p->zstreams = std::max(1, std::atoi(zs2));
     }
     p->xL = pick_lines(g.Wx, 16, kSmemCap, x_smem);
     p->yL = pick_lines(g.Wy, 16, kSmemCap, yz_smem);
@@ -1572,16 +1346,6 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     p->xpf = g.Wz > 1 ? 3 : 0;
     if (const char* nts = std::getenv("VK_RL_NO_TMA_STORE")) p->tma_store = nts[0] != '1';
     if (const char* xpf = std::getenv("VK_RL_XPF")) p->xpf = std::atoi(xpf);
-    if (p->fx && (p->xpf & 12)) {  // look-ahead: one resident wave of x-pass CTAs
-      int dev = 0, nsm = 0, per = 0;
-      const void* k = p->fx->xtk && p->xtma ? p->fx->xtk : p->fx->xk;
-      if (cudaGetDevice(&dev) == cudaSuccess &&
-          cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev) == cudaSuccess &&
-          cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per, k, p->fx->NTx, p->fx->smem_xp) == cudaSuccess)
-        p->xpfd = per * nsm;
-      cudaGetLastError();
-      if (const char* d = std::getenv("VK_RL_XPFD")) p->xpfd = std::atoi(d);
-    }
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
     // kx-chunked y/z convolution (VK_RL_KXCHUNK = target MB of S_B per
@@ -1589,7 +1353,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     // on 2 streams where S_B does not fit L2 anyway (> 64 MB): C2 +6.5%, C4
     // +1.5%, chunk/stream sweep in profiles/r02/kxchunk.md; small volumes
     // (C1/C3, S_B 26 MB) keep the whole-volume passes.
-    if (p->ztma && !conv && !zslab && !p->df && !p->cl && !p->zchunk) {
+    if (p->ztma && !conv && !zslab) {
       const char* kc = std::getenv("VK_RL_KXCHUNK");
       const double sb_mb = (double)g.Hx * g.Pz * g.Wy * 8 / 1e6;
       const double mb = kc ? std::atof(kc) : (sb_mb > 64.0 ? 20.0 : 0.0);
@@ -1629,7 +1393,6 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
                 encode_otf_map(p, p->otf_flip.p, &p->omap_flip);
     }
     p->est.alloc((size_t)g.Pz * g.Py * g.Px, "estimate");
-    if (p->df) setup_dataflow(p);
     p->stats.alloc(1, "stats");
     p->ycrop = g.cy;  // until the OTF ramp below folds it in
 
@@ -1667,7 +1430,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     // Where the y inverse bulk-stores its lines (ypass_tma), the y crop is one
     // too, so the cropped lines start at slot 0 (16-byte aligned); C2 y inverse
     // -10% (profiles/r01/final/tst.log).
-    const bool yramp = p->fy && p->ytma && p->tma_store && !p->df && !p->cl && g.cy != 0;
+    const bool yramp = p->fy && p->ytma && p->tma_store && g.cy != 0;
     p->ycrop = yramp ? 0 : g.cy;
     const int cxr = p->fx ? g.cx : 0, cyr = yramp ? g.cy : 0;
     if (cxr != 0 || cyr != 0) {
@@ -1814,8 +1577,8 @@ void setup_frc(vk_rl_plan p) {
 }
 
 // frc_resolution(frc(even, odd), 2*spacing) of the current estimate crop
-// (metrics.cpp:146-239); the host walks the few hundred ring values.
-double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
+// (metrics.cpp:146-239): the ring sums into frc_bins (no sync).
+void frc_bins_enqueue(vk_rl_plan p, cudaStream_t s) {
   vk_rl_plan_s* f = p->frc;
   const int nb = p->frc_nbins;
 
@@ -1855,6 +1618,12 @@ double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
   }
   vk::frc_bins_reduce<<<3 * nb, 256, 0, s>>>(p->frc_bins.p + 3 * nb, kFrcBlocks, 3 * nb, p->frc_bins.p);
   launch_check(p, "frc reduce");
+}
+
+// ... and the host walks the few hundred ring values (one sync).
+double frc_eval(vk_rl_plan p, cudaStream_t s, double spacing) {
+  frc_bins_enqueue(p, s);
+  const int nb = p->frc_nbins;
   ck(cudaMemcpyAsync(p->h_frc, p->frc_bins.p, (size_t)3 * nb * sizeof(double), cudaMemcpyDeviceToHost, s),
      "frc D2H");
   ck(cudaStreamSynchronize(s), "frc");
@@ -1903,16 +1672,12 @@ void setup_ssim(vk_rl_plan p, int iters) {
   }
 }
 
-// ssim(crop(est), previous) for iteration `it` (1-based); previous is the
-// observed image at it = 1 and the crop of iteration it-1 afterwards
-// (deconv.cpp:352, 403, 423).  The sum lands in ss_sum[it-1]; no sync.
-void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
+// The three separable smoothing passes and the SSIM-map sum of cur against
+// prev (whose range is range_prev[0..1]), reduced in a fixed order into *sum.
+void ssim_passes(vk_rl_plan p, cudaStream_t s, const float* cur, const float* prev, const unsigned* range_prev,
+                 double* sum_out) {
   const Geom& g = p->g;
   const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
-  float* cur = p->ss_img[it % 2].p;
-  const float* prev = it == 1 ? d_obs : p->ss_img[(it - 1) % 2].p;
-  vk::crop_range_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, cur, g, p->ss_range.p + 2 * it);
-  launch_check(p, "ssim crop");
   static const vk::SsimTaps taps = [] {  // filters.cpp:78-90
     vk::SsimTaps t{};
     const double sigma = 1.5;
@@ -1925,8 +1690,7 @@ void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
     for (double& v : t.w) v /= sum;
     return t;
   }();
-  const unsigned* range = p->ss_range.p + 2 * (it - 1);
-  double* sum = p->part.p;  // block partials of the last pass, reduced into ss_sum[it-1] below
+  double* sum = p->part.p;  // block partials of the last pass
   const int grid = 148 * 8;
   size_t stride = 1;
   size_t strides[3];
@@ -1934,6 +1698,7 @@ void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
     strides[a] = stride;
     stride *= p->ishape[a];
   }
+  const unsigned* range = range_prev;
   for (int k = 0; k < p->rank; ++k) {
     const int ext = (int)p->ishape[k];
     const double* in = k == 0 ? nullptr : p->ss_f[(k - 1) % 2].p;
@@ -1953,8 +1718,152 @@ void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
                                                                      taps, range, sum);
     launch_check(p, "ssim pass");
   }
-  vk::reduce_partials_kernel<<<1, 256, 0, s>>>(p->part.p, grid, 1, p->ss_sum.p + (it - 1));
+  vk::reduce_partials_kernel<<<1, 256, 0, s>>>(p->part.p, grid, 1, sum_out);
   launch_check(p, "ssim reduce");
+}
+
+// ssim(crop(est), previous) for iteration `it` (1-based); previous is the
+// observed image at it = 1 and the crop of iteration it-1 afterwards
+// (deconv.cpp:352, 403, 423).  The sum lands in ss_sum[it-1]; no sync.
+void ssim_eval(vk_rl_plan p, cudaStream_t s, int it, const float* d_obs) {
+  const Geom& g = p->g;
+  float* cur = p->ss_img[it % 2].p;
+  const float* prev = it == 1 ? d_obs : p->ss_img[(it - 1) % 2].p;
+  vk::crop_range_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, cur, g, p->ss_range.p + 2 * it);
+  launch_check(p, "ssim crop");
+  ssim_passes(p, s, cur, prev, p->ss_range.p + 2 * (it - 1), p->ss_sum.p + (it - 1));
+}
+
+// ssim_vs_prev inside the graph body: fixed slots instead of the per-iteration
+// ping-pong -- current crop ss_img[0] and range row 1, previous ss_img[1] and
+// row 0 (seeded with the observed image), rolled over after the evaluation;
+// the SSIM-map sum lands in gmetric.
+void ssim_eval_graph(vk_rl_plan p, cudaStream_t s) {
+  const Geom& g = p->g;
+  const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
+  ck(cudaMemcpyAsync(p->ss_range.p + 2, p->grange_init.p, 2 * sizeof(unsigned), cudaMemcpyDeviceToDevice, s),
+     "ssim range");
+  vk::crop_range_kernel<<<148 * 4, kThreads, 0, s>>>(p->est.p, p->ss_img[0].p, g, p->ss_range.p + 2);
+  launch_check(p, "ssim crop");
+  ssim_passes(p, s, p->ss_img[0].p, p->ss_img[1].p, p->ss_range.p, p->gmetric.p);
+  ck(cudaMemcpyAsync(p->ss_img[1].p, p->ss_img[0].p, nI * sizeof(float), cudaMemcpyDeviceToDevice, s), "ssim roll");
+  ck(cudaMemcpyAsync(p->ss_range.p, p->ss_range.p + 2, 2 * sizeof(unsigned), cudaMemcpyDeviceToDevice, s),
+     "ssim roll");
+}
+
+// Iterations 1.. of richardson_lucy with the stopping rule decided on the
+// device (deconv.cpp:401-423): one iteration = one CUDA graph (convolutions,
+// x passes, metric, rule kernel) under a WHILE conditional node; the rule
+// kernel sets the condition, so nothing returns to the host until the run
+// ends.  The graph is built once per (observed buffer, rule) and replayed.
+// Outputs: iterations run, stop flag, per-iteration metric values, device
+// timestamps (wall_s), and acc rows (LL, sums).
+void run_graph_loop(vk_rl_plan p, cudaStream_t s, const float* d_obs, const vk_stop_rule* rule, bool frc, bool ssim,
+                    double spacing, std::vector<double>& values, std::vector<double>& wall, int& run, bool& stopped) {
+  const Geom& g = p->g;
+  const int iters = rule->max_iters;
+  const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
+  if (!p->gstate.p) {
+    p->gstate.alloc(1, "stop state");
+    p->gmetric.alloc(1, "metric");
+    p->grange_init.alloc(2, "range init");
+    const unsigned init[2] = {0x7f800000u, 0u};
+    ck(cudaMemcpy(p->grange_init.p, init, sizeof(init), cudaMemcpyHostToDevice), "range init");
+  }
+  if (p->gvalues.n < (size_t)iters) {
+    p->gvalues.alloc(iters, "metric values");
+    p->gts.alloc(iters + 1, "timestamps");
+  }
+  const int metric = frc ? VK_METRIC_FRC_RESOLUTION : ssim ? VK_METRIC_SSIM_VS_PREV : VK_METRIC_SI_PSNR_VS_INPUT;
+  vk_rl_plan_s::GraphKey key;
+  key.obs = d_obs;
+  key.metric = metric;
+  key.iters = iters;
+  key.patience = rule->patience;
+  key.rel_tol = rule->rel_tol;
+  key.spacing = spacing;
+  if (!p->grx || !(key == p->grkey)) {
+    if (p->grx) cudaGraphExecDestroy(p->grx);
+    if (p->gr) cudaGraphDestroy(p->gr);
+    p->grx = nullptr;
+    p->gr = nullptr;
+    ck(cudaGraphCreate(&p->gr, 0), "graph");
+    cudaGraphConditionalHandle h;
+    ck(cudaGraphConditionalHandleCreate(&h, p->gr, 1, cudaGraphCondAssignDefault), "graph condition");
+    cudaGraphNodeParams cp{};
+    cp.type = cudaGraphNodeTypeConditional;
+    cp.conditional.handle = h;
+    cp.conditional.type = cudaGraphCondTypeWhile;
+    cp.conditional.size = 1;
+    cudaGraphNode_t node;
+    ck(cudaGraphAddNode(&node, p->gr, nullptr, 0, &cp), "graph while node");
+    cudaGraph_t body = cp.conditional.phGraph_out[0];
+    const uint64_t before = p->launches;
+    ck(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal), "capture");
+    t_capturing = true;
+    try {
+      conv_yz(p, s, p->otf.p);
+      // every iteration's partials in slot 0: the rule kernel reduces them before the next
+      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
+      conv_yz(p, s, p->otf_flip.p);
+      x_pass(p, s, vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
+      if (frc) {
+        frc_bins_enqueue(p, s);
+        vk::frc_value_kernel<<<1, 32, 0, s>>>(p->frc_bins.p, p->frc_nbins, p->frc_binf, spacing, p->gmetric.p);
+        launch_check(p, "frc value");
+      }
+      if (ssim) ssim_eval_graph(p, s);
+      vk::RuleArgs ra{};
+      ra.st = p->gstate.p;
+      ra.values = p->gvalues.p;
+      ra.ts = p->gts.p;
+      ra.xpart = p->xpart.p;
+      ra.nblocks = p->xblocks;
+      ra.acc = p->acc.p;
+      ra.obs = p->stats.p;
+      ra.n_img = (double)nI;
+      ra.metric_in = p->gmetric.p;
+      ra.metric = metric;
+      ra.rel_tol = rule->rel_tol;
+      ra.patience = rule->patience;
+      ra.iters = iters;
+      ra.handle = h;
+      vk::rule_step_kernel<<<1, 256, 0, s>>>(ra);
+      launch_check(p, "rule");
+    } catch (...) {
+      t_capturing = false;
+      cudaGraph_t junk;
+      cudaStreamEndCapture(s, &junk);
+      cudaGetLastError();
+      throw;
+    }
+    t_capturing = false;
+    ck(cudaStreamEndCapture(s, &body), "end capture");
+    ck(cudaGraphInstantiate(&p->grx, p->gr, 0), "graph instantiate");
+    p->gr_body_launches = p->launches - before;
+    p->launches = before;
+    p->grkey = key;
+  }
+  ck(cudaMemsetAsync(p->gstate.p, 0, sizeof(vk::StopState), s), "stop state");
+  vk::timestamp_kernel<<<1, 1, 0, s>>>(p->gts.p);
+  launch_check(p, "timestamp");
+  if (ssim) {  // previous = the observed image (deconv.cpp:352), its range already in row 0
+    ck(cudaMemcpyAsync(p->ss_img[1].p, d_obs, nI * sizeof(float), cudaMemcpyDeviceToDevice, s), "ssim seed");
+  }
+  ck(cudaGraphLaunch(p->grx, s), "graph launch");
+  vk::StopState st{};
+  ck(cudaMemcpyAsync(&st, p->gstate.p, sizeof(st), cudaMemcpyDeviceToHost, s), "stop state D2H");
+  ck(cudaStreamSynchronize(s), "graph run");
+  run = st.it;
+  stopped = st.stopped != 0;
+  p->launches += p->gr_body_launches * (uint64_t)run;
+  values.resize(run);
+  std::vector<unsigned long long> ts(run + 1);
+  ck(cudaMemcpy(values.data(), p->gvalues.p, run * sizeof(double), cudaMemcpyDeviceToHost), "values D2H");
+  ck(cudaMemcpy(ts.data(), p->gts.p, (run + 1) * sizeof(unsigned long long), cudaMemcpyDeviceToHost), "ts D2H");
+  wall.resize(run);
+  for (int k = 0; k < run; ++k) wall[k] = (double)(ts[k + 1] - ts[k]) * 1e-9;
+  p->sum_done = run;  // acc rows were written by the rule kernel
 }
 
 // The richardson_lucy loop on device buffers (deconv.cpp:333-430).
@@ -2024,32 +1933,33 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
   x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, 0, nullptr,
          p->fx ? g.cx : 0);
-  const bool chunked = p->zchunk > 0;
-  if (chunked)  // the chunked schedule enters each iteration at the z convolution
-    y_pass(p, s, vk::YM_FWD, g.Hx * g.Pz, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
 
   // Early stop is only possible from iteration patience+1 on (fails counts
   // from iteration 2); before that no host round-trip is needed.
   const bool may_stop = rule->patience + 1 <= iters;
   int run = 0;
   bool stopped = false;
-  std::vector<double> values;
+  std::vector<double> values, gwall;
+  // A run that may stop early decides on the device (run_graph_loop) unless
+  // per-launch profiling is on or VK_RL_NO_GRAPH=1; fixed-count runs (e.g.
+  // the benchmark, patience = max_iters) launch the passes directly.
+  const char* nograph = std::getenv("VK_RL_NO_GRAPH");
+  const bool graph = may_stop && !p->prof && !(nograph && nograph[0] == '1');
+  if (graph) {
+    run_graph_loop(p, s, d_obs, rule, frc, ssim, spacing, values, gwall, run, stopped);
+    vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
+    launch_check(p, "crop");
+  }
   ck(cudaEventRecord(p->events[0], s), "event");
-  for (int it = 1; it <= iters; ++it) {
+  for (int it = 1; it <= iters && !graph; ++it) {
     // the last iteration writes the cropped output directly unless a metric
     // still needs the updated estimate
     const bool last = it == iters && !frc && !ssim;
-    if (chunked) {
-      chunked_half(p, s, p->otf.p, vk::XM_RATIO, p->est.p, d_obs, it, nullptr, true);
-      chunked_half(p, s, p->otf_flip.p, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, p->est.p, d_obs, it,
-                   last ? d_out : nullptr, it < iters);
-    } else {
-      conv_yz(p, s, p->otf.p);
-      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, nullptr);
-      conv_yz(p, s, p->otf_flip.p);
-      x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
-             it, last ? d_out : nullptr);
-    }
+    conv_yz(p, s, p->otf.p);
+    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, nullptr);
+    conv_yz(p, s, p->otf_flip.p);
+    x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
+           it, last ? d_out : nullptr);
     if (frc) values.push_back(frc_eval(p, s, spacing));  // syncs: the value is needed on the host
     if (ssim) ssim_eval(p, s, it, d_obs);
     ck(cudaEventRecord(p->events[it], s), "event");
@@ -2079,14 +1989,16 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
       }
     }
   }
-  if ((frc || ssim) && !stopped) {  // the last iteration ran in UPDATE mode: crop now
+  if ((frc || ssim) && !stopped && !graph) {  // the last iteration ran in UPDATE mode: crop now
     vk::crop_kernel<<<sgrid, kThreads, 0, s>>>(p->est.p, d_out, g);
     launch_check(p, "crop");
   }
   flush_sums(p, s, run);
   ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
   ck(cudaStreamSynchronize(s), "run");
-  if (ssim) {
+  if (graph) {
+    // values, stop decision and timestamps come from the device
+  } else if (ssim) {
     std::vector<double> sums(run);
     ck(cudaMemcpy(sums.data(), p->ss_sum.p, (size_t)run * sizeof(double), cudaMemcpyDeviceToHost), "ssim D2H");
     values.resize(run);
@@ -2109,9 +2021,12 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     for (int i = 0; i < 3; ++i) trace->fft_shape[i] = i < p->rank ? p->wshape[i] : 0;
     for (int k = 0; k < run && k < trace->capacity; ++k) {
       const double* a = p->h_acc + (size_t)k * 4;
-      if (trace->metric) trace->metric[k] = (frc || ssim) ? values[k] : si_psnr_from_sums(rs, a[1], a[2], a[3]);
+      if (trace->metric)
+        trace->metric[k] = (frc || ssim || graph) ? values[k] : si_psnr_from_sums(rs, a[1], a[2], a[3]);
       if (trace->log_likelihood) trace->log_likelihood[k] = a[0];
-      if (trace->wall_s) {
+      if (trace->wall_s && graph) {
+        trace->wall_s[k] = gwall[k];
+      } else if (trace->wall_s) {
         float ms = 0;
         ck(cudaEventElapsedTime(&ms, p->events[k], p->events[k + 1]), "elapsed");
         trace->wall_s[k] = ms * 1e-3;
@@ -2413,7 +2328,7 @@ vk_status vk_rl_plan_device_bytes(vk_rl_plan p, uint64_t* bytes) {
     if (!p || !bytes) fail(VK_ERR_ARG, "NULL argument");
     *bytes = (p->SA.n + p->SB.n + p->otf.n + p->otf_flip.n + p->ofac.n) * sizeof(float2) +
              (p->est.n + p->obs.n + p->out.n) * sizeof(float) + p->acc.n * sizeof(double) +
-             p->ring.n * sizeof(float2) + (p->ss_img[0].n + p->ss_img[1].n) * sizeof(float) +
+             p->ring2.n * sizeof(float2) + (p->ss_img[0].n + p->ss_img[1].n) * sizeof(float) +
              (p->ss_f[0].n + p->ss_f[1].n + p->ss_sum.n) * sizeof(double) +
              (p->frc_even.n + p->frc_odd.n) * sizeof(float);
     if (p->frc) *bytes += (p->frc->SA.n + p->frc->SB.n + p->frc->otf.n + p->frc->otf_flip.n) * sizeof(float2);
@@ -2438,22 +2353,12 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
                     " P=" + std::to_string(g.Pz) + "x" + std::to_string(g.Py) + "x" + std::to_string(g.Px) + " " +
                     axis("x", p->fx, p->fx ? p->fx->Lx : p->xL) + " " + axis("y", p->fy, p->fy ? p->fy->Ly : p->yL) +
                     " " + axis("z", p->fz, p->fz ? p->fz->Lz : p->zL) + " yz:";
-    if (p->cl)
-      s += "cluster(C=" + std::to_string(p->cl->C) + ",clusters=" + std::to_string(p->cl_clusters) +
-           ",NT=" + std::to_string(p->cl->NT) + ",smem=" + std::to_string(p->cl->smem) + ")";
-    else if (p->df)
-      s += "dataflow(blocks=" + std::to_string(p->df_blocks) + ",D=" + std::to_string(p->df_D) +
-           ",R=" + std::to_string(p->df_R) + ",tasks=" + std::to_string(p->df_ntasks) +
-           ",l2_window=" + std::to_string(p->df_window) + ")";
-    else
-      s += g.Wz > 1 ? "3-pass" : "y-conv";
-    if (p->zchunk) s += " zchunk=" + std::to_string(p->zchunk);
+    s += p->kxc ? "kx-chunks(" + std::to_string(p->kxc) + "x" + std::to_string(p->kxs) +
+                      (p->ring_window ? ",l2persist" : "") + ")"
+                : g.Wz > 1 ? "3-pass" : "y-conv";
     if (p->ztma) s += " z:tma";
     if (p->ofactored) s += " otf:factored";
     if (p->ohalf) s += " otf:half";
-    if (p->kxc)
-      s += " yz:kx-chunks(" + std::to_string(p->kxc) + "x" + std::to_string(p->kxs) + (p->ring_window ? ",l2persist" : "") +
-           ")";
     if (p->ytma) s += " y:bulk";
     if (p->xtma) s += " x:tma";
     std::strncpy(buf, s.c_str(), (size_t)len - 1);

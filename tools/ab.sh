@@ -17,7 +17,7 @@ try:
     r = d["roofline"]
     print(sys.argv[2], "value %.4g" % d["value"], "ms/step %.3f" % d["ms_per_step"],
           " ".join("%s=%.4f" % (k, v["ms_per_step"]) for k, v in r["per_kernel"].items()),
-          "itfrac %.3f" % r["iteration_frac"], "clk", d["clocks"]["sm_mhz"], d["config"]["plan"].split("yz:")[-1])
+          "itfrac %.3f" % r["iteration_frac"], "clk", d["clocks"]["sm_mhz"], d["plan"]["describe"].split("yz:")[-1])
 except Exception as e:
     print(sys.argv[2], "FAILED", e)
 PY
