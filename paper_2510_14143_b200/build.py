@@ -39,8 +39,15 @@ CLI_SRC = os.path.join(PKG, "host", "vk_cli.cu")
 CLI = os.path.join(LIBDIR, "voxelkit_b200")
 
 
-# rl_fast_len.cu is compiled once per compile-time FFT length (-DVK_LEN=N)
-FAST_LENGTHS = (64, 96, 144, 192, 256, 288, 576, 1080, 2160)
+# rl_fast_len.cu is compiled once per compile-time FFT length (-DVK_LEN=N),
+# the lengths listed in csrc/fast_lengths.def
+def _fast_lengths():
+    import re
+    with open(os.path.join(CSRC, "fast_lengths.def")) as f:
+        return tuple(int(m) for m in re.findall(r"^VK_FAST_LEN\((\d+)\)", f.read(), re.M))
+
+
+FAST_LENGTHS = _fast_lengths()
 
 
 def sources():
@@ -93,9 +100,17 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra_flags)
 
+    headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".def"))] + [
+        os.path.join(ROOT, "include", h) for h in ("vk_rl.h", "vk_io.h")]
+    newest_header = max(os.path.getmtime(h) for h in headers)
+
     def compile_one(unit):
         src, extra, obj = unit
-        cmd = [_nvcc(), *compile_flags, *extra, "-c", "-o", os.path.join(objdir, obj), src]
+        out = os.path.join(objdir, obj)
+        if (not force and os.path.exists(out) and os.path.getmtime(out) >= os.path.getmtime(src)
+                and os.path.getmtime(out) >= newest_header and not extra_flags):
+            return None, None  # up to date (source and every header older than the object)
+        cmd = [_nvcc(), *compile_flags, *extra, "-c", "-o", out, src]
         r = subprocess.run(cmd, capture_output=True, text=True)
         return cmd, r
 
@@ -105,6 +120,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
     with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
         results = list(ex.map(compile_one, units()))
     for cmd, r in results:
+        if cmd is None:
+            continue
         if verbose:
             print(" ".join(cmd))
         if r.returncode != 0:

@@ -39,7 +39,41 @@ FastEntry fast_entry_1080() { return make_entry<30, 36, 8, 4, false, true, 2, tr
 // stack): C5 x passes 0.0774 vs 0.0801 ms per field-iteration (final/x2160.log)
 FastEntry fast_entry_2160() { return make_entry<45, 48, 4, 2, true, false, 2, false, false, true, 1, false, 2, 2, 0, true, true>(); }  // y L=2
 #else
-#error "no fast-table entry for VK_LEN"
+// Any other even 5-smooth length with a two-pass split R1 x R2 (R1 <= R2 <= 48):
+// the variant choices follow the measured entries above by size class
+// (lines per CTA from shared memory, twiddles from global for long lines,
+// a TMA z tile with a resident-CTA floor up to 256 points, PDL except at
+// 2160-class lengths).
+namespace gen {
+constexpr int isqrt(int n) {
+  int r = 0;
+  while ((r + 1) * (r + 1) <= n) ++r;
+  return r;
+}
+constexpr int r1(int n) {
+  for (int d = isqrt(n); d > 1; --d)
+    if (n % d == 0) return d;
+  return 1;
+}
+constexpr int N = VK_LEN, R1 = r1(N), R2 = N / R1;
+static_assert(R1 > 1 && R2 <= 48, "VK_LEN needs a two-pass split with radices <= 48");
+constexpr int LX = N <= 640 ? 8 : N <= 1280 ? 4 : 2;
+constexpr int LZ = N <= 256 ? 16 : LX;
+constexpr bool TWG = (LX == 8 && N >= 512) || N >= 1500;
+constexpr bool ZTWG = N >= 128;
+constexpr int cmin(int a, int b) { return a < b ? a : b; }
+constexpr int NTZ = (16 * R2 + 31) / 32 * 32;
+// TMA z tile: resident CTAs by shared memory, capped at 6 and at >= 56 registers per thread
+constexpr int ZFLOOR = LZ == 16 ? cmin(cmin(6, 200 * 1024 / (2 * N * 16 * 8 + (ZTWG ? 0 : N * 8))), 65536 / (NTZ * 56))
+                                : 0;
+}  // namespace gen
+#define VK_CAT2(a, b) a##b
+#define VK_CAT(a, b) VK_CAT2(a, b)
+FastEntry VK_CAT(fast_entry_, VK_LEN)() {
+  using namespace gen;
+  return make_entry<R1, R2, LX, LZ, TWG, (N <= 640), (LX <= 2 ? 2 : 1), (LX <= 4), ZTWG, (N < 128), 1, (N < 2000), 2,
+                    0, ZFLOOR, true, false>();
+}
 #endif
 
 }  // namespace vk

@@ -9,29 +9,17 @@
 
 namespace vk {
 
-// rl_fast_len.cu, one object per length
-FastEntry fast_entry_64();
-FastEntry fast_entry_96();
-FastEntry fast_entry_144();
-FastEntry fast_entry_192();
-FastEntry fast_entry_256();
-FastEntry fast_entry_288();
-FastEntry fast_entry_576();
-FastEntry fast_entry_1080();
-FastEntry fast_entry_2160();
+// rl_fast_len.cu, one object per length (fast_lengths.def)
+#define VK_FAST_LEN(n) FastEntry fast_entry_##n();
+#include "fast_lengths.def"
+#undef VK_FAST_LEN
 
 namespace {
 
 const FastEntry kTable[] = {
-    fast_entry_64(),
-    fast_entry_96(),
-    fast_entry_144(),
-    fast_entry_192(),
-    fast_entry_256(),
-    fast_entry_288(),
-    fast_entry_576(),
-    fast_entry_1080(),
-    fast_entry_2160(),
+#define VK_FAST_LEN(n) fast_entry_##n(),
+#include "fast_lengths.def"
+#undef VK_FAST_LEN
 };
 
 }  // namespace

@@ -265,6 +265,19 @@ void parallel_memcpy(void* dst, const void* src, size_t bytes) {
   });
 }
 
+// Faults in the pages of a fresh pageable output buffer (one write per page,
+// split over the pool), so the copy-out after the run does not page-fault.
+void prefault(void* dst, size_t bytes) {
+  constexpr size_t kPage = 4096, kPiece = 8 << 20;
+  HostPool& pool = HostPool::get();
+  const int n = (int)std::max<size_t>(1, std::min<size_t>((size_t)pool.size(), bytes / kPiece));
+  const size_t per = (bytes / n + kPage - 1) / kPage * kPage;
+  pool.run(n, [&](int i) {
+    volatile char* b = (volatile char*)dst;
+    for (size_t o = (size_t)i * per; o < std::min(bytes, (size_t)(i + 1) * per); o += kPage) b[o] = 0;
+  });
+}
+
 bool host_pinned(const void* p) {
   cudaPointerAttributes a{};
   if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
@@ -769,9 +782,7 @@ void z_pass_chunk(vk_rl_plan p, cudaStream_t s, const float2* otf, int kx0, int 
 // two HBM round trips per convolution; profiles/r02/kxchunk.md).
 void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   const Geom& g = p->g;
-  // per-launch profiling times each kernel with events on its stream: the
-  // profiled runs keep the chunks on one stream so kernels do not overlap
-  const int ns = p->prof ? 1 : p->kxs;
+  const int ns = p->kxs;
   if (!p->kev[0]) {
     for (int i = 0; i < p->kxs; ++i) {
       if (i) ck(cudaStreamCreateWithFlags(&p->kstream[i], cudaStreamNonBlocking), "cudaStreamCreate");
@@ -818,7 +829,9 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
     y_pass(p, s, vk::YM_CONV, nl, g.Py, g.Py, g.Py, g.Py, p->ycrop, p->SA.p, p->SA.p, otf);
     return;
   }
-  if (p->kxc) {
+  // profiled runs take the whole-volume passes: chunk launches on several
+  // streams overlap, so per-launch events could not attribute time to kernels
+  if (p->kxc && !p->prof) {
     conv_yz_chunked(p, s, otf);
     return;
   }
@@ -2449,7 +2462,16 @@ vk_status vk_rl_run(vk_rl_plan p, const float* obs, float* est, const vk_stop_ru
     if (p->obs.n < n) p->obs.alloc(n, "observed");
     if (p->out.n < n) p->out.alloc(n, "output");
     p->staging.h2d(p->obs.p, obs, n * sizeof(float), p->stream);
-    run_device(p, p->obs.p, p->out.p, rule, flat_init, trace, p->stream, true);
+    // a pageable output (e.g. a fresh array) is faulted in while the GPU runs
+    std::thread touch;
+    if (!host_pinned(est)) touch = std::thread([=] { prefault(est, n * sizeof(float)); });
+    try {
+      run_device(p, p->obs.p, p->out.p, rule, flat_init, trace, p->stream, true);
+    } catch (...) {
+      if (touch.joinable()) touch.join();
+      throw;
+    }
+    if (touch.joinable()) touch.join();
     p->staging.d2h(est, p->out.p, n * sizeof(float), p->stream);
   });
 }

@@ -625,3 +625,40 @@ def test_random_shapes_fast_z(shape, kshape):
     rf = vk.richardson_lucy(obs, psf, fixed_rule(3), True)
     itf, _ = run_oracle(obs, psf, 3, True)
     assert rel_l2(rf.estimate, itf[-1]) <= TOL_1
+
+
+def _fast_lengths():
+    import re
+    path = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "paper_2510_14143_b200", "csrc",
+                        "fast_lengths.def")
+    with open(path) as f:
+        return [int(m) for m in re.findall(r"^VK_FAST_LEN\((\d+)\)", f.read(), re.M)]
+
+
+@pytest.mark.parametrize("n", _fast_lengths())
+def test_every_fast_length_matches_generic(n):
+    """Every compile-time length of fast_lengths.def on the x and y axes (2D,
+    N x N grid) and on the z axis (3D, N x 32 x 32 grid) against the generic
+    Stockham kernels (VK_RL_GENERIC=1), 2 iterations; the smallest ones also
+    against the oracle."""
+    rng = np.random.default_rng(n)
+    rule = fixed_rule(2)
+    psf2 = O.gaussian_psf((3, 3), 0.8)
+    img = (rng.random((n - 4, n - 4)) + 0.1).astype(np.float32)
+    plan = vk.RlPlan(img.shape, psf2)
+    assert plan.fft_shape_ == (n, n) and "x:fast" in plan.describe() and "y:fast" in plan.describe(), plan.describe()
+    plan.close()
+    fast = vk.richardson_lucy(img, psf2, rule)
+    gen = _with_env({"VK_RL_GENERIC": "1"}, lambda: vk.richardson_lucy(img, psf2, rule))
+    assert rel_l2(fast.estimate, gen.estimate) <= 2e-6
+    psf3 = O.gaussian_psf((3, 3, 3), 0.8)
+    vol = (rng.random((n - 4, 28, 28)) + 0.1).astype(np.float32)
+    plan = vk.RlPlan(vol.shape, psf3)
+    assert plan.fft_shape_[0] == n and "z:fast" in plan.describe(), plan.describe()
+    plan.close()
+    fast3 = vk.richardson_lucy(vol, psf3, rule)
+    gen3 = _with_env({"VK_RL_GENERIC": "1"}, lambda: vk.richardson_lucy(vol, psf3, rule))
+    assert rel_l2(fast3.estimate, gen3.estimate) <= 2e-6
+    if n <= 128:
+        its, _ = run_oracle(vol, psf3, 2)
+        assert rel_l2(fast3.estimate, its[-1]) <= TOL_1
