@@ -49,7 +49,7 @@ FastEntry make_entry() {
   }
   if constexpr (ZTMA > 0 && LZ == 16) {
     e.ztk = (const void*)zpass_tma<R1, R2, ZTWG, ZTMA>;
-    e.smem_zt = (size_t)(2 * R1 * R2 * 16 + (ZTWG ? 0 : R1 * R2)) * sizeof(float2);  // tile + OTF tile
+    e.smem_zt = (size_t)(2 * R1 * R2 * 16 + (ZTWG ? 0 : (R1 * R2 + 15) / 16 * 16)) * sizeof(float2);  // twiddles + tile + OTF tile
     e.smem_zt_half = e.smem_zt + (size_t)R1 * R2 * (kHalfBox - 16) * sizeof(float2);  // 18-wide half-OTF tile
   }
   return e;

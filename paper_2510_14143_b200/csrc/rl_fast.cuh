@@ -745,7 +745,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   const float2* const otf = ta.z.otf;
   extern __shared__ __align__(128) float2 smem[];
   float2* tw = TWG ? nullptr : smem;
-  float2* A = TWG ? smem : smem + N;  // dense [z][16]; N*16*8 B, 128-B aligned (N multiple of 8)
+  float2* A = TWG ? smem : smem + (N + 15) / 16 * 16;  // dense [z][16], 128-B aligned (TMA destination)
   float2* O = A + N * L;              // OTF tile [kz][16] (half OTF: [kz][kHalfBox]) when ta.otf_tma
   __shared__ uint64_t bar, obar;
   const bool otma = ta.otf_tma != 0;

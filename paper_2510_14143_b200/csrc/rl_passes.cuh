@@ -112,6 +112,13 @@ struct ZArgs {
 
 __device__ __forceinline__ int clampi(int v, int lo, int hi) { return v < lo ? lo : (v > hi ? hi : v); }
 
+// Interleaved line pitch of the generic kernels: L + 1 (conflict-free
+// transposed staging), except one line per CTA (long lines), which needs no
+// pad -- that halves the shared memory of the longest lines, so the generic
+// path plans axes up to ~14k points (the paper's own volume, W = 90 x 6480 x
+// 7680 with a PSF as large as the image).
+__host__ __device__ __forceinline__ int line_pitch(int L) { return L == 1 ? 1 : L + 1; }
+
 // Deterministic sums.  Every block writes its N partial sums (a fixed
 // shuffle tree, then warp 0 over the warps in order) to dst[0..N) -- no
 // atomics -- and reduce_partials_kernel / reduce_iter_partials_kernel add the
@@ -197,7 +204,7 @@ __device__ __forceinline__ void x_forward_store(float2* in, float2* tmp, const X
 
 __global__ void __launch_bounds__(256) xpass_kernel(const XArgs a) {
   extern __shared__ float2 smem[];
-  const int L = a.L, LP = L + 1, Wx = a.g.Wx, Hx = a.g.Hx;
+  const int L = a.L, LP = line_pitch(L), Wx = a.g.Wx, Hx = a.g.Hx;
   float2* A = smem;
   float2* B = smem + Wx * LP;  // B also stages Hx*2L (host sizes it as max of both)
   const int z = blockIdx.y + a.zoff;
@@ -313,7 +320,7 @@ __global__ void __launch_bounds__(256) xpass_kernel(const XArgs a) {
 
 __global__ void __launch_bounds__(256) ypass_kernel(const YArgs a) {
   extern __shared__ float2 smem[];
-  const int L = a.L, LP = L + 1, N = a.plan.n;
+  const int L = a.L, LP = line_pitch(L), N = a.plan.n;
   float2* A = smem;
   float2* B = smem + N * LP;
   const int line0 = blockIdx.x * L;
@@ -349,7 +356,7 @@ __global__ void __launch_bounds__(256) ypass_kernel(const YArgs a) {
 
 __global__ void __launch_bounds__(256) zpass_kernel(const ZArgs a) {
   extern __shared__ float2 smem[];
-  const int L = a.L, LP = L + 1, N = a.plan.n;
+  const int L = a.L, LP = line_pitch(L), N = a.plan.n;
   float2* A = smem;
   float2* B = smem + N * LP;
   const int kx = blockIdx.y;

@@ -173,10 +173,10 @@ int pick_lines(int n, int lmax, size_t cap, size_t (*bytes)(int n, int L)) {
   return L;
 }
 size_t x_smem(int Wx, int L) {
-  const size_t LP = L + 1, Hx = Wx / 2 + 1;
+  const size_t LP = vk::line_pitch(L), Hx = Wx / 2 + 1;
   return (Wx * LP + std::max<size_t>(Wx * LP, 2 * L * Hx)) * sizeof(float2);
 }
-size_t yz_smem(int N, int L) { return 2 * (size_t)N * (L + 1) * sizeof(float2); }
+size_t yz_smem(int N, int L) { return 2 * (size_t)N * vk::line_pitch(L) * sizeof(float2); }
 
 // ---- host staging -----------------------------------------------------------
 // Host-pointer calls (vk_rl_run, vk_rl_step, vk_conv_run, the batch form)

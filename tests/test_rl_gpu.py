@@ -662,3 +662,24 @@ def test_every_fast_length_matches_generic(n):
     if n <= 128:
         its, _ = run_oracle(vol, psf3, 2)
         assert rel_l2(fast3.estimate, its[-1]) <= TOL_1
+
+
+@pytest.mark.parametrize("shape,kshape,W", [((2560,), (2561,), (7680,)), ((6, 2560), (3, 2561), (10, 7680)),
+                                            ((3, 4, 4500), (3, 3, 3), (8, 8, 4608)),
+                                            ((2, 5520, 5), (1, 481, 3), (2, 6480, 9))])
+def test_long_axes_generic(shape, kshape, W):
+    """Axes beyond the compile-time lengths run on the generic Stockham kernels
+    with one unpadded line per CTA, up to ~14k points: the x length of the
+    paper's own volume (image and PSF both 30x2160x2560 ->
+    W = 90 x 6480 x 7680) and the y length 6480, against the oracle."""
+    rng = np.random.default_rng(len(shape))
+    psf = rng.random(kshape) + 0.1
+    psf = (psf / psf.sum()).astype(np.float32)
+    obs = (rng.random(shape) + 0.1).astype(np.float32)
+    plan = vk.RlPlan(shape, psf)
+    assert plan.fft_shape_ == W, plan.fft_shape_
+    plan.close()
+    its, t = run_oracle(obs, psf, 3)
+    got = vk.richardson_lucy(obs, psf, fixed_rule(3))
+    assert tuple(got.trace.fft_shape) == tuple(t.fft_shape)
+    assert rel_l2(got.estimate, its[-1]) <= TOL_1
