@@ -232,11 +232,16 @@ def test_kx_chunked_conv_matches_whole_volume(name, shape, mk):
         assert np.array_equal(got.estimate, whole.estimate), env
         plan = _with_env(env, lambda: vk.RlPlan(shape, psf))
         assert "kx-chunks(" in plan.describe(), plan.describe()
-        plan.profile(True)
         plan.run(obs, rule)
-        prof = plan.profile_read()
-        assert prof["z_conv"][1] > 2 * 3, prof  # several chunk launches per convolution
+        chunked_launches = plan.launches()
+        plan.profile(True)  # profiled runs take the whole-volume passes (events cannot split overlapping chunks)
+        assert np.array_equal(plan.run(obs, rule).estimate, whole.estimate)
+        plan.profile(False)
         plan.close()
+        wplan = _with_env({"VK_RL_KXCHUNK": "0"}, lambda: vk.RlPlan(shape, psf))
+        wplan.run(obs, rule)
+        assert chunked_launches > wplan.launches()  # several chunk launches per convolution
+        wplan.close()
     its, _ = run_oracle(obs, psf, 1)
     r1 = vk.richardson_lucy(obs, psf, fixed_rule(1))
     assert rel_l2(r1.estimate, its[0]) <= TOL_1
