@@ -688,3 +688,18 @@ def test_long_axes_generic(shape, kshape, W):
     got = vk.richardson_lucy(obs, psf, fixed_rule(3))
     assert tuple(got.trace.fft_shape) == tuple(t.fft_shape)
     assert rel_l2(got.estimate, its[-1]) <= TOL_1
+
+
+def test_device_side_stopping_with_kx_chunks():
+    """The graph capture follows the kx-chunked convolution's streams (fork /
+    join events become graph edges): same run as the host-driven loop."""
+    psf = O.widefield_psf(15)
+    obs = synth.blurred(synth.blobs((40, 100, 96), 12, 4, 7, seed=22), psf)
+    rule = vk.StoppingRule("si_psnr_vs_input", 3e-3, 2, 30)
+    env = {"VK_RL_KXCHUNK": "1", "VK_RL_KXSTREAMS": "3"}
+    assert "kx-chunks(" in _with_env(env, lambda: vk.RlPlan(obs.shape, psf)).describe()
+    dev = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule))
+    host = _with_env(dict(env, VK_RL_NO_GRAPH="1"), lambda: vk.richardson_lucy(obs, psf, rule))
+    assert len(dev.trace.records) == len(host.trace.records) < 30
+    assert dev.trace.stop_reason == host.trace.stop_reason == "converged"
+    assert np.array_equal(dev.estimate, host.estimate)
