@@ -23,7 +23,10 @@ FastEntry fast_entry_256() { return make_entry<16, 16, 16, 16, false, true, 1, f
 #elif VK_LEN == 288
 // 288: TMA-staged x pass (C1 x passes 0.0730 vs 0.0753 ms per iteration; at
 // 576 it loses: profiles/r01/final/xtma.log)
-FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 1, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
+// x pass with a 3-CTA register floor: the packed complex arithmetic took the
+// staged kernel from 72 to 75 registers, i.e. from 3 to 2 resident CTAs
+// (C1 x passes +13%, profiles/r02/final)
+FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 3, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
 #elif VK_LEN == 576
 FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(); }  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
 #elif VK_LEN == 1080
