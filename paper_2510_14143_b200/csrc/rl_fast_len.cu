@@ -28,7 +28,13 @@ FastEntry fast_entry_256() { return make_entry<16, 16, 16, 16, false, true, 1, f
 // (C1 x passes +13%, profiles/r02/final)
 FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 3, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
 #elif VK_LEN == 576
+#if defined(VK_X576_VARIANT) && VK_X576_VARIANT == 1  // experiment: 16-line x pass (32 rows, 256-byte pieces), 2 CTAs/SM
+FastEntry fast_entry_576() { return make_entry<24, 24, 16, 8, true, true, 2, false, false, true, 1, true, 2, 8, 0, true>(); }
+#elif defined(VK_X576_VARIANT) && VK_X576_VARIANT == 2  // the same with TMA-staged spectrum rows
+FastEntry fast_entry_576() { return make_entry<24, 24, 16, 8, true, true, 2, false, false, true, 1, true, 2, 8, 0, true, true>(); }
+#else
 FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(); }  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
+#endif
 #elif VK_LEN == 1080
 // 1080: TMA-staged x pass with a 2-CTA register floor (96 regs, 80 B stack;
 // without the floor the staged loads take 129 registers and 1 CTA/SM): C4
