@@ -96,7 +96,8 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
     if not variant and not force and up_to_date():
         return LIB
     os.makedirs(os.path.dirname(lib), exist_ok=True)
-    objdir = os.path.join(ROOT, "build", "obj" + ("_" + variant if variant else ""))
+    # side builds keep their objects out of the tree (the GPU snapshot is size-capped)
+    objdir = os.path.join("/tmp", "vk_build_obj_" + variant) if variant else os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra_flags)
 
