@@ -394,9 +394,6 @@ struct vk_rl_plan_s {
   // y-forward -> z -> y-inverse through a ring slot (one per stream) small
   // enough to stay L2-resident, so S_B does not make HBM round trips
   int kxc = 0, kxs = 2;  // planes per chunk, streams (= ring slots)
-  // z-chunked y-inverse -> x -> y-forward (zx_half): chunks of zxc z rows on
-  // zxs streams, so S_A rows stay in L2 between the y and x passes
-  int zxc = 0, zxs = 2;
   size_t ring_window = 0;  // bytes of ring2 under a persisting L2 access window (0: none)
   DevBuf<float2> ring2;
   CUtensorMap zmap_ring[4]{};
@@ -825,7 +822,7 @@ void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
 // 'same' linear convolution of the x-transformed P-domain field held in SA
 // with `otf` (deconv.cpp:135-147 minus the x transforms, which live in the
 // fused X-pass).  Result back in SA.
-void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf, bool sb_ready = false) {
+void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   const Geom& g = p->g;
   const int nl = g.Hx * g.Pz;
   if (g.Wz == 1) {
@@ -838,62 +835,9 @@ void conv_yz(vk_rl_plan p, cudaStream_t s, const float2* otf, bool sb_ready = fa
     conv_yz_chunked(p, s, otf);
     return;
   }
-  if (!sb_ready) y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
+  y_pass(p, s, vk::YM_FWD, nl, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
   z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
   y_pass(p, s, vk::YM_INV, nl, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr);
-}
-
-// The z-chunked half iteration (zxc > 0): the whole-volume z convolution,
-// then per chunk of zxc z rows y-inverse -> x pass (xmode) -> y-forward
-// (skipped when !fwd_after), chunk d on stream d mod zxs.  The x pass then
-// reads its S_A rows from L2, where the chunk's y-inverse just wrote them,
-// instead of fetching 128-byte pieces from DRAM.
-void zx_half(vk_rl_plan p, cudaStream_t s, const float2* otf, int xmode, const float* d_obs, int it, float* d_out,
-             bool fwd_after) {
-  const Geom& g = p->g;
-  z_pass(p, s, vk::ZM_CONV, g.Pz, g.Pz, g.Pz, g.cz, p->SB.p, otf, nullptr);
-  const int ns = p->zxs;
-  if (!p->kev[0]) {
-    for (int i = 0; i < ns; ++i) {
-      if (i) ck(cudaStreamCreateWithFlags(&p->kstream[i], cudaStreamNonBlocking), "cudaStreamCreate");
-      ck(cudaEventCreateWithFlags(&p->kev[i], cudaEventDisableTiming), "event");
-    }
-  }
-  ck(cudaEventRecord(p->kev[0], s), "event");
-  for (int i = 1; i < ns; ++i) ck(cudaStreamWaitEvent(p->kstream[i], p->kev[0], 0), "wait");
-  int c = 0;
-  for (int z0 = 0; z0 < g.Pz; z0 += p->zxc, ++c) {
-    const int zn = std::min(p->zxc, g.Pz - z0);
-    cudaStream_t cs = c % ns ? p->kstream[c % ns] : s;
-    y_pass(p, cs, vk::YM_INV, g.Hx * zn, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, p->SB.p, p->SA.p, nullptr, z0, zn, g.Pz);
-    x_pass(p, cs, xmode, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, d_out, 0, z0, zn);
-    if (fwd_after)
-      y_pass(p, cs, vk::YM_FWD, g.Hx * zn, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr, z0, zn, g.Pz);
-  }
-  for (int i = 1; i < ns; ++i) {
-    ck(cudaEventRecord(p->kev[i], p->kstream[i]), "event");
-    ck(cudaStreamWaitEvent(s, p->kev[i], 0), "wait");
-  }
-}
-
-// One RL iteration's passes (deconv.cpp:360-398): forward convolution, ratio x
-// pass, correlation, update x pass.  it: the sums slot; last: the update
-// writes the cropped output (d_out) instead of the estimate's spectrum.
-void iteration(vk_rl_plan p, cudaStream_t s, const float* d_obs, int it, bool last, float* d_out) {
-  const Geom& g = p->g;
-  if (p->zxc && !p->prof) {  // S_B already holds y-forward(estimate) (prologue / previous iteration)
-    zx_half(p, s, p->otf.p, vk::XM_RATIO, d_obs, it, nullptr, true);
-    zx_half(p, s, p->otf_flip.p, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, d_obs, it, last ? d_out : nullptr,
-            !last);
-    return;
-  }
-  conv_yz(p, s, p->otf.p, p->zxc != 0);  // zx plans keep S_B = y-forward(estimate) between iterations
-  x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, nullptr);
-  conv_yz(p, s, p->otf_flip.p);
-  x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it,
-         last ? d_out : nullptr);
-  if (p->zxc && !last)  // keep the zx invariant: S_B = y-forward(estimate) between iterations
-    y_pass(p, s, vk::YM_FWD, g.Hx * g.Pz, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
 }
 
 // Full r2c spectrum [Hx][Wz][Wy] of a real block [rz][ry][rx] corner-embedded
@@ -1422,12 +1366,7 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     // on 2 streams where S_B does not fit L2 anyway (> 64 MB): C2 +6.5%, C4
     // +1.5%, chunk/stream sweep in profiles/r02/kxchunk.md; small volumes
     // (C1/C3, S_B 26 MB) keep the whole-volume passes.
-    if (const char* zx = std::getenv("VK_RL_ZXCHUNK"); zx && !conv && !zslab && g.Wz > 1 && p->fx && p->fy) {
-      const int rows = std::atoi(zx);
-      p->zxc = rows > 0 && rows < g.Pz ? rows : 0;
-      if (const char* zs = std::getenv("VK_RL_ZXSTREAMS")) p->zxs = std::max(1, std::min(4, std::atoi(zs)));
-    }
-    if (p->ztma && !conv && !zslab && !p->zxc) {
+    if (p->ztma && !conv && !zslab) {
       const char* kc = std::getenv("VK_RL_KXCHUNK");
       const double sb_mb = (double)g.Hx * g.Pz * g.Wy * 8 / 1e6;
       const double mb = kc ? std::atof(kc) : (sb_mb > 64.0 ? 20.0 : 0.0);
@@ -1876,8 +1815,11 @@ void run_graph_loop(vk_rl_plan p, cudaStream_t s, const float* d_obs, const vk_s
     ck(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal), "capture");
     t_capturing = true;
     try {
+      conv_yz(p, s, p->otf.p);
       // every iteration's partials in slot 0: the rule kernel reduces them before the next
-      iteration(p, s, d_obs, 1, false, nullptr);
+      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
+      conv_yz(p, s, p->otf_flip.p);
+      x_pass(p, s, vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
       if (frc) {
         frc_bins_enqueue(p, s);
         vk::frc_value_kernel<<<1, 32, 0, s>>>(p->frc_bins.p, p->frc_nbins, p->frc_binf, spacing, p->gmetric.p);
@@ -2004,8 +1946,6 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
   x_pass(p, s, vk::XM_FWD, p->est.p, g.Pz, g.Py, g.Px, 1.0f, nullptr, nullptr, 0, nullptr,
          p->fx ? g.cx : 0);
-  if (p->zxc)  // the z-chunked schedule enters each iteration at the z convolution
-    y_pass(p, s, vk::YM_FWD, g.Hx * g.Pz, g.Py, g.Py, g.Wy, g.Wy, 0, p->SA.p, p->SB.p, nullptr);
 
   // Early stop is only possible from iteration patience+1 on (fails counts
   // from iteration 2); before that no host round-trip is needed.
@@ -2028,7 +1968,11 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
     // the last iteration writes the cropped output directly unless a metric
     // still needs the updated estimate
     const bool last = it == iters && !frc && !ssim;
-    iteration(p, s, d_obs, it, last, d_out);
+    conv_yz(p, s, p->otf.p);
+    x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, it, nullptr);
+    conv_yz(p, s, p->otf_flip.p);
+    x_pass(p, s, last ? vk::XM_UPDATE_LAST : vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs,
+           it, last ? d_out : nullptr);
     if (frc) values.push_back(frc_eval(p, s, spacing));  // syncs: the value is needed on the host
     if (ssim) ssim_eval(p, s, it, d_obs);
     ck(cudaEventRecord(p->events[it], s), "event");
@@ -2422,10 +2366,9 @@ vk_status vk_rl_plan_describe(vk_rl_plan p, char* buf, int len) {
                     " P=" + std::to_string(g.Pz) + "x" + std::to_string(g.Py) + "x" + std::to_string(g.Px) + " " +
                     axis("x", p->fx, p->fx ? p->fx->Lx : p->xL) + " " + axis("y", p->fy, p->fy ? p->fy->Ly : p->yL) +
                     " " + axis("z", p->fz, p->fz ? p->fz->Lz : p->zL) + " yz:";
-    s += p->zxc   ? "zx-chunks(" + std::to_string(p->zxc) + "x" + std::to_string(p->zxs) + ")"
-         : p->kxc ? "kx-chunks(" + std::to_string(p->kxc) + "x" + std::to_string(p->kxs) +
-                        (p->ring_window ? ",l2persist" : "") + ")"
-                  : g.Wz > 1 ? "3-pass" : "y-conv";
+    s += p->kxc ? "kx-chunks(" + std::to_string(p->kxc) + "x" + std::to_string(p->kxs) +
+                      (p->ring_window ? ",l2persist" : "") + ")"
+                : g.Wz > 1 ? "3-pass" : "y-conv";
     if (p->ztma) s += " z:tma";
     if (p->ofactored) s += " otf:factored";
     if (p->ohalf) s += " otf:half";

@@ -703,27 +703,3 @@ def test_device_side_stopping_with_kx_chunks():
     assert len(dev.trace.records) == len(host.trace.records) < 30
     assert dev.trace.stop_reason == host.trace.stop_reason == "converged"
     assert np.array_equal(dev.estimate, host.estimate)
-
-
-@pytest.mark.parametrize("env", [{"VK_RL_ZXCHUNK": "12"}, {"VK_RL_ZXCHUNK": "7", "VK_RL_ZXSTREAMS": "3"}])
-def test_zx_chunked_schedule_matches_default(env):
-    """The z-chunked y-inverse -> x -> y-forward schedule (VK_RL_ZXCHUNK rows,
-    chunks on VK_RL_ZXSTREAMS streams): same kernels on row ranges, so the
-    estimate, LL and metric agree bitwise with the whole-volume passes; also
-    under device-side stopping, flat_init and a profiled run."""
-    psf = O.widefield_psf(15)
-    obs = synth.blurred(synth.blobs((40, 100, 96), 12, 4, 7, seed=23), psf)
-    base = {"VK_RL_KXCHUNK": "0"}
-    for rule, flat in ((fixed_rule(4), False), (vk.StoppingRule("si_psnr_vs_input", 3e-3, 2, 30), True)):
-        ref = _with_env(base, lambda: vk.richardson_lucy(obs, psf, rule, flat))
-        got = _with_env(env, lambda: vk.richardson_lucy(obs, psf, rule, flat))
-        assert np.array_equal(got.estimate, ref.estimate)
-        assert [r.value for r in got.trace.records] == [r.value for r in ref.trace.records]
-        assert list(got.trace.log_likelihood) == list(ref.trace.log_likelihood)
-    plan = _with_env(env, lambda: vk.RlPlan(obs.shape, psf))
-    assert "zx-chunks(" in plan.describe(), plan.describe()
-    plan.profile(True)
-    r = plan.run(obs, fixed_rule(4))
-    plan.profile(False)
-    assert np.array_equal(r.estimate, _with_env(base, lambda: vk.richardson_lucy(obs, psf, fixed_rule(4))).estimate)
-    plan.close()
