@@ -33,11 +33,7 @@ FastEntry fast_entry_576() { return make_entry<24, 24, 16, 8, true, true, 2, fal
 #elif defined(VK_X576_VARIANT) && VK_X576_VARIANT == 2  // the same with TMA-staged spectrum rows
 FastEntry fast_entry_576() { return make_entry<24, 24, 16, 8, true, true, 2, false, false, true, 1, true, 2, 8, 0, true, true>(); }
 #else
-#if defined(VK_X576_TMA)  // experiment: TMA-staged x variant available (VK_RL_XTMA_MODES picks the passes)
-FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true, true>(); }
-#else
 FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, false, false, true, 1, true, 2, 0, 0, true>(); }  // 576: global twiddles -> 5 x/y CTAs/SM (y L=4: slower); y bulk copies
-#endif
 #endif
 #elif VK_LEN == 1080
 // 1080: TMA-staged x pass with a 2-CTA register floor (96 regs, 80 B stack;

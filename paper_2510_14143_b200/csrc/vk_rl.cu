@@ -386,7 +386,6 @@ struct vk_rl_plan_s {
   int xpf = 0;  // x-pass L2 prefetch mask (XArgs::pf)
   int ycrop = 0;
   bool xtma = false;  // xpass_tma for the RATIO/UPDATE x passes (S_A rows staged by TMA)
-  int xtma_modes = 3;  // which of them (bit 0 RATIO, bit 1 UPDATE; VK_RL_XTMA_MODES)
   CUtensorMap xmap{};
   int xtbk = 0, xtnb = 0;  // crop offset of the y inverse: g.cy, or 0 when folded into the OTFs as a ramp
   bool tma_store = true;  // TMA/bulk stores of the z tile and y-forward lines (VK_RL_NO_TMA_STORE=1: thread stores)  // S_A kx-blocked by 1 << blk_lb (= the y pass's lines per CTA); 0: [Hx][Pz][Py]
@@ -637,9 +636,7 @@ void x_pass(vk_rl_plan p, cudaStream_t s, int mode, const float* src, int rows_z
   dim3 grid((rows_y + 2 * a.L - 1) / (2 * a.L), nz < 0 ? rows_z : nz);
   const int kind = mode == vk::XM_FWD ? VK_KIND_X_FWD : mode == vk::XM_RATIO ? VK_KIND_X_RATIO : VK_KIND_X_UPDATE;
   const size_t t = prof_begin(p, s);
-  // xtma_modes: bit 0 the RATIO pass, bit 1 the UPDATE passes take the TMA-staged kernel
-  const int mbit = mode == vk::XM_RATIO ? 1 : 2;
-  if (p->fx && p->xtma && mode != vk::XM_FWD && (p->xtma_modes & mbit)) {
+  if (p->fx && p->xtma && mode != vk::XM_FWD) {
     vk::XTmaArgs ta{};
     ta.map = p->xmap;
     a.tbk = p->xtbk;
@@ -1349,7 +1346,6 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     if (p->fx && p->fx->xtk) {
       const char* nx = std::getenv("VK_RL_NO_XTMA");
       p->xtma = !(nx && nx[0] == '1') && encode_xmap(p);
-      if (const char* xm = std::getenv("VK_RL_XTMA_MODES")) p->xtma_modes = std::atoi(xm);
     }
     if (g.Wz > 1) p->SB.alloc(sb, "spectrum B");
     // TMA-staged z tile (zpass_tma) where the length has one and the box
