@@ -19,7 +19,9 @@
  *    overlapping the DMA of the previous one.
  *  - Every function returns a vk_status.  On failure vk_last_error() returns
  *    the exact message the reference would put in the exception's what()
- *    (thread-local, valid until the next call on the same thread).
+ *    (thread-local, valid until the next call on the same thread), and the
+ *    contents of output buffers are unspecified (a pageable output may have
+ *    been faulted in, i.e. zeroed, while the run was in flight).
  *  - A plan is not re-entrant (one run at a time, like RlTransforms,
  *    deconv.hpp:64-65); distinct plans may be used concurrently.
  */
