@@ -92,3 +92,25 @@ def test_bench_roofline_groups_kinds_by_kernel():
     assert k["xpass"]["bytes"] == 10 * 500 + 10 * 900 and k["xpass"]["ms"] == 30.0
     assert abs(k["xpass"]["gbs"] - (14000 / 0.030) / 1e9) < 1e-12
     assert k["zpass"]["otf_bytes"] == 20 * 256 and k["zpass"]["bytes"] == 20 * 400
+
+
+def test_bench_config_records_match_the_reference_rules():
+    """Both bench arms print the same config dict; its fft_shape / padded
+    domain follow the reference's rules (deconv.cpp:114-116, 210-219) and
+    SURVEY.md §8(a0)."""
+    import importlib.util
+    import os
+
+    spec = importlib.util.spec_from_file_location(
+        "bench", os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    for n in list(range(0, 300)) + [2077, 6479, 7679]:
+        assert bench.good_size(n) == O.good_size(n)
+    want = {"c1": ([78, 270, 270], [96, 288, 288]), "c2": ([158, 542, 542], [192, 576, 576]),
+            "c4": ([120, 1020, 1020], [144, 1080, 1080]), "c5": ([2078, 2078], [2160, 2160])}
+    for name, (padded, fft) in want.items():
+        cfg = bench.CONFIGS[name]
+        d = bench.config_dict(cfg, 1, cfg.get("volumes", 0))
+        assert d["padded_domain"] == padded and d["fft_shape"] == fft
+        assert d == bench.config_dict(cfg, 1, cfg.get("volumes", 0))
