@@ -241,10 +241,14 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
       const float2* Sb = a.S + ((unsigned)z * g.Py + (vb ? yb : 0));
       const unsigned plane = (unsigned)g.Pz * g.Py;
       const bool vec = (g.Py & 1) == 0;  // then vb == va (ya even)
-      for (int kx0 = group_remap<L>(threadIdx.x / L, KS); kx0 < Hx; kx0 += KS * U) {
-        float2 xa[U], xb[U];
+#ifndef VK_XLOAD_U
+#define VK_XLOAD_U 4
+#endif
+      constexpr int UL = VK_XLOAD_U;  // spectrum loads in flight per thread
+      for (int kx0 = group_remap<L>(threadIdx.x / L, KS); kx0 < Hx; kx0 += KS * UL) {
+        float2 xa[UL], xb[UL];
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < UL; ++u) {
           const int kx = kx0 + u * KS;
           const bool ok = kx < Hx;
           if (vec) {  // rows 2l, 2l+1 adjacent and 16-byte aligned: one load
@@ -258,7 +262,7 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
           }
         }
 #pragma unroll
-        for (int u = 0; u < U; ++u) {
+        for (int u = 0; u < UL; ++u) {
           const int kx = kx0 + u * KS;
           if (kx >= Hx) break;
           if (kx == 0 || 2 * kx == N) {
