@@ -242,9 +242,9 @@ __device__ __forceinline__ void xpass_body(const XArgs& a, const CUtensorMap* xm
       const unsigned plane = (unsigned)g.Pz * g.Py;
       const bool vec = (g.Py & 1) == 0;  // then vb == va (ya even)
 #ifndef VK_XLOAD_U
-#define VK_XLOAD_U 4
+#define VK_XLOAD_U 6  // C2 x passes -1.8% vs 4 (and no spill at 576); 8 / 12: -2.0% / +-0
 #endif
-      constexpr int UL = VK_XLOAD_U;  // spectrum loads in flight per thread
+      constexpr int UL = VK_XLOAD_U;  // spectrum loads in flight per thread (profiles/r02/xload_u_ab.txt)
       for (int kx0 = group_remap<L>(threadIdx.x / L, KS); kx0 < Hx; kx0 += KS * UL) {
         float2 xa[UL], xb[UL];
 #pragma unroll

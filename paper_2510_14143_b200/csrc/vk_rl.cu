@@ -2341,7 +2341,8 @@ vk_status vk_rl_plan_device_bytes(vk_rl_plan p, uint64_t* bytes) {
     if (!p || !bytes) fail(VK_ERR_ARG, "NULL argument");
     *bytes = (p->SA.n + p->SB.n + p->otf.n + p->otf_flip.n + p->ofac.n) * sizeof(float2) +
              (p->est.n + p->obs.n + p->out.n) * sizeof(float) + p->acc.n * sizeof(double) +
-             p->ring2.n * sizeof(float2) + (p->ss_img[0].n + p->ss_img[1].n) * sizeof(float) +
+             p->ring2.n * sizeof(float2) + (p->xpart.n + p->part.n) * sizeof(double) +
+             (p->ss_img[0].n + p->ss_img[1].n) * sizeof(float) +
              (p->ss_f[0].n + p->ss_f[1].n + p->ss_sum.n) * sizeof(double) +
              (p->frc_even.n + p->frc_odd.n) * sizeof(float);
     if (p->frc) *bytes += (p->frc->SA.n + p->frc->SB.n + p->frc->otf.n + p->frc->otf_flip.n) * sizeof(float2);
