@@ -55,10 +55,10 @@ def sources():
                   if f.endswith((".cu", ".cpp")) and f != "rl_fast_len.cu")
 
 
-def units():
+def units(lengths=FAST_LENGTHS):
     """(source, extra flags, object name) for every object of the library."""
     u = [(src, [], os.path.splitext(os.path.basename(src))[0] + ".o") for src in sources()]
-    u += [(os.path.join(CSRC, "rl_fast_len.cu"), [f"-DVK_LEN={n}"], f"rl_fast_len_{n}.o") for n in FAST_LENGTHS]
+    u += [(os.path.join(CSRC, "rl_fast_len.cu"), [f"-DVK_LEN={n}"], f"rl_fast_len_{n}.o") for n in lengths]
     return u
 
 
@@ -89,9 +89,11 @@ def build_cli(verbose: bool = False) -> str:
     return CLI
 
 
-def build(force: bool = False, verbose: bool = False, variant: str = "", extra_flags=()) -> str:
+def build(force: bool = False, verbose: bool = False, variant: str = "", extra_flags=(), lengths=None) -> str:
     """variant: a side build (lib/<variant>/libvkrl.so, own objects) with
-    extra_flags, for A/B measurements (load it with VK_RL_LIB=...)."""
+    extra_flags, for A/B measurements (load it with VK_RL_LIB=...); lengths:
+    only these compile-time lengths (the others take the generic kernels),
+    which keeps side libraries small enough for the size-capped snapshot."""
     lib = os.path.join(LIBDIR, variant, "libvkrl.so") if variant else LIB
     if not variant and not force and up_to_date():
         return LIB
@@ -100,6 +102,13 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
     objdir = os.path.join("/tmp", "vk_build_obj_" + variant) if variant else os.path.join(ROOT, "build", "obj")
     os.makedirs(objdir, exist_ok=True)
     compile_flags = [f for f in NVCC_FLAGS if f != "-shared"] + list(extra_flags)
+    if lengths:
+        assert variant, "a length subset is for side builds only"
+        deff = os.path.join(objdir, "fast_lengths.def")
+        with open(deff, "w") as f:
+            f.writelines(f"VK_FAST_LEN({n})\n" for n in lengths)
+        compile_flags.append(f'-DVK_FAST_LENGTHS_DEF="{deff}"')
+    lens = tuple(lengths) if lengths else FAST_LENGTHS
 
     headers = [os.path.join(CSRC, f) for f in os.listdir(CSRC) if f.endswith((".cuh", ".h", ".def"))] + [
         os.path.join(ROOT, "include", h) for h in ("vk_rl.h", "vk_io.h")]
@@ -119,7 +128,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
 
     # the per-length kernels dominate the build: compile every object at once
     with ThreadPoolExecutor(max_workers=max(1, os.cpu_count() or 1)) as ex:
-        results = list(ex.map(compile_one, units()))
+        results = list(ex.map(compile_one, units(lens)))
     for cmd, r in results:
         if cmd is None:
             continue
@@ -131,7 +140,7 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
             print(r.stderr)
     tmp = lib + ".tmp"
     cmd = [_nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp,
-           *[os.path.join(objdir, u[2]) for u in units()]]
+           *[os.path.join(objdir, u[2]) for u in units(lens)]]
     if verbose:
         print(" ".join(cmd))
     r = subprocess.run(cmd, capture_output=True, text=True)
@@ -147,6 +156,12 @@ def build(force: bool = False, verbose: bool = False, variant: str = "", extra_f
 if __name__ == "__main__":
     if "--variant" in sys.argv:  # python -m paper_2510_14143_b200.build --variant NAME -DFLAG=1 ...
         i = sys.argv.index("--variant")
-        print(build(verbose=False, variant=sys.argv[i + 1], extra_flags=sys.argv[i + 2:]))
+        rest = sys.argv[i + 2:]
+        lens = None
+        if "--lengths" in rest:  # --lengths 2160,1080
+            j = rest.index("--lengths")
+            lens = [int(n) for n in rest[j + 1].split(",")]
+            rest = rest[:j] + rest[j + 2:]
+        print(build(verbose=False, variant=sys.argv[i + 1], extra_flags=rest, lengths=lens))
     else:
         print(build(force="--force" in sys.argv, verbose=True))

@@ -7,18 +7,23 @@
 #include "fast_table.h"
 #include "rl_fast.cuh"
 
+// Side builds for A/B runs may list a subset of lengths (build.py --lengths)
+#ifndef VK_FAST_LENGTHS_DEF
+#define VK_FAST_LENGTHS_DEF "fast_lengths.def"
+#endif
+
 namespace vk {
 
 // rl_fast_len.cu, one object per length (fast_lengths.def)
 #define VK_FAST_LEN(n) FastEntry fast_entry_##n();
-#include "fast_lengths.def"
+#include VK_FAST_LENGTHS_DEF
 #undef VK_FAST_LEN
 
 namespace {
 
 const FastEntry kTable[] = {
 #define VK_FAST_LEN(n) fast_entry_##n(),
-#include "fast_lengths.def"
+#include VK_FAST_LENGTHS_DEF
 #undef VK_FAST_LEN
 };
 

@@ -166,6 +166,16 @@ std::vector<float2> twiddles(int n) {
   return t;
 }
 
+// Butterfly-major pass-2 twiddles of a fast length (reg::load_twiddles2
+// layout) from its natural table tw[m] = w_N^m.
+std::vector<float2> fast_twiddles(const vk::FastEntry* e, const std::vector<float2>& tw) {
+  const int R1 = e->R1, R2 = e->N / R1;
+  std::vector<float2> t((size_t)R1 * R2);
+  for (int j = 0; j < R1; ++j)
+    for (int r = 0; r < R2; ++r) t[(size_t)j * R2 + r] = tw[(size_t)r * j];
+  return t;
+}
+
 // Largest power-of-two line count (<= lmax) whose ping-pong smem fits `cap`.
 int pick_lines(int n, int lmax, size_t cap, size_t (*bytes)(int n, int L)) {
   int L = lmax;
@@ -201,18 +211,20 @@ class HostPool {
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
+    // `grp` lives on this frame: the count drops under the mutex so the
+    // caller cannot see zero, return and destroy it while the last worker is
+    // still about to touch the mutex / condition variable (a lock-free
+    // decrement followed by lock + notify crashed sporadically)
     struct Group {
-      std::atomic<int> left;
+      int left;
       std::mutex m;
       std::condition_variable cv;
     } grp;
     grp.left = n;
     auto one = [&](int i) {
       f(i);
-      if (grp.left.fetch_sub(1) == 1) {
-        std::lock_guard<std::mutex> g(grp.m);
-        grp.cv.notify_all();
-      }
+      std::lock_guard<std::mutex> g(grp.m);
+      if (--grp.left == 0) grp.cv.notify_all();
     };
     {
       std::lock_guard<std::mutex> g(mu_);
@@ -221,7 +233,7 @@ class HostPool {
     cv_.notify_all();
     one(0);
     std::unique_lock<std::mutex> g(grp.m);
-    grp.cv.wait(g, [&] { return grp.left.load() == 0; });
+    grp.cv.wait(g, [&] { return grp.left == 0; });
   }
 
  private:
@@ -1287,28 +1299,19 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       p->fz = g.Wz > 1 ? vk::fast_lookup(g.Wz) : nullptr;
       if (conv) p->fx = nullptr;  // XM_CONV_OUT lives in the generic x kernel
       if (p->fx) {  // butterfly-major pass-2 twiddles of the fast x pass (reg::load_twiddles2 layout)
-        const int R1 = p->fx->R1, R2 = g.Wx / R1;
-        std::vector<float2> t2((size_t)R1 * R2);
-        for (int j = 0; j < R1; ++j)
-          for (int r = 0; r < R2; ++r) t2[(size_t)j * R2 + r] = tx[(size_t)r * j];
+        const auto t2 = fast_twiddles(p->fx, tx);
         p->twx2.alloc(t2.size(), "twiddles");
         ck(cudaMemcpy(p->twx2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
         p->lpx.tw2 = p->twx2.p;
       }
       if (p->fz) {  // and the fast z pass
-        const int R1 = p->fz->R1, R2 = g.Wz / R1;
-        std::vector<float2> t2((size_t)R1 * R2);
-        for (int j = 0; j < R1; ++j)
-          for (int r = 0; r < R2; ++r) t2[(size_t)j * R2 + r] = tz[(size_t)r * j];
+        const auto t2 = fast_twiddles(p->fz, tz);
         p->twz2.alloc(t2.size(), "twiddles");
         ck(cudaMemcpy(p->twz2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
         p->lpz.tw2 = p->twz2.p;
       }
       if (p->fy) {  // same for the fast y pass
-        const int R1 = p->fy->R1, R2 = g.Wy / R1;
-        std::vector<float2> t2((size_t)R1 * R2);
-        for (int j = 0; j < R1; ++j)
-          for (int r = 0; r < R2; ++r) t2[(size_t)j * R2 + r] = ty[(size_t)r * j];
+        const auto t2 = fast_twiddles(p->fy, ty);
         p->twy2.alloc(t2.size(), "twiddles");
         ck(cudaMemcpy(p->twy2.p, t2.data(), t2.size() * sizeof(float2), cudaMemcpyHostToDevice), "twiddles");
         p->lpy.tw2 = p->twy2.p;
