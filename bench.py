@@ -427,6 +427,7 @@ def main():
     e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
     e2e_value = None
     e2e_vols = 0
+    first_call_ms = None
     if e2e_steps > 0:
         # batch configs: at most 64 volumes per rank (pageable host memory for
         # the whole C5 block would be 2 x 69 GB)
@@ -439,7 +440,9 @@ def main():
                 return [r.estimate for r in vk.richardson_lucy_batch(host_in, psf, rule, device=local)]
             return [vk.richardson_lucy(host_in[0], psf, rule, device=local).estimate]
 
+        tc = time.perf_counter()
         e2e_call()  # warm: builds and caches the plan
+        first_call_ms = (time.perf_counter() - tc) * 1e3
         if dist:
             dist.barrier()
         t0 = time.perf_counter()
@@ -498,6 +501,9 @@ def main():
                 "api": ("vk_richardson_lucy_batch (deconv::richardson_lucy_batch)" if n_batch
                         else "vk_richardson_lucy (deconv::richardson_lucy)")
                        + ": pageable host arrays, pinned staging ring, cached plan",
+                "first_call_ms": first_call_ms,
+                "first_call": "the untimed warm-up call: plan creation (device buffers, both OTFs, their "
+                              "symmetry / rank-1 tests) + the same run; the timed calls reuse the cached plan",
                 "volumes_per_rank": e2e_vols, "steps": e2e_steps},
         "gpu_launches": launches,
         "clocks": clk.summary(),

@@ -13,6 +13,7 @@
 
 #include <algorithm>
 #include <atomic>
+#include <chrono>
 #include <condition_variable>
 #include <deque>
 #include <functional>
@@ -188,6 +189,15 @@ size_t x_smem(int Wx, int L) {
 }
 size_t yz_smem(int N, int L) { return 2 * (size_t)N * vk::line_pitch(L) * sizeof(float2); }
 
+// VK_RL_TIMING=1: host-side phase times of the host-buffer calls on stderr
+bool timing_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("VK_RL_TIMING");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 // ---- host staging -----------------------------------------------------------
 // Host-pointer calls (vk_rl_run, vk_rl_step, vk_conv_run, the batch form)
 // take whatever memory the caller has: pinned pointers are DMA'd directly;
@@ -300,10 +310,18 @@ bool host_pinned(const void* p) {
 }
 
 struct Staging {
-  static constexpr int kSlots = 4;
-  static constexpr size_t kChunk = 16 << 20;
-  void* h[kSlots]{};
-  cudaEvent_t ev[kSlots]{};
+  static constexpr int kMaxSlots = 16;
+  // ring geometry: VK_RL_STAGE_MB (chunk size) x VK_RL_STAGE_SLOTS
+  const int kSlots = [] {
+    const char* e = std::getenv("VK_RL_STAGE_SLOTS");
+    return e ? std::max(2, std::min(kMaxSlots, std::atoi(e))) : 4;
+  }();
+  const size_t kChunk = [] {
+    const char* e = std::getenv("VK_RL_STAGE_MB");
+    return (size_t)(e ? std::max(1, std::atoi(e)) : 16) << 20;
+  }();
+  void* h[kMaxSlots]{};
+  cudaEvent_t ev[kMaxSlots]{};
   ~Staging() {
     for (int i = 0; i < kSlots; ++i) {
       if (h[i]) cudaFreeHost(h[i]);
@@ -324,14 +342,38 @@ struct Staging {
       return;
     }
     ensure();
+    const bool tm = timing_on();
+    std::vector<cudaEvent_t> te;  // VK_RL_TIMING: per-chunk DMA times
+    std::vector<double> cpy;
     size_t off = 0;
     for (int c = 0; off < bytes; ++c, off += kChunk) {
       const int k = c % kSlots;
       const size_t n = std::min(kChunk, bytes - off);
       if (c >= kSlots) ck(cudaEventSynchronize(ev[k]), "staging");  // slot's previous DMA done
+      const auto t0 = std::chrono::steady_clock::now();
       parallel_memcpy(h[k], (const char*)src + off, n);
+      if (tm) {
+        cpy.push_back(std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count());
+        te.resize(te.size() + 2);
+        cudaEventCreate(&te[te.size() - 2]);
+        cudaEventCreate(&te[te.size() - 1]);
+        cudaEventRecord(te[te.size() - 2], s);
+      }
       ck(cudaMemcpyAsync((char*)dst + off, h[k], n, cudaMemcpyHostToDevice, s), "H2D");
+      if (tm) cudaEventRecord(te.back(), s);
       ck(cudaEventRecord(ev[k], s), "staging");
+    }
+    if (tm) {
+      cudaStreamSynchronize(s);
+      std::fprintf(stderr, "  h2d chunks (host copy / DMA ms):");
+      for (size_t i = 0; i < cpy.size(); ++i) {
+        float ms = 0;
+        cudaEventElapsedTime(&ms, te[2 * i], te[2 * i + 1]);
+        std::fprintf(stderr, " %.3f/%.3f", cpy[i], ms);
+        cudaEventDestroy(te[2 * i]);
+        cudaEventDestroy(te[2 * i + 1]);
+      }
+      std::fprintf(stderr, "\n");
     }
   }
   // device -> host after everything enqueued on s; returns when dst is written
@@ -1815,20 +1857,23 @@ void run_graph_loop(vk_rl_plan p, cudaStream_t s, const float* d_obs, const vk_s
     ck(cudaGraphAddNode(&node, p->gr, nullptr, 0, &cp), "graph while node");
     cudaGraph_t body = cp.conditional.phGraph_out[0];
     const uint64_t before = p->launches;
-    ck(cudaStreamBeginCaptureToGraph(s, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal), "capture");
+    // The body is captured on the plan's own stream: the caller's `s` may be
+    // the legacy NULL stream, which cannot capture.  Only the launch uses `s`.
+    cudaStream_t cs = p->stream;
+    ck(cudaStreamBeginCaptureToGraph(cs, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal), "capture");
     t_capturing = true;
     try {
-      conv_yz(p, s, p->otf.p);
+      conv_yz(p, cs, p->otf.p);
       // every iteration's partials in slot 0: the rule kernel reduces them before the next
-      x_pass(p, s, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
-      conv_yz(p, s, p->otf_flip.p);
-      x_pass(p, s, vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
+      x_pass(p, cs, vk::XM_RATIO, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
+      conv_yz(p, cs, p->otf_flip.p);
+      x_pass(p, cs, vk::XM_UPDATE, nullptr, g.Pz, g.Py, g.Px, 1.f, p->est.p, d_obs, 1, nullptr);
       if (frc) {
-        frc_bins_enqueue(p, s);
-        vk::frc_value_kernel<<<1, 32, 0, s>>>(p->frc_bins.p, p->frc_nbins, p->frc_binf, spacing, p->gmetric.p);
+        frc_bins_enqueue(p, cs);
+        vk::frc_value_kernel<<<1, 32, 0, cs>>>(p->frc_bins.p, p->frc_nbins, p->frc_binf, spacing, p->gmetric.p);
         launch_check(p, "frc value");
       }
-      if (ssim) ssim_eval_graph(p, s);
+      if (ssim) ssim_eval_graph(p, cs);
       vk::RuleArgs ra{};
       ra.st = p->gstate.p;
       ra.values = p->gvalues.p;
@@ -1844,17 +1889,17 @@ void run_graph_loop(vk_rl_plan p, cudaStream_t s, const float* d_obs, const vk_s
       ra.patience = rule->patience;
       ra.iters = iters;
       ra.handle = h;
-      vk::rule_step_kernel<<<1, 256, 0, s>>>(ra);
+      vk::rule_step_kernel<<<1, 256, 0, cs>>>(ra);
       launch_check(p, "rule");
     } catch (...) {
       t_capturing = false;
       cudaGraph_t junk;
-      cudaStreamEndCapture(s, &junk);
+      cudaStreamEndCapture(cs, &junk);
       cudaGetLastError();
       throw;
     }
     t_capturing = false;
-    ck(cudaStreamEndCapture(s, &body), "end capture");
+    ck(cudaStreamEndCapture(cs, &body), "end capture");
     ck(cudaGraphInstantiate(&p->grx, p->gr, 0), "graph instantiate");
     p->gr_body_launches = p->launches - before;
     p->launches = before;
@@ -1901,19 +1946,24 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   const size_t nI = (size_t)g.Iz * g.Iy * g.Ix;
   const size_t nP = (size_t)g.Pz * g.Py * g.Px;
 
+  const auto ta = std::chrono::steady_clock::now();
   vk::ObsStats init{};
   init.minbits = 0x7f800000u;
   init.maxbits = 0u;
   ck(cudaMemcpyAsync(p->stats.p, &init, sizeof(init), cudaMemcpyHostToDevice, s), "stats init");
+  const auto tb = std::chrono::steady_clock::now();
   ck(cudaMemsetAsync(p->acc.p, 0, (size_t)iters * 4 * sizeof(double), s), "acc");
   const int sgrid = 148 * 4;
   vk::obs_stats_kernel<<<kStatBlocks, kThreads, 0, s>>>(d_obs, nI, p->stats.p, p->part.p);
   launch_check(p, "obs_stats");
   vk::reduce_partials_kernel<<<2, 256, 0, s>>>(p->part.p, kStatBlocks, 2, &p->stats.p->sr);
   launch_check(p, "obs_stats reduce");
+  const auto tc = std::chrono::steady_clock::now();
   vk::ObsStats st{};
   ck(cudaMemcpyAsync(&st, p->stats.p, sizeof(st), cudaMemcpyDeviceToHost, s), "stats D2H");
+  const auto tr0 = std::chrono::steady_clock::now();
   ck(cudaStreamSynchronize(s), "stats");
+  const auto tr1 = std::chrono::steady_clock::now();
   if (check_obs && st.neg) fail(VK_ERR_NEGATIVE, "NegativeInput: observed image must be nonnegative");
   if (p->psf_status) fail((vk_status)p->psf_status, p->psf_msg);
   float fmin, fmax;
@@ -2011,7 +2061,19 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
   }
   flush_sums(p, s, run);
   ck(cudaMemcpyAsync(p->h_acc, p->acc.p, (size_t)run * 4 * sizeof(double), cudaMemcpyDeviceToHost, s), "acc D2H");
+  const auto tr2 = std::chrono::steady_clock::now();
   ck(cudaStreamSynchronize(s), "run");
+  if (timing_on()) {
+    const auto tr3 = std::chrono::steady_clock::now();
+    auto ms = [](std::chrono::steady_clock::time_point a, std::chrono::steady_clock::time_point b) {
+      return std::chrono::duration<double, std::milli>(b - a).count();
+    };
+    std::fprintf(stderr,
+                 "run_device: stats init %.3f  stats launch %.3f  stats D2H %.3f  stats wait %.3f  enqueue %.3f  "
+                 "final wait %.3f ms (%llu launches)\n",
+                 ms(ta, tb), ms(tb, tc), ms(tc, tr0), ms(tr0, tr1), ms(tr1, tr2), ms(tr2, tr3),
+                 (unsigned long long)p->launches);
+  }
   if (graph) {
     // values, stop decision and timestamps come from the device
   } else if (ssim) {
@@ -2463,20 +2525,33 @@ vk_status vk_rl_run(vk_rl_plan p, const float* obs, float* est, const vk_stop_ru
     check_rule(rule);
     DeviceGuard dg(p->device);
     const size_t n = image_count(p);
+    const bool timing = timing_on();
+    using clk = std::chrono::steady_clock;
+    const auto t0 = clk::now();
     if (p->obs.n < n) p->obs.alloc(n, "observed");
     if (p->out.n < n) p->out.alloc(n, "output");
     p->staging.h2d(p->obs.p, obs, n * sizeof(float), p->stream);
+    const auto t1 = clk::now();
     // a pageable output (e.g. a fresh array) is faulted in while the GPU runs
     std::thread touch;
     if (!host_pinned(est)) touch = std::thread([=] { prefault(est, n * sizeof(float)); });
+    const auto t1b = clk::now();
     try {
       run_device(p, p->obs.p, p->out.p, rule, flat_init, trace, p->stream, true);
     } catch (...) {
       if (touch.joinable()) touch.join();
       throw;
     }
+    const auto t2 = clk::now();
     if (touch.joinable()) touch.join();
+    const auto t3 = clk::now();
     p->staging.d2h(est, p->out.p, n * sizeof(float), p->stream);
+    if (timing) {
+      const auto t4 = clk::now();
+      auto ms = [](clk::time_point a, clk::time_point b) { return std::chrono::duration<double, std::milli>(b - a).count(); };
+      std::fprintf(stderr, "vk_rl_run: h2d(enqueue+host copy) %.3f  prefault spawn %.3f  run %.3f  prefault wait %.3f  d2h %.3f ms\n",
+                   ms(t0, t1), ms(t1, t1b), ms(t1b, t2), ms(t2, t3), ms(t3, t4));
+    }
   });
 }
 

@@ -563,6 +563,27 @@ def test_plan_reuse_batch_and_device_api():
     assert rel_l2(batch[2].estimate, its[-1]) <= TOL_N
 
 
+def test_device_stopping_on_the_null_stream():
+    """A rule that may stop early runs as a CUDA graph; the caller's stream
+    may be the legacy NULL stream (which cannot capture): the body is captured
+    on the plan's own stream and launched on the caller's."""
+    import torch
+
+    psf = O.gaussian_psf((7, 7, 7), 1.2)
+    obs = synth.blurred(synth.blobs((20, 48, 40), 6, 4, 7, seed=5), psf)
+    plan = vk.RlPlan(obs.shape, psf)
+    rule = vk.StoppingRule("si_psnr_vs_input", 1e-2, 2, 12)
+    host = plan.run(obs, rule)
+    d_obs = torch.from_numpy(obs).cuda()
+    for stream in (0, torch.cuda.current_stream().cuda_stream):
+        d_out = torch.empty_like(d_obs)
+        tr = plan.run_device(d_obs.data_ptr(), d_out.data_ptr(), rule, stream=stream)
+        torch.cuda.synchronize()
+        assert tr.stop_reason == host.trace.stop_reason
+        assert len(tr.records) == len(host.trace.records)
+        assert np.array_equal(d_out.cpu().numpy(), host.estimate)
+
+
 def test_ssim_too_small_is_loud():
     psf = O.gaussian_psf((3, 3, 3), 1.0)
     obs = np.ones((6, 8, 8), np.float32) + np.arange(384, dtype=np.float32).reshape(6, 8, 8) / 384
