@@ -211,6 +211,11 @@ bool timing_on() {
 // Process-wide workers for parallel host memcpy.  run(n, f) calls f(0..n-1)
 // on the pool and the calling thread and returns when all are done; the tasks
 // never block, so concurrent callers (batch lanes) cannot deadlock.
+// Staging calls it once per chunk, back to back, so dispatch latency matters:
+// idle workers spin for a while before they sleep on the condition variable,
+// the caller helps drain the queue, and completion is a spin on an atomic
+// count (a condition-variable round trip per chunk cost ~0.15 ms:
+// profiles/r02/staging_dma.md).
 class HostPool {
  public:
   static HostPool& get() {
@@ -224,54 +229,88 @@ class HostPool {
       for (int i = 0; i < n; ++i) f(i);
       return;
     }
-    // `grp` lives on this frame: the count drops under the mutex so the
-    // caller cannot see zero, return and destroy it while the last worker is
-    // still about to touch the mutex / condition variable (a lock-free
-    // decrement followed by lock + notify crashed sporadically)
-    struct Group {
-      int left;
-      std::mutex m;
-      std::condition_variable cv;
-    } grp;
-    grp.left = n;
+    // `left` lives on this frame: a task's decrement is its last access to
+    // it, so the caller may return as soon as it reads zero
+    std::atomic<int> left{n};
     auto one = [&](int i) {
       f(i);
-      std::lock_guard<std::mutex> g(grp.m);
-      if (--grp.left == 0) grp.cv.notify_all();
+      left.fetch_sub(1, std::memory_order_acq_rel);
     };
     {
       std::lock_guard<std::mutex> g(mu_);
       for (int i = 1; i < n; ++i) q_.push_back([&one, i] { one(i); });
+      pending_.fetch_add(n - 1, std::memory_order_release);
     }
-    cv_.notify_all();
+    if (sleepers_.load(std::memory_order_acquire) > 0) cv_.notify_all();
     one(0);
-    std::unique_lock<std::mutex> g(grp.m);
-    grp.cv.wait(g, [&] { return grp.left == 0; });
+    std::function<void()> t;
+    while (pop(t)) t();  // help: ours or another caller's tasks
+    for (int k = 0; left.load(std::memory_order_acquire) != 0; ++k) pause(k);
   }
 
  private:
+  static void pause(int k) {
+#if defined(__x86_64__)
+    if (k < 4096) {
+      _mm_pause();
+      return;
+    }
+#endif
+    std::this_thread::yield();
+  }
+  bool pop(std::function<void()>& t) {
+    if (pending_.load(std::memory_order_acquire) == 0) return false;
+    std::lock_guard<std::mutex> g(mu_);
+    if (q_.empty()) return false;
+    t = std::move(q_.front());
+    q_.pop_front();
+    pending_.fetch_sub(1, std::memory_order_relaxed);
+    return true;
+  }
+  void worker() {
+    using clk = std::chrono::steady_clock;
+    for (;;) {
+      std::function<void()> t;
+      if (pop(t)) {
+        t();
+        continue;
+      }
+      // spin ~0.5 ms for the next chunk before sleeping
+      const auto t0 = clk::now();
+      bool more = false;
+      for (int k = 0;; ++k) {
+        if (pending_.load(std::memory_order_acquire) > 0) {
+          more = true;
+          break;
+        }
+#if defined(__x86_64__)
+        _mm_pause();
+#endif
+        if ((k & 255) == 255 && clk::now() - t0 > std::chrono::microseconds(500)) break;
+      }
+      if (more) continue;
+      std::unique_lock<std::mutex> g(mu_);
+      sleepers_.fetch_add(1, std::memory_order_acq_rel);
+      cv_.wait(g, [&] { return !q_.empty(); });
+      sleepers_.fetch_sub(1, std::memory_order_acq_rel);
+      t = std::move(q_.front());
+      q_.pop_front();
+      pending_.fetch_sub(1, std::memory_order_relaxed);
+      g.unlock();
+      t();
+    }
+  }
   HostPool() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
     int n = (int)std::min(hw, 16u) - 1;
     if (const char* e = std::getenv("VK_RL_HOST_THREADS")) n = std::max(0, std::atoi(e) - 1);
-    for (int i = 0; i < n; ++i)
-      th_.emplace_back([this] {
-        for (;;) {
-          std::function<void()> t;
-          {
-            std::unique_lock<std::mutex> g(mu_);
-            cv_.wait(g, [&] { return !q_.empty(); });
-            t = std::move(q_.front());
-            q_.pop_front();
-          }
-          t();
-        }
-      });
+    for (int i = 0; i < n; ++i) th_.emplace_back([this] { worker(); });
     for (auto& t : th_) t.detach();
   }
   std::mutex mu_;
   std::condition_variable cv_;
   std::deque<std::function<void()>> q_;
+  std::atomic<int> pending_{0}, sleepers_{0};
   std::vector<std::thread> th_;
 };
 
@@ -2165,7 +2204,7 @@ void run_device(vk_rl_plan p, const float* d_obs, float* d_out, const vk_stop_ru
 
 // Lanes for a batch of n independent volumes: VK_RL_LANES, else enough to
 // fill the GPU when one volume's x-pass grid is short of a few waves.
-int lane_count(vk_rl_plan p, int n) {
+int lane_count(vk_rl_plan p, int n, bool host) {
   const char* env = std::getenv("VK_RL_LANES");
   int want;
   if (env && std::atoi(env) > 0) {
@@ -2175,7 +2214,10 @@ int lane_count(vk_rl_plan p, int n) {
     // C3 (64x256x256 volumes) 2/3/4 lanes = 3.58/3.36/3.33e10, C5 (2048^2
     // fields) 1/2/3/4 = 3.07/3.57/3.70/3.54e10 voxel-iters/s.  (With the
     // round's first kernels, profiles/r01/lanes.log, C3 peaked at 3 lanes.)
-    want = p->rank == 2 ? 3 : 2;
+    // Host-buffer batches: a lane's copies leave the GPU to the others, so
+    // one more lane pays (C3, 8 pageable volumes: 2/3/4 lanes = 2.89/2.64-2.76/
+    // 2.74 ms per volume, profiles/r02/staging_dma.md).
+    want = p->rank == 2 ? 3 : (host ? 3 : 2);
   }
   return std::max(1, std::min(want, n));
 }
@@ -2183,9 +2225,9 @@ int lane_count(vk_rl_plan p, int n) {
 // Runs fn(lane_plan, volume) for volumes 0..n-1, volume i on lane i % lanes,
 // each lane on its own host thread and stream; rethrows the first failure.
 template <class F>
-void run_lanes(vk_rl_plan p, int n, F&& fn) {
+void run_lanes(vk_rl_plan p, int n, bool host, F&& fn) {
   if (n <= 0) return;
-  const int nl = lane_count(p, n);
+  const int nl = lane_count(p, n, host);
   while ((int)p->lanes.size() < nl - 1) {
     vk_rl_plan q = create_plan(p->device, p->rank, p->ishape, p->rank, p->kshape, p->psf_host.data(), p->pad ? 1 : 0);
     q->prof = p->prof;
@@ -2610,7 +2652,7 @@ vk_status vk_rl_run_batch(vk_rl_plan p, int n, const float* const* obs, float* c
   return guarded([&] {
     if (!p || n < 0 || (n > 0 && (!obs || !est))) fail(VK_ERR_ARG, "NULL argument");
     check_rule(rule);
-    run_lanes(p, n, [&](vk_rl_plan q, int i) {
+    run_lanes(p, n, true, [&](vk_rl_plan q, int i) {
       const vk_status st = vk_rl_run(q, obs[i], est[i], rule, flat_init, traces ? &traces[i] : nullptr);
       if (st != VK_OK) fail(st, "volume " + std::to_string(i) + ": " + g_last_error);
     });
@@ -2624,7 +2666,7 @@ vk_status vk_rl_run_batch_device(vk_rl_plan p, int n, const float* const* d_obs,
     check_rule(rule);
     DeviceGuard dg(p->device);
     ck(cudaStreamSynchronize((cudaStream_t)stream), "batch inputs");  // the lanes read them
-    run_lanes(p, n, [&](vk_rl_plan q, int i) {
+    run_lanes(p, n, false, [&](vk_rl_plan q, int i) {
       run_device(q, d_obs[i], d_est[i], rule, flat_init, traces ? &traces[i] : nullptr, q->stream, true);
     });
   });
