@@ -82,9 +82,13 @@ __device__ __forceinline__ void bulk_store(void* gdst, const void* smem_src, uns
 }
 // generic-proxy shared-memory writes -> visible to the async (TMA) proxy
 __device__ __forceinline__ void fence_proxy_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
-__device__ __forceinline__ void bulk_commit_and_wait() {
+// End-of-kernel bulk / TMA stores: wait only until the shared source has
+// been read (the writes complete with the grid), so the CTA's slot frees
+// without waiting out the store's global write latency (y passes -4 to -6%,
+// C2 +1.1%: profiles/r02/bulk_wait_read_ab.txt).
+__device__ __forceinline__ void bulk_commit_and_release() {
   asm volatile("cp.async.bulk.commit_group;" ::: "memory");
-  asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+  asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
 }
 __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* map, uint64_t* bar, int c0, int c1,
                                             int c2) {
@@ -815,7 +819,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
     __syncthreads();
     if (threadIdx.x == 0) {
       tma_store_3d(&ta.map, A + out_off * L, ky0, 0, kx);  // columns ky >= Wy are clipped
-      bulk_commit_and_wait();
+      bulk_commit_and_release();
     }
     return;
   }
@@ -916,7 +920,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
       for (int l = 0; l < nvalid; ++l)
         bulk_store(a.out + (size_t)y_line(a, line0 + l) * a.out_pitch, A + l * NP + a.out_off,
                    (unsigned)(a.n_out * sizeof(float2)));
-      bulk_commit_and_wait();
+      bulk_commit_and_release();
     }
     return;
   }
