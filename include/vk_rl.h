@@ -284,6 +284,12 @@ vk_status vk_rl_plan_otf_bytes(vk_rl_plan plan, int n_kinds, uint64_t* otf_bytes
 const char* vk_last_error(void);
 int vk_abi_version(void);
 
+/* Debug: with VK_RL_GUARD=1 in the environment every device buffer a plan
+ * allocates carries a 64 KB guard band of a fixed pattern on each side.
+ * Returns the number of bands found overwritten (freed buffers so far plus
+ * the live ones checked now), or -1 when guards are off. */
+int vk_debug_guard_check(void);
+
 #ifdef __cplusplus
 }
 #endif

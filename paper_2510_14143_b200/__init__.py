@@ -199,8 +199,17 @@ def lib() -> ctypes.CDLL:
     L.vk_good_size.restype = ctypes.c_uint64
     L.vk_last_error.restype = ctypes.c_char_p
     L.vk_abi_version.restype = ctypes.c_int
+    L.vk_debug_guard_check.argtypes = []
+    L.vk_debug_guard_check.restype = ctypes.c_int
     _lib = L
     return L
+
+
+def debug_guard_check() -> int:
+    """With VK_RL_GUARD=1 set before the library is loaded: the number of
+    device-buffer guard bands found overwritten so far (vk_debug_guard_check);
+    -1 when guards are off."""
+    return int(lib().vk_debug_guard_check())
 
 
 def plan_cache_clear() -> None:

@@ -94,6 +94,45 @@ uint64_t good_size(uint64_t n) {
   }
 }
 
+// ---- guard bands (VK_RL_GUARD=1) --------------------------------------------
+// compute-sanitizer is closed on the GPU pool this was built on, so plan
+// buffers can carry their own out-of-bounds-write check: every device
+// allocation gets a 64 KB band of a fixed byte pattern on each side; the bands
+// are verified when the buffer is freed and by vk_debug_guard_check().
+constexpr size_t kGuard = 64 << 10;
+constexpr unsigned char kGuardByte = 0xA5;
+bool guard_on() {
+  static const bool on = [] {
+    const char* e = std::getenv("VK_RL_GUARD");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+struct GuardReg {
+  std::mutex mu;
+  std::vector<std::pair<char*, std::pair<size_t, std::string>>> live;  // raw base, (payload bytes, name)
+  long long violations = 0;
+  static GuardReg& get() {
+    static GuardReg* g = new GuardReg();
+    return *g;
+  }
+  // 1 if either band of `raw` no longer holds the pattern
+  static int damaged(char* raw, size_t bytes, const std::string& what) {
+    std::vector<unsigned char> h(kGuard);
+    for (int side = 0; side < 2; ++side) {
+      char* band = side ? raw + kGuard + bytes : raw;
+      if (cudaMemcpy(h.data(), band, kGuard, cudaMemcpyDeviceToHost) != cudaSuccess) return 1;
+      for (size_t i = 0; i < kGuard; ++i)
+        if (h[i] != kGuardByte) {
+          std::fprintf(stderr, "vk guard: %s band of '%s' (%zu bytes) overwritten at byte %zu\n",
+                       side ? "upper" : "lower", what.c_str(), bytes, side ? i : kGuard - i);
+          return 1;
+        }
+    }
+    return 0;
+  }
+};
+
 // RAII device pointer owned by a plan.
 template <class T>
 struct DevBuf {
@@ -102,11 +141,37 @@ struct DevBuf {
   void alloc(size_t count, const char* what) {
     free();
     if (count == 0) count = 1;
-    ck(cudaMalloc(&p, count * sizeof(T)), what);
+    if (guard_on()) {
+      char* raw = nullptr;
+      const size_t bytes = count * sizeof(T);
+      ck(cudaMalloc(&raw, bytes + 2 * kGuard), what);
+      ck(cudaMemset(raw, kGuardByte, kGuard), what);
+      ck(cudaMemset(raw + kGuard + bytes, kGuardByte, kGuard), what);
+      p = reinterpret_cast<T*>(raw + kGuard);
+      GuardReg& g = GuardReg::get();
+      std::lock_guard<std::mutex> lk(g.mu);
+      g.live.push_back({raw, {bytes, what}});
+    } else {
+      ck(cudaMalloc(&p, count * sizeof(T)), what);
+    }
     n = count;
   }
   void free() {
-    if (p) cudaFree(p);
+    if (p && guard_on()) {
+      char* raw = reinterpret_cast<char*>(p) - kGuard;
+      GuardReg& g = GuardReg::get();
+      std::lock_guard<std::mutex> lk(g.mu);
+      for (size_t i = 0; i < g.live.size(); ++i)
+        if (g.live[i].first == raw) {
+          cudaDeviceSynchronize();
+          g.violations += GuardReg::damaged(raw, g.live[i].second.first, g.live[i].second.second);
+          g.live.erase(g.live.begin() + i);
+          break;
+        }
+      cudaFree(raw);
+    } else if (p) {
+      cudaFree(p);
+    }
     p = nullptr;
     n = 0;
   }
@@ -537,6 +602,7 @@ struct vk_rl_plan_s {
   // y-forward -> z -> y-inverse through a ring slot (one per stream) small
   // enough to stay L2-resident, so S_B does not make HBM round trips
   int kxc = 0, kxs = 2;  // planes per chunk, streams (= ring slots)
+  int kxn = 0;           // > 0: kxn chunks with boundaries kx0 = c * Hx / kxn (sizes differ by <= 1)
   size_t ring_window = 0;  // bytes of ring2 under a persisting L2 access window (0: none)
   DevBuf<float2> ring2;
   CUtensorMap zmap_ring[4]{};
@@ -947,14 +1013,16 @@ void conv_yz_chunked(vk_rl_plan p, cudaStream_t s, const float2* otf) {
   for (int i = 1; i < ns; ++i) ck(cudaStreamWaitEvent(p->kstream[i], p->kev[0], 0), "wait");
   const size_t plane_a = (size_t)g.Pz * g.Py, slot_b = (size_t)p->kxc * g.Pz * g.Wy;
   int c = 0;
-  for (int kx0 = 0; kx0 < g.Hx; kx0 += p->kxc, ++c) {
-    const int nk = std::min(p->kxc, g.Hx - kx0), slot = c % ns;
+  for (int kx0 = 0; kx0 < g.Hx; ++c) {
+    const int kx1 = p->kxn ? (int)((long long)(c + 1) * g.Hx / p->kxn) : std::min(kx0 + p->kxc, g.Hx);
+    const int nk = kx1 - kx0, slot = c % ns;
     cudaStream_t cs = slot ? p->kstream[slot] : s;
     float2* sa = p->SA.p + (size_t)kx0 * plane_a;
     float2* sb = p->ring2.p + (size_t)slot * slot_b;
     y_pass(p, cs, vk::YM_FWD, nk * g.Pz, g.Py, g.Py, g.Wy, g.Wy, 0, sa, sb, nullptr);
     z_pass_chunk(p, cs, otf, kx0, nk, slot);
     y_pass(p, cs, vk::YM_INV, nk * g.Pz, g.Wy, g.Wy, g.Py, g.Py, p->ycrop, sb, sa, nullptr);
+    kx0 = kx1;
   }
   for (int i = 1; i < ns; ++i) {
     ck(cudaEventRecord(p->kev[i], p->kstream[i]), "event");
@@ -1507,7 +1575,14 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
       if (mb > 0) {
         const double plane = (double)g.Pz * g.Wy * 8;
         const int c = std::max(1, (int)(mb * 1e6 / plane));
-        const int nch = (g.Hx + c - 1) / c;
+        int nch = (g.Hx + c - 1) / c;
+        if (const char* ks = std::getenv("VK_RL_KXSTREAMS")) p->kxs = std::max(2, std::min(4, std::atoi(ks)));
+        const char* ke = std::getenv("VK_RL_KXEVEN");
+        if (ke && ke[0] == '1' && nch > 1) {
+          // a multiple of the stream count: the streams' last chunks end together
+          nch = std::min((nch + p->kxs - 1) / p->kxs * p->kxs, g.Hx);  // no empty chunk
+          p->kxn = nch;
+        }
         p->kxc = nch > 1 ? (g.Hx + nch - 1) / nch : 0;  // balanced chunks
       }
       if (const char* ks = std::getenv("VK_RL_KXSTREAMS")) p->kxs = std::max(2, std::min(4, std::atoi(ks)));
@@ -2469,6 +2544,17 @@ uint64_t otf_bytes(vk_rl_plan p, int kind) {
 extern "C" {
 
 uint64_t vk_good_size(uint64_t n) { return good_size(n); }
+
+int vk_debug_guard_check(void) {
+  if (!guard_on()) return -1;
+  cudaDeviceSynchronize();
+  GuardReg& g = GuardReg::get();
+  std::lock_guard<std::mutex> lk(g.mu);
+  long long v = g.violations;
+  for (auto& e : g.live) v += GuardReg::damaged(e.first, e.second.first, e.second.second);
+  return (int)std::min<long long>(v, 1 << 30);
+}
+
 const char* vk_last_error(void) { return g_last_error.c_str(); }
 int vk_abi_version(void) { return VK_RL_ABI_VERSION; }
 

@@ -59,7 +59,21 @@ def main(mode):
         y = vk.fft_convolve(x, gauss((3, 3, 3), 1.0), circular=circ)
         assert np.isfinite(y).all()
     print("fft_convolve ok", a.shape, flush=True)
+    # the benchmarked paths: kx-chunked y/z convolution at the C2 grid
+    # (576 x / y, 192 z, half OTF), the C4 grid (1080 x TMA pass), a 2160-point
+    # 2D field, device-side stopping (CUDA graph), rl_step
+    os.environ["VK_RL_KXCHUNK"] = "2"
+    run(vol((128, 512, 60)), O.widefield_psf(31), iters=2)
+    run(vol((100, 1000, 20)), gauss((21, 21, 21), 2.5), iters=2)
+    del os.environ["VK_RL_KXCHUNK"]
+    if mode == "full":
+        run(vol((2048, 2048)), gauss((31, 31), 3.75), iters=2)
+    r = vk.richardson_lucy(vol((24, 48, 40)), gauss((7, 7, 7), 1.2), vk.StoppingRule("si_psnr_vs_input", 1e-2, 2, 12))
+    print("graph stop", len(r.trace.records), r.trace.stop_reason, flush=True)
+    e, o = vol((20, 30, 40)), vol((20, 30, 40))
+    assert np.isfinite(vk.rl_step(e, o, gauss((5, 5, 5), 1.0))).all()
     vk.plan_cache_clear()
+    print("GUARD_VIOLATIONS", vk.debug_guard_check(), flush=True)
     print("SANITIZE_CASES_DONE")
 
 
