@@ -602,7 +602,7 @@ struct vk_rl_plan_s {
   // y-forward -> z -> y-inverse through a ring slot (one per stream) small
   // enough to stay L2-resident, so S_B does not make HBM round trips
   int kxc = 0, kxs = 2;  // planes per chunk, streams (= ring slots)
-  int kxn = 0;           // > 0: kxn chunks with boundaries kx0 = c * Hx / kxn (sizes differ by <= 1)
+  int kxn = 0;           // chunks; boundaries kx0 = c * Hx / kxn (sizes differ by <= 1)
   size_t ring_window = 0;  // bytes of ring2 under a persisting L2 access window (0: none)
   DevBuf<float2> ring2;
   CUtensorMap zmap_ring[4]{};
@@ -1563,29 +1563,34 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     if (const char* xpf = std::getenv("VK_RL_XPF")) p->xpf = std::atoi(xpf);
     if (p->fz && p->fz->ztk && g.Wz > 1 && g.Pz <= 256 && g.Wy % 2 == 0 && !(notma && notma[0] == '1'))
       p->ztma = encode_zmap(p, std::max(g.Pz, p->Kz));
-    // kx-chunked y/z convolution (VK_RL_KXCHUNK = target MB of S_B per
-    // chunk, 0 = whole-volume passes), TMA z plans of RL kind.  Default 20 MB
-    // on 2 streams where S_B does not fit L2 anyway (> 64 MB): C2 +6.5%, C4
-    // +1.5%, chunk/stream sweep in profiles/r02/kxchunk.md; small volumes
-    // (C1/C3, S_B 26 MB) keep the whole-volume passes.
+    // kx-chunked y/z convolution where S_B does not fit L2 anyway (> 64 MB);
+    // small volumes (C1/C3, S_B 26 MB) keep the whole-volume passes.  Chunk
+    // count: a multiple of the stream count (the streams' last chunks end
+    // together: C4 +1.0%) near Hx * ceil(Wy/16) / 1250, i.e. ~1250 z-tile CTAs
+    // per chunk -- the optimum of both measured grids (C2: 8 chunks of 36-37
+    // planes, 3.72e10 vs 3.69e10 / 3.60e10 at 10 / 6 chunks; C4: 30 chunks of
+    // 18, 3.589e10 vs 3.571e10 / 3.557e10 at 38 / 24: profiles/r02/kxchunk_even_ab.txt).
+    // VK_RL_KXCHUNK = target MB of S_B per chunk instead (0 = whole volume).
     if (p->ztma && !conv && !zslab) {
       const char* kc = std::getenv("VK_RL_KXCHUNK");
-      const double sb_mb = (double)g.Hx * g.Pz * g.Wy * 8 / 1e6;
-      const double mb = kc ? std::atof(kc) : (sb_mb > 64.0 ? 20.0 : 0.0);
-      if (mb > 0) {
-        const double plane = (double)g.Pz * g.Wy * 8;
-        const int c = std::max(1, (int)(mb * 1e6 / plane));
-        int nch = (g.Hx + c - 1) / c;
-        if (const char* ks = std::getenv("VK_RL_KXSTREAMS")) p->kxs = std::max(2, std::min(4, std::atoi(ks)));
-        const char* ke = std::getenv("VK_RL_KXEVEN");
-        if (ke && ke[0] == '1' && nch > 1) {
-          // a multiple of the stream count: the streams' last chunks end together
-          nch = std::min((nch + p->kxs - 1) / p->kxs * p->kxs, g.Hx);  // no empty chunk
-          p->kxn = nch;
-        }
-        p->kxc = nch > 1 ? (g.Hx + nch - 1) / nch : 0;  // balanced chunks
-      }
       if (const char* ks = std::getenv("VK_RL_KXSTREAMS")) p->kxs = std::max(2, std::min(4, std::atoi(ks)));
+      const double sb_mb = (double)g.Hx * g.Pz * g.Wy * 8 / 1e6;
+      int nch = 0;
+      if (kc) {
+        const double mb = std::atof(kc);
+        if (mb > 0) {
+          const int c = std::max(1, (int)(mb * 1e6 / ((double)g.Pz * g.Wy * 8)));
+          nch = (g.Hx + c - 1) / c;
+        }
+      } else if (sb_mb > 64.0) {
+        nch = (int)std::lround((double)g.Hx * ((g.Wy + 15) / 16) / 1250.0);
+      }
+      if (nch > 1) {
+        nch = std::max(p->kxs, (int)std::lround((double)nch / p->kxs) * p->kxs);
+        nch = std::min(nch, g.Hx);  // no empty chunk
+        p->kxn = nch;
+        p->kxc = (g.Hx + nch - 1) / nch;  // ring slot: the largest chunk
+      }
       if (p->kxc) {
         p->ring2.alloc((size_t)p->kxs * p->kxc * g.Pz * g.Wy, "S_B ring");
         for (int k = 0; k < p->kxs; ++k)
