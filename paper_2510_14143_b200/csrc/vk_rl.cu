@@ -601,7 +601,7 @@ struct vk_rl_plan_s {
   // kx-chunked y/z convolution (conv_yz_chunked): chunks of kxc planes run
   // y-forward -> z -> y-inverse through a ring slot (one per stream) small
   // enough to stay L2-resident, so S_B does not make HBM round trips
-  int kxc = 0, kxs = 2;  // planes per chunk, streams (= ring slots)
+  int kxc = 0, kxs = 3;  // planes per chunk, streams (= ring slots)
   int kxn = 0;           // chunks; boundaries kx0 = c * Hx / kxn (sizes differ by <= 1)
   size_t ring_window = 0;  // bytes of ring2 under a persisting L2 access window (0: none)
   DevBuf<float2> ring2;
@@ -1566,10 +1566,11 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
     // kx-chunked y/z convolution where S_B does not fit L2 anyway (> 64 MB);
     // small volumes (C1/C3, S_B 26 MB) keep the whole-volume passes.  Chunk
     // count: a multiple of the stream count (the streams' last chunks end
-    // together: C4 +1.0%) near Hx * ceil(Wy/16) / 1250, i.e. ~1250 z-tile CTAs
-    // per chunk -- the optimum of both measured grids (C2: 8 chunks of 36-37
-    // planes, 3.72e10 vs 3.69e10 / 3.60e10 at 10 / 6 chunks; C4: 30 chunks of
-    // 18, 3.589e10 vs 3.571e10 / 3.557e10 at 38 / 24: profiles/r02/kxchunk_even_ab.txt).
+    // together: C4 +1.0%) near Hx * ceil(Wy/16) / T z-tile CTAs per chunk,
+    // T = 1250 on 2 streams (C2: 8 chunks, 3.72e10 vs 3.69e10 / 3.60e10 at
+    // 10 / 6; C4: 30 chunks, 3.589e10 vs 3.571e10 / 3.557e10 at 38 / 24) and
+    // 650 on 3 (C2 15 chunks: +0.4 to +1.0% over 2 streams; C4 57: equal):
+    // profiles/r02/kxchunk_even_ab.txt.  3 streams by default.
     // VK_RL_KXCHUNK = target MB of S_B per chunk instead (0 = whole volume).
     if (p->ztma && !conv && !zslab) {
       const char* kc = std::getenv("VK_RL_KXCHUNK");
@@ -1583,7 +1584,10 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
           nch = (g.Hx + c - 1) / c;
         }
       } else if (sb_mb > 64.0) {
-        nch = (int)std::lround((double)g.Hx * ((g.Wy + 15) / 16) / 1250.0);
+        // z-tile CTAs per chunk: 1250 on 2 streams, 650 on 3 (C2 sweep:
+        // 15 chunks of 19 planes on 3 streams), 500 on 4
+        const double per = p->kxs == 2 ? 1250.0 : p->kxs == 3 ? 650.0 : 500.0;
+        nch = (int)std::lround((double)g.Hx * ((g.Wy + 15) / 16) / per);
       }
       if (nch > 1) {
         nch = std::max(p->kxs, (int)std::lround((double)nch / p->kxs) * p->kxs);
