@@ -59,11 +59,26 @@ for rep, out in (("prof_x.ncu-rep", "ncu_full_c2_xpass.md"), ("prof_yz.ncu-rep",
         summary([os.path.join(SRC, rep)], out)
 
 
-def iter_traffic(path, iters):
+def iter_traffic(path):
+    """DRAM bytes and kernel time per RL iteration from an ncu --metrics CSV:
+    only whole iterations are counted, from the first x-pass launch of the
+    window to the last one that starts an iteration (2 x passes each)."""
     txt = open(path).read()
-    body = txt[txt.index('"ID"'):]
+    rows = list(csv.DictReader(io.StringIO(txt[txt.index('"ID"'):])))
+    ids = []
+    for row in rows:
+        if row["ID"] not in ids:
+            ids.append(row["ID"])
+    name = {row["ID"]: row["Kernel Name"] for row in rows}
+    xs = [i for i in ids if "xpass" in name[i]]
+    iters = (len(xs) - 1) // 2
+    if iters < 1:
+        return None, 0, 0, 0
+    keep = set(ids[ids.index(xs[0]):ids.index(xs[2 * iters])])
     acc = collections.defaultdict(float)
-    for row in csv.DictReader(io.StringIO(body)):
+    for row in rows:
+        if row["ID"] not in keep:
+            continue
         k = row["Kernel Name"]
         kind = "x" if "xpass" in k else "y" if "ypass" in k else "z"
         v = float(row["Metric Value"].replace(",", ""))
@@ -76,7 +91,7 @@ def iter_traffic(path, iters):
         out[kind] = (acc[(kind, "dram__bytes_read.sum")] / iters / 1e6, acc[(kind, "dram__bytes_write.sum")] / iters / 1e6)
     tot = sum(a + b for a, b in out.values()) / 1e3
     t = sum(v for (k, m), v in acc.items() if m == "gpu__time_duration.sum") / iters
-    return out, tot, t
+    return out, tot, t, iters
 
 
 lines = []
@@ -84,12 +99,10 @@ for f, label in (("iter.csv", "kx-chunked y/z (default)"), ("iter_whole.csv", "w
     p = os.path.join(SRC, f)
     if not os.path.exists(p):
         continue
-    # launches per C2 iteration: chunked 2 x + 27 chunks x (2 y + 1 z... ) -> count by the x launches (2 per iteration)
-    txt = open(p).read()
-    nx = sum(1 for row in csv.DictReader(io.StringIO(txt[txt.index('"ID"'):]))
-             if "xpass" in row["Kernel Name"] and row["Metric Name"] == "gpu__time_duration.sum")
-    iters = max(1, nx // 2)
-    out, tot, t = iter_traffic(p, iters)
+    out, tot, t, iters = iter_traffic(p)
+    if out is None:
+        print(f"{f}: fewer than one whole iteration in the window")
+        continue
     lines.append(f"| {label} | {out['x'][0]:.0f} / {out['x'][1]:.0f} MB | {out['y'][0]:.0f} / {out['y'][1]:.0f} MB | "
                  f"{out['z'][0]:.0f} / {out['z'][1]:.0f} MB | **{tot:.2f} GB** | {t:.3f} ms | {iters} |")
 if lines:
