@@ -470,16 +470,10 @@ struct Staging {
     const char* e = std::getenv("VK_RL_STAGE_SLOTS");
     return e ? std::max(2, std::min(kMaxSlots, std::atoi(e))) : 4;
   }();
-  const char* const kChunkEnv = std::getenv("VK_RL_STAGE_MB");
-  const size_t kChunk = (size_t)(kChunkEnv ? std::max(1, std::atoi(kChunkEnv)) : 16) << 20;
-  // A transfer of one or two chunks cannot overlap its host copy with its
-  // DMA; split it in two (>= 8 MB each): C1's 16 MB volume 3.96-4.09 vs
-  // 4.08-4.20 ms end to end (profiles/r02/staging_dma.md)
-  size_t chunk_for(size_t bytes) const {
-    if (kChunkEnv) return kChunk;
-    const size_t half = ((bytes / 2) + (1 << 20) - 1) & ~(size_t)((1 << 20) - 1);
-    return std::min(kChunk, std::max((size_t)8 << 20, half));
-  }
+  const size_t kChunk = [] {
+    const char* e = std::getenv("VK_RL_STAGE_MB");
+    return (size_t)(e ? std::max(1, std::atoi(e)) : 16) << 20;
+  }();
   void* h[kMaxSlots]{};
   cudaEvent_t ev[kMaxSlots]{};
   ~Staging() {
@@ -505,7 +499,7 @@ struct Staging {
     const bool tm = timing_on();
     std::vector<cudaEvent_t> te;  // VK_RL_TIMING: per-chunk DMA times
     std::vector<double> cpy;
-    const size_t cs = chunk_for(bytes);
+    const size_t cs = kChunk;
     size_t off = 0;
     for (int c = 0; off < bytes; ++c, off += cs) {
       const int k = c % kSlots;
@@ -546,7 +540,7 @@ struct Staging {
       return;
     }
     ensure();
-    const size_t cs = chunk_for(bytes);
+    const size_t cs = kChunk;
     const int nc = (int)((bytes + cs - 1) / cs);
     auto issue = [&](int c) {
       const int k = c % kSlots;
