@@ -104,9 +104,6 @@ __device__ __forceinline__ void tma_load_3d(void* smem_dst, const CUtensorMap* m
 // the next one launch as soon as all of its CTAs are resident (the next
 // grid's CTAs then fill the SMs our tail wave frees), and waits for the
 // previous grid to complete and flush before touching its results.
-#ifndef VK_PDL_LATE
-#define VK_PDL_LATE 0  // experiment: y/z TMA passes trigger their dependents after the transforms
-#endif
 __device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
 __device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
 
@@ -774,9 +771,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   if (!TWG) reg::load_twiddles2<R1, R2>(tw, ta.z.plan.tw);
   const float2* twp = TWG ? ta.z.plan.tw2 : tw;
   __syncthreads();
-#if !VK_PDL_LATE
   pdl_trigger();
-#endif
   pdl_wait();
   if (threadIdx.x == 0) {
     mbar_expect_tx(&bar, (unsigned)(n_in * L * sizeof(float2)));
@@ -819,9 +814,6 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, 16, true>::NT, MINB == 1 ? 0 :
   }
   __syncthreads();
   reg::fft2<R1, R2, L, NT, true, L, TWG>(A, twp);
-#if VK_PDL_LATE
-  pdl_trigger();
-#endif
   if (ta.tma_store) {  // rows [out_off, out_off+n_out) of the tile ARE the box (n_out = Pz): one TMA store
     fence_proxy_async_smem();
     __syncthreads();
@@ -876,9 +868,7 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
   if (!TWG) reg::load_twiddles2<R1, R2>(tw, a.plan.tw);
   const float2* twp = TWG ? a.plan.tw2 : tw;
   __syncthreads();
-#if !VK_PDL_LATE
   pdl_trigger();
-#endif
   pdl_wait();
   const int nvalid = min(L, a.nlines - line0);
   if (threadIdx.x == 0) {
@@ -923,9 +913,6 @@ __global__ void __launch_bounds__(FastCfg<R1, R2, L, true>::NT) ypass_tma(const 
       reg::fft2<R1, R2, L, NT, true, 1, TWG, NP>(A, twp);
     }
   }
-#if VK_PDL_LATE
-  pdl_trigger();
-#endif
   if (a.bst) {  // 16-byte aligned output lines: one bulk store per line
     fence_proxy_async_smem();
     __syncthreads();
