@@ -63,12 +63,29 @@ CONFIGS = {
     "c5": dict(image=(2048, 2048), psf=("gaussian", 31, 3.75), iters=25,
                volumes=4096,
                label="C5: batch of 4096 fields 2048x2048 f32, 31^2 Gaussian PSF (sigma 3.75), 25 RL iterations"),
+    # the paper's own deconvolution volume (reference PAPER.md:406,429: image and
+    # PSF both 30x2160x2560): W = 90x6480x7680, not a BASELINE config; the CPU
+    # reference would take hours per iteration and is not run (no_cpu)
+    "paper": dict(image=(30, 2160, 2560), psf=("widefield_full", (30, 2160, 2560), None), iters=5, no_cpu=True,
+                  e2e_steps=0,
+                  label="Paper volume: 30x2160x2560 f32, same-size widefield PSF (PAPER.md:429), 5 RL iterations"),
 }
 
 
 def make_psf(kind, k, sigma, rank):
     """PSFs of SURVEY.md §8(d); same formulas as oracle/rl_oracle.py (restated
     here so the product bench does not import the oracle)."""
+    if kind == "widefield_full":  # the widefield planes on a k = (Kz, Ky, Kx) grid
+        kz, ky, kx = k
+        dz = np.arange(kz, dtype=np.float64) - kz // 2
+        gy = np.arange(ky, dtype=np.float64) - ky // 2
+        gx = np.arange(kx, dtype=np.float64) - kx // 2
+        out = np.zeros(k, np.float32)
+        for i, z in enumerate(dz):
+            sg = 1.5 * math.sqrt(1.0 + ((z * (1.0 + 0.15 * np.sign(z))) / 4.0) ** 2)
+            plane = np.multiply.outer(np.exp(-0.5 * (gy / sg) ** 2), np.exp(-0.5 * (gx / sg) ** 2))
+            out[i] = (plane / plane.sum() * math.exp(-abs(z) / 8.0)).astype(np.float32)
+        return out / np.float32(out.astype(np.float64).sum())
     if kind == "widefield":
         h = k // 2
         d = np.arange(-h, h + 1, dtype=np.float64)
@@ -105,10 +122,11 @@ def good_size(n: int) -> int:
 def config_dict(cfg, ws, n_batch):
     """The workload record both arms print (identical keys and values)."""
     shape, k = cfg["image"], cfg["psf"][1]
-    padded = [s + 2 * (k // 2) for s in shape]
+    ks = list(k) if isinstance(k, tuple) else [k] * len(shape)
+    padded = [s + 2 * (kk // 2) for s, kk in zip(shape, ks)]
     return {"workload": cfg["label"] + (" per GPU" if ws > 1 and not n_batch else ""), "image": list(shape),
-            "psf": [k] * len(shape), "iters_per_step": cfg["iters"], "volumes": n_batch or ws,
-            "fft_shape": [good_size(p + k - 1) for p in padded], "padded_domain": padded,
+            "psf": ks, "iters_per_step": cfg["iters"], "volumes": n_batch or ws,
+            "fft_shape": [good_size(p + kk - 1) for p, kk in zip(padded, ks)], "padded_domain": padded,
             "parallelism": (f"volume blocks over {ws} ranks" if n_batch else f"independent volumes x{ws}"),
             "l2": "inputs larger than L2" if int(np.prod(shape)) * 4 > 126e6 or n_batch else
                   "single volume partly L2-resident (126 MB L2)"}
@@ -257,6 +275,10 @@ def synth_host(shape, seed):
 
 def run_reference_arm(args, cfg, ws, rank):
     if rank != 0:
+        return
+    if cfg.get("no_cpu"):
+        print(json.dumps({"impl": "reference", "unavailable": "the reference on this grid takes hours per iteration"}),
+              flush=True)
         return
     shape = cfg["image"]
     psf = make_psf(*cfg["psf"], rank=len(shape))
@@ -424,7 +446,7 @@ def main():
     # ---- end-to-end through the reference-facing one-shot call ----------------
     # deconv::richardson_lucy[_batch] = vk_richardson_lucy[_batch]: pageable
     # numpy arrays in and out, host staging, the plan from the call's cache
-    e2e_steps = args.e2e_steps if args.e2e_steps is not None else max(1, min(args.steps, 5))
+    e2e_steps = args.e2e_steps if args.e2e_steps is not None else cfg.get("e2e_steps", max(1, min(args.steps, 5)))
     e2e_value = None
     e2e_vols = 0
     first_call_ms = None
@@ -512,7 +534,10 @@ def main():
     }
     if gathered:
         line["results_gather"] = gathered
-    if rank == 0 and ws == 1 and not args.no_cpu_baseline:
+    if rank == 0 and ws == 1 and cfg.get("no_cpu"):
+        line["cpu_baseline"] = {"value": None, "unit": UNIT, "cores": host_cores(), "kind": "reference",
+                                "sample": "not run: the reference on this grid takes hours per iteration"}
+    elif rank == 0 and ws == 1 and not args.no_cpu_baseline:
         try:
             host_obs = obs.cpu().numpy()
             t0 = time.perf_counter()

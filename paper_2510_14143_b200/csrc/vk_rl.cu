@@ -1590,6 +1590,10 @@ vk_rl_plan create_plan(int device, int rank, const uint64_t* shape, int psf_rank
         // 15 chunks of 19 planes on 3 streams), 500 on 4
         const double per = p->kxs == 2 ? 1250.0 : p->kxs == 3 ? 650.0 : 500.0;
         nch = (int)std::lround((double)g.Hx * ((g.Wy + 15) / 16) / per);
+        // at most 64 chunks: the paper's 90x6480x7680 grid would otherwise
+        // get 2394 chunks of 2 planes (5.57e8 vs 6.03e8 voxel-iters/s with 60,
+        // profiles/r02/paper_volume.md)
+        nch = std::min(nch, 64);
       }
       if (nch > 1) {
         nch = std::max(p->kxs, (int)std::lround((double)nch / p->kxs) * p->kxs);
