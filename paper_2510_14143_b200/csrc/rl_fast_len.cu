@@ -26,7 +26,11 @@ FastEntry fast_entry_256() { return make_entry<16, 16, 16, 16, false, true, 1, f
 // x pass with a 3-CTA register floor: the packed complex arithmetic took the
 // staged kernel from 72 to 75 registers, i.e. from 3 to 2 resident CTAs
 // (C1 x passes +13%, profiles/r02/final)
-FastEntry fast_entry_288() { return make_entry<16, 18, 16, 16, false, true, 3, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
+// 8 lines per CTA (1326 CTAs on the C1 grid instead of 702 at 3 per SM, i.e.
+// ~1.5 waves at 6 per SM instead of 1.6 at 3 with a 58%-full tail): C1 +2.0%,
+// C3 +1.8% (profiles/r02/x288_l8_ab.txt; a 5-CTA register floor without
+// the 32-byte stack measured the same).
+FastEntry fast_entry_288() { return make_entry<16, 18, 8, 16, false, true, 6, false, false, true, 1, true, 2, 8, 0, true, true>(); }  // 288 (y: bulk, L=8)
 #elif VK_LEN == 576
 #if defined(VK_X576_VARIANT) && VK_X576_VARIANT == 1  // experiment: 16-line x pass (32 rows, 256-byte pieces), 2 CTAs/SM
 FastEntry fast_entry_576() { return make_entry<24, 24, 16, 8, true, true, 2, false, false, true, 1, true, 2, 8, 0, true>(); }
