@@ -43,6 +43,8 @@ FastEntry fast_entry_576() { return make_entry<24, 24, 8, 8, true, true, 5, fals
 // 1080: TMA-staged x pass with a 2-CTA register floor (96 regs, 80 B stack;
 // without the floor the staged loads take 129 registers and 1 CTA/SM): C4
 // 2.884 vs 2.940 ms per iteration (profiles/r01/final/x1080.log)
+// y pass: 4 lines per CTA (C4 3.59e10; 2 lines 3.47e10, 8 lines 3.11e10:
+// profiles/r02/y1080_lines_ab.txt)
 FastEntry fast_entry_1080() { return make_entry<30, 36, 8, 4, false, true, 2, true, false, true, 1, true, 2, 4, 0, true, true>(); }  // 1080 (Ix = 1000: partial chunks are common)
 #elif VK_LEN == 2160
 // 2160: no smem twiddles / OTF tile -> 2 CTAs per SM; no PDL (CTAs parked
